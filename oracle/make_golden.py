@@ -1,0 +1,146 @@
+"""Generate tests/golden/*.npz by running the REFERENCE implementation.
+
+TEST INFRASTRUCTURE ONLY.  Run in the build container (where the read-only
+reference lives at /root/reference); the GPU box never runs this, it only
+reads the committed fixtures:
+
+    python oracle/make_golden.py
+
+Every fixture is produced through the reference's own public API
+(`mcstokes.mesh`, `dofmap.FeSystem`, `assembly.assemble_element_blocks`,
+`condensation.condense_sigma_omega` / `double_schur`,
+`preconditioners.*`, `driver.velocity_preconditioner`, `krylov.cg`), on the
+seeded inputs of `paper_2207_08481_b200.problems` (SURVEY §8d protocol).
+"""
+
+from __future__ import annotations
+
+import os
+import sys
+
+import numpy as np
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+ROOT = os.path.dirname(HERE)
+REF = os.environ.get("MCS_REFERENCE_SRC", "/root/reference/pkg/src")
+OUT = os.path.join(ROOT, "tests", "golden")
+
+
+def _ref():
+    sys.path.insert(0, REF)
+    import mcstokes  # noqa: F401
+    from mcstokes import assembly, condensation, dofmap, driver, krylov, mesh
+    from mcstokes import preconditioners as pc
+    return dict(assembly=assembly, condensation=condensation, dofmap=dofmap,
+                driver=driver, krylov=krylov, mesh=mesh, pc=pc)
+
+
+def _csr(prefix, A, out):
+    A = A.tocsr()
+    A.sort_indices()
+    out[prefix + "_data"] = A.data
+    out[prefix + "_indices"] = A.indices.astype(np.int32)
+    out[prefix + "_indptr"] = A.indptr.astype(np.int64)
+    out[prefix + "_shape"] = np.array(A.shape)
+
+
+def case(R, name, cfg, n, with_matrices=True, comps=("additive", "multiplicative")):
+    sys.path.insert(0, ROOT)
+    from paper_2207_08481_b200.problems import baseline_config
+    prob = baseline_config(cfg, n)
+    m = R["mesh"].from_arrays(prob.mesh.vertices, prob.mesh.triangles)
+    eps = 1e-12
+    key = "tilde_neumann" if cfg == 3 else "neumann"
+    regions = R["mesh"].classify_boundary(
+        m, dirichlet=lambda x: x[0] < 1 - eps, **{key: lambda x: x[0] >= 1 - eps})
+    fes = R["dofmap"].FeSystem(m, regions, prob.k)
+    out = dict(k=prob.k, nu=prob.nu, n=n, cfg=cfg)
+    out["vertices"], out["triangles"] = m.vertices, m.triangles
+    for a in ("facets", "facet_tri", "facet_normal", "facet_tangent",
+              "facet_length", "facet_start", "tri_facets"):
+        out["mesh_" + a] = getattr(m, a)
+    out["bdm_coef"], out["sigma_coef"] = fes.bdm.coef, fes.sigma.coef
+    out["v_l2g"], out["v_signs"] = fes.dof_v.loc2glob, fes.dof_v.signs
+    out["h_l2g"], out["h_signs"] = fes.dof_vhat.loc2glob, fes.dof_vhat.signs
+    out["vv_free"], out["vbar_free"] = fes.vv_free, fes.dof_vbar.is_free
+
+    blocks = R["assembly"].all_element_blocks(fes, prob.nu, prob.body_force)
+    if with_matrices:
+        for b in ("msig", "bws", "bus", "bhs", "adiv", "bpu", "load"):
+            out["eb_" + b] = np.array([getattr(eb, b) for eb in blocks])
+    sys_ = R["condensation"].condense_sigma_omega(fes, prob.nu, prob.body_force,
+                                                  blocks=blocks)
+    R["condensation"].double_schur(sys_)
+    if with_matrices:
+        _csr("S", sys_.S, out)
+        _csr("Sd", sys_.Sd, out)
+        out["ext"] = np.array(sys_.ext)
+        out["soo"] = np.array(sys_.soo_dense)
+        out["recovery"] = np.array(sys_.recovery)
+    out["load_vv"] = sys_.load
+    pc = R["pc"]
+    E = pc.build_embedding(fes)
+    Ec = pc.embedding_cpl(fes, sys_, E)
+    _csr("Ec", Ec, out)
+    coarse = pc.build_coarse(fes, prob.nu, penalty_C=4.0)
+    _csr("coarse", coarse.matrix, out)
+    blocks_s = pc.facet_blocks_schur(fes, sys_)
+    out["fblk_ptr"] = np.cumsum([0] + [len(b) for b in blocks_s])
+    out["fblk_idx"] = np.concatenate(blocks_s)
+
+    free = fes.vv_free
+    S_free = sys_.S[free][:, free].tocsr()
+    rhs_u, _ = R["driver"].condensed_rhs(fes, sys_)
+    out["rhs_u"] = rhs_u
+    rng = np.random.default_rng(11)
+    v = rng.standard_normal(S_free.shape[0])
+    out["probe_v"] = v
+    out["probe_Sv"] = S_free @ v
+    for comp in comps:
+        opts = R["driver"].SolverOptions(mode="elliptic", target="Sd",
+                                         smoother="jacobi", composition=comp,
+                                         rtol=1e-8, maxit=2000)
+        M = R["driver"].velocity_preconditioner(fes, sys_, prob.nu, opts)
+        out[f"probe_M_{comp}"] = M(v)
+        x, rep = R["krylov"].cg(lambda u: S_free @ u, rhs_u, M, rtol=1e-8, maxit=2000)
+        out[f"cg_{comp}_iters"] = rep.iterations
+        out[f"cg_{comp}_res"] = np.array(rep.residuals)
+        out[f"cg_{comp}_x"] = x
+        # the multiplicative composition's power-iteration scale
+        free_cpl = sys_.free_mask_cpl()
+        A = sys_.Sd[free_cpl][:, free_cpl].tocsr()
+        sm = pc.FacetBlockSmoother(A, blocks_s, "jacobi")
+        asp = pc.AspPreconditioner(A, sm, Ec, coarse, comp, 1)
+        out[f"jacobi_scale_{comp}"] = asp.jacobi_scale
+    path = os.path.join(OUT, name + ".npz")
+    np.savez_compressed(path, **out)
+    print(f"{path}: {os.path.getsize(path) / 1e3:.0f} kB, cg iters",
+          {c: int(out[f'cg_{c}_iters']) for c in comps})
+
+
+def microbench(R):
+    import scipy.linalg as sla
+    sys.path.insert(0, ROOT)
+    from paper_2207_08481_b200.problems import microbench_host
+    A, B = microbench_host(16, seed=3)
+    # the reference idiom of condensation.py:216-224
+    S = np.array([B[i].T @ sla.cho_solve(sla.cho_factor(A[i], check_finite=False),
+                                         B[i], check_finite=False)
+                  for i in range(len(A))])
+    path = os.path.join(OUT, "micro.npz")
+    np.savez_compressed(path, A=A, B=B, S=S)
+    print(path)
+
+
+def main():
+    os.makedirs(OUT, exist_ok=True)
+    R = _ref()
+    case(R, "c1_n2", 1, 2)
+    case(R, "c2_n3", 2, 3)
+    case(R, "c3_n2", 3, 2)
+    case(R, "cfg1", 1, 16, with_matrices=False)
+    microbench(R)
+
+
+if __name__ == "__main__":
+    main()
