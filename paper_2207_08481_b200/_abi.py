@@ -1,0 +1,74 @@
+"""ctypes binding of the C ABI in `include/mcs_abi.h` (libmcsgpu.so).
+
+Every entry point takes device pointers owned by the caller (torch tensors)
+and a `cudaStream_t`; calls are asynchronous on that stream.  Return codes:
+0 ok, <0 CUDA / argument error, >0 first failing element (1-based).  There is
+deliberately NO fallback: if the library is missing or a call fails, the
+product path raises.
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+import os
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libmcsgpu.so")
+
+_p, _i, _l, _d = C.c_void_p, C.c_int, C.c_int64, C.c_double
+
+# name -> argtypes (restype int).  Mirrors include/mcs_abi.h one to one.
+SIGNATURES = {
+    "mcs_spd_schur_batched": [_i, _i, _l, _p, _p, _p, _p, _p],
+    "mcs_record_len": [_i],
+    "mcs_st_stride": [_i],
+    "mcs_condense": [_i, _l, _p, _p, _p, _p],
+    "mcs_element_blocks": [_l, _i, _p, _i, _p, _p, _p, _p, _p],
+}
+
+_lib = None
+
+
+class McsError(RuntimeError):
+    pass
+
+
+def lib():
+    """Load libmcsgpu.so (raises if it is missing: no CPU fallback)."""
+    global _lib
+    if _lib is None:
+        if not os.path.exists(LIB_PATH):
+            raise McsError(f"{LIB_PATH} missing: run `python -m "
+                           "paper_2207_08481_b200.build` (no CPU fallback)")
+        L = C.CDLL(LIB_PATH)
+        for name, args in SIGNATURES.items():
+            fn = getattr(L, name)
+            fn.argtypes = args
+            fn.restype = C.c_int
+        _lib = L
+    return _lib
+
+
+def ptr(t) -> int:
+    """Raw device pointer of a torch tensor (None -> NULL)."""
+    if t is None:
+        return None
+    if not t.is_cuda:
+        raise McsError("expected a CUDA tensor")
+    if not t.is_contiguous():
+        raise McsError("expected a contiguous tensor")
+    return t.data_ptr()
+
+
+def stream(s=None) -> int:
+    import torch
+    s = s if s is not None else torch.cuda.current_stream()
+    return s.cuda_stream
+
+
+def call(name, *args):
+    rc = getattr(lib(), name)(*args)
+    if rc < 0:
+        raise McsError(f"{name} failed with CUDA error {-rc}"
+                       if rc > -1000 else f"{name}: unsupported arguments ({rc})")
+    return rc

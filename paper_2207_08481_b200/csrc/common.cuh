@@ -1,0 +1,78 @@
+// Shared helpers for the MCS condensation / PCG kernels (sm_100a only).
+#pragma once
+#include <cstdint>
+#include <cuda_runtime.h>
+
+#if defined(__CUDA_ARCH__) && (__CUDA_ARCH__ < 1000)
+#error "this library targets sm_100a (B200) only"
+#endif
+
+#define MCS_API extern "C" __attribute__((visibility("default")))
+
+namespace mcs {
+
+// lower-packed, row-major: (i, j) with j <= i  ->  i(i+1)/2 + j
+__host__ __device__ constexpr int pk(int i, int j) { return i * (i + 1) / 2 + j; }
+__host__ __device__ constexpr int npk(int n) { return n * (n + 1) / 2; }
+__host__ __device__ constexpr int even(int n) { return (n + 1) & ~1; }
+
+// local sizes of the MCS element at degree k
+template <int K>
+struct Sizes {
+  static constexpr int k = K;
+  static constexpr int ns = 3 * (K + 1) * (K + 2) / 2 - 3;
+  static constexpr int nw = K * (K + 1) / 2;
+  static constexpr int nu = (K + 1) * (K + 2);
+  static constexpr int nh = 3 * K;
+  static constexpr int nloc = nu + nh;
+  static constexpr int n_em = 3 * (K + 1);
+  static constexpr int n_int = (K + 1) * (K - 1);
+  static constexpr int ncpl = nloc - n_int;
+  static constexpr int naug = ns + nw + nloc;   // augmented saddle size
+};
+
+inline int err_code(cudaError_t e) { return e == cudaSuccess ? 0 : -static_cast<int>(e); }
+
+// Return the pending launch error (if any) as a negative code.
+inline int launch_status() { return err_code(cudaGetLastError()); }
+
+// dof code: 2*index + (sign < 0), or -1 for a constrained dof (reads 0, no write)
+__device__ __forceinline__ double code_sign(int c) { return (c & 1) ? -1.0 : 1.0; }
+__device__ __forceinline__ int code_index(int c) { return c >> 1; }
+
+__device__ __forceinline__ uint32_t smem_addr(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+
+// ---- 1-D bulk async copy (TMA engine, cp.async.bulk) global -> shared ----
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(smem_addr(bar)), "r"(count));
+}
+__device__ __forceinline__ void fence_barrier_init() {
+  asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(smem_addr(bar)),
+               "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n" ::"r"(
+          smem_addr(dst)),
+      "l"(src), "r"(bytes), "r"(smem_addr(bar))
+      : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t phase) {
+  asm volatile(
+      "{\n"
+      ".reg .pred p;\n"
+      "WAIT_%=:\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+      "@!p bra WAIT_%=;\n"
+      "}\n" ::"r"(smem_addr(bar)),
+      "r"(phase)
+      : "memory");
+}
+
+}  // namespace mcs
