@@ -19,11 +19,39 @@ _p, _i, _l, _d = C.c_void_p, C.c_int, C.c_int64, C.c_double
 
 # name -> argtypes (restype int).  Mirrors include/mcs_abi.h one to one.
 SIGNATURES = {
+    # condense.cu
     "mcs_spd_schur_batched": [_i, _i, _l, _p, _p, _p, _p, _p],
     "mcs_record_len": [_i],
     "mcs_st_stride": [_i],
     "mcs_condense": [_i, _l, _p, _p, _p, _p],
     "mcs_element_blocks": [_l, _i, _p, _i, _p, _p, _p, _p, _p],
+    # double_schur.cu
+    "mcs_ext_stride": [_i],
+    "mcs_sd_stride": [_i],
+    "mcs_double_schur": [_i, _l, _p, _p, _p, _p, _p],
+    # apply.cu
+    "mcs_apply_elem": [_i, _i, _l, _p, _p, _p, _p, _l, _p],
+    "mcs_ext_restrict": [_i, _l, _p, _p, _p, _p, _p, _p, _l, _p],
+    "mcs_ext_prolong": [_i, _l, _p, _p, _p, _p, _p, _p, _p],
+    "mcs_gather_sub": [_i, _p, _p, _p, _p, _p],
+    "mcs_scatter": [_i, _p, _p, _p, _p],
+    # precond.cu
+    "mcs_jacobi_setup": [_i, _i, _p, _i, _p, _p, _p, _p, _p, _p, _p],
+    "mcs_jacobi_apply": [_i, _i, _p, _p, _p, _p, _d, _p],
+    "mcs_csr_spmv": [_i, _p, _p, _p, _p, _p, _d, _d, _i, _p],
+    "mcs_dense_gemv": [_i, _p, _p, _p, _p],
+    # coarse.cu
+    "mcs_mf_set_max_own": [_i],
+    "mcs_mf_forward_own": [_i, _p, _p, _p, _p, _p, _p, _p, _p, _p],
+    "mcs_mf_forward_out": [_i, _p, _p, _p, _p, _p, _p, _p],
+    "mcs_mf_backward": [_i, _p, _p, _p, _p, _p, _p, _p, _p],
+    "mcs_mf_backward2": [_i, _p, _p, _p, _p, _p, _p, _p, _p],
+    # blas1.cu
+    "mcs_reduce_workspace_len": [],
+    "mcs_dot": [_l, _p, _p, _p, _p, _p, _p],
+    "mcs_cg_update": [_l, _p, _p, _p, _p, _p, _i, _i, _i, _p, _p, _p],
+    "mcs_xpby": [_l, _p, _p, _p, _i, _i, _p],
+    "mcs_axpby": [_l, _d, _p, _d, _p, _p],
 }
 
 _lib = None

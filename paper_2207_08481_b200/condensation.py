@@ -1,0 +1,218 @@
+"""Drop-in `condense_sigma_omega` / `double_schur` / `CondensedSystem` on B200.
+
+Reference: `condensation.py:26-239`.  Same entry points, same argument
+meaning, same exceptions; the per-element work runs in the CUDA kernels of
+`csrc/condense.cu` (A1 block generation + A3 elimination) and
+`csrc/double_schur.cu` (A4), and the results stay resident in HBM:
+
+  S_T    (nt, st_stride)  packed lower S_T per element
+  ext    (nt, ext_stride) [X | S_oo^-1] per element
+  Sd_T   (nt, sd_stride)  packed lower Sd_T per element
+
+The assembled host CSR matrices the reference exposes (`S`, `Sd`, `B`) and the
+per-element host lists (`ext`, `soo_dense`, `soo_chol`) are materialised
+lazily from the device data only when a caller touches them (tests,
+exports); the solver path never does.
+"""
+
+from __future__ import annotations
+
+from typing import Optional
+
+import numpy as np
+import scipy.sparse as sp
+
+from . import _abi, engine
+from .maps import element_maps, local_splits
+from .refblocks import build_refs, element_weights, load_vectors, local_sizes
+
+
+def _torch():
+    import torch
+    return torch
+
+
+def _assemble(n, l2g, sg, mats):
+    nt, m = l2g.shape
+    vals = mats * sg[:, :, None] * sg[:, None, :]
+    I = np.repeat(l2g, m, axis=1).ravel()
+    J = np.tile(l2g, (1, m)).ravel()
+    return sp.coo_matrix((vals.ravel(), (I, J)), shape=(n, n)).tocsr()
+
+
+class CondensedSystem:
+    """GPU-resident condensed system with the reference's attribute surface."""
+
+    def __init__(self, fes, nu, S_dev, load, maps, refs, records=None):
+        self.fes, self.nu = fes, nu
+        z = local_sizes(fes.k)
+        self.k, self.z = fes.k, z
+        self.S_dev = S_dev                  # (nt, st_stride) float64 cuda
+        self.records = records
+        self.load = load
+        self.maps = maps
+        self.refs = refs
+        self.vv_l2g, self.vv_signs = maps.vv_l2g, maps.vv_signs
+        self.n_cpl_loc = z["ncpl"]
+        self.nloc_u = z["nu"]
+        self.ext_dev = None
+        self.Sd_dev = None
+        self.cpl_of_vv = None
+        self.vv_of_cpl = None
+        self._S = self._Sd = self._B = None
+        self._dev_maps = None
+
+    # -------------------------------------------------------------- indexing
+    @property
+    def n_vv(self):
+        return self.fes.n_vv
+
+    def free_mask_vv(self):
+        return self.fes.vv_free
+
+    def free_mask_cpl(self):
+        return self.fes.vv_free[self.vv_of_cpl]
+
+    def local_vv(self, x_full, t):
+        return x_full[self.vv_l2g[t]] * self.vv_signs[t]
+
+    def _local_splits(self):
+        return local_splits(self.k)
+
+    def dev_maps(self):
+        """int32 device maps used by the operators (built once)."""
+        if self._dev_maps is None:
+            m = self.maps
+            self._dev_maps = dict(
+                vv_codes=engine.to_dev(m.vv_codes),
+                bubble_idx=engine.to_dev(m.bubble_idx),
+                cpl_codes=engine.to_dev(m.cpl_codes),
+                c2v=engine.to_dev(m.cplfree_to_vvfree))
+        return self._dev_maps
+
+    # ------------------------------------------------- lazy host compatibility
+    def S_T_host(self):
+        return engine.unpack_sym(self.S_dev.cpu().numpy(), self.z["nloc"])
+
+    @property
+    def S(self):
+        if self._S is None:
+            self._S = _assemble(self.fes.n_vv, self.vv_l2g, self.vv_signs, self.S_T_host())
+        return self._S
+
+    @property
+    def B(self):
+        if self._B is None:
+            fes = self.fes
+            nt, nu_l = fes.mesh.num_triangles, self.z["nu"]
+            bpu = self.refs.bpu
+            vals = bpu[None] * self.vv_signs[:, None, :nu_l]
+            rows = np.repeat(fes.dof_q.loc2glob, nu_l, axis=1).ravel()
+            cols = np.tile(self.vv_l2g[:, :nu_l], (1, bpu.shape[0])).ravel()
+            self._B = sp.coo_matrix((vals.ravel(), (rows, cols)),
+                                    shape=(fes.dof_q.ndof, fes.n_vv)).tocsr()
+        return self._B
+
+    @property
+    def Sd(self):
+        if self.Sd_dev is None:
+            return None
+        if self._Sd is None:
+            icpl, _ = local_splits(self.k)
+            rows = self.cpl_of_vv[self.vv_l2g[:, icpl]]
+            Sd_T = engine.unpack_sym(self.Sd_dev.cpu().numpy(), self.z["ncpl"])
+            self._Sd = _assemble(len(self.vv_of_cpl), rows, self.vv_signs[:, icpl], Sd_T)
+        return self._Sd
+
+    def _ext_host(self):
+        z = self.z
+        E = self.ext_dev.cpu().numpy()
+        ni, nc = z["n_int"], z["ncpl"]
+        X = E[:, :ni * nc].reshape(-1, ni, nc)
+        Sinv = engine.unpack_sym(E[:, ni * nc:], ni)
+        return X, Sinv
+
+    @property
+    def ext(self):
+        if self.ext_dev is None:
+            return None
+        return list(self._ext_host()[0])
+
+    @property
+    def soo_dense(self):
+        if self.ext_dev is None:
+            return None
+        icpl, iint = local_splits(self.k)
+        S = self.S_T_host()
+        return list(S[:, iint][:, :, iint])
+
+    @property
+    def soo_chol(self):
+        import scipy.linalg as sla
+        if self.ext_dev is None:
+            return None
+        return [sla.cho_factor(s) for s in self.soo_dense]
+
+    @property
+    def recovery(self):
+        raise NotImplementedError(
+            "stress recovery (condensation.py:64-74) is SURVEY §8f row 3, not on "
+            "the GPU path yet")
+
+    def s_energy(self, x_full):
+        return float(x_full @ (self.S @ x_full))
+
+    def check_info(self, info, what):
+        bad = np.flatnonzero(info.cpu().numpy())
+        if len(bad):
+            raise RuntimeError(f"{what} on element {int(bad[0])}")
+
+
+def condense_sigma_omega(fes, nu: float, body_force=None, blocks=None,
+                         stream=None) -> CondensedSystem:
+    """Eliminate (sigma, omega) element-wise on the GPU (reference
+    `condensation.py:136-188`).  `blocks` (a list of ElementBlocks, as the
+    reference accepts) is packed and uploaded; otherwise the blocks are
+    generated on the GPU from the element geometry (refblocks.py)."""
+    torch = _torch()
+    _abi.lib()
+    k = fes.k
+    refs = build_refs(fes)
+    nt = fes.mesh.num_triangles
+    if blocks is not None:
+        arr = lambda name: np.array([getattr(b, name) for b in blocks])
+        rec_h = engine.pack_records(k, arr("msig"), arr("bws"), arr("bus"),
+                                    arr("bhs"), arr("adiv"))
+        records = engine.to_dev(rec_h)
+        loads = np.array([b.load for b in blocks])
+    else:
+        W = engine.to_dev(element_weights(fes, nu))
+        prog = [engine.to_dev(a) for a in engine.block_program(refs)]
+        records = engine.element_records(nt, W, prog, k, stream=stream)
+        loads = load_vectors(fes, refs, body_force)
+    S_dev, info = engine.condense(k, records, stream=stream)
+    maps = element_maps(fes)
+    load = np.zeros(fes.n_vv)
+    nu_l = refs.bus_vol.shape[0]
+    np.add.at(load, maps.vv_l2g[:, :nu_l].ravel(),
+              (loads * maps.vv_signs[:, :nu_l]).ravel())
+    sys_ = CondensedSystem(fes, nu, S_dev, load, maps, refs, records)
+    sys_.check_info(info, "singular local stress block")
+    return sys_
+
+
+def double_schur(sys_: CondensedSystem, stream=None) -> CondensedSystem:
+    """Eliminate interior bubbles per element on the GPU (reference
+    `condensation.py:191-239`); mutates and returns `sys_`."""
+    torch = _torch()
+    k = sys_.k
+    nt = sys_.S_dev.shape[0]
+    ext = torch.empty((nt, _abi.call("mcs_ext_stride", k)), dtype=torch.float64, device="cuda")
+    Sd = torch.empty((nt, _abi.call("mcs_sd_stride", k)), dtype=torch.float64, device="cuda")
+    info = torch.empty(nt, dtype=torch.int32, device="cuda")
+    _abi.call("mcs_double_schur", k, nt, _abi.ptr(sys_.S_dev), _abi.ptr(ext), _abi.ptr(Sd),
+              _abi.ptr(info), _abi.stream(stream))
+    sys_.ext_dev, sys_.Sd_dev = ext, Sd
+    sys_.vv_of_cpl, sys_.cpl_of_vv = sys_.maps.vv_of_cpl, sys_.maps.cpl_of_vv
+    sys_.check_info(info, "interior velocity block not SPD")
+    return sys_

@@ -1,0 +1,140 @@
+// PCG vector algebra (krylov.py:103-137).
+//
+// Scalars stay on the device (`sc[]`): alpha = rz/pAp and beta = rz_new/rz
+// are formed inside the kernels that consume them, so one iteration needs a
+// single 16-byte device->host read (pAp, ||r||^2) for the reference's
+// stopping test and negative-curvature check.  Reductions are deterministic:
+// a fixed grid, fixed per-thread strides, a fixed shuffle tree per block and
+// the last-arriving block summing the block partials in index order.
+#include "common.cuh"
+
+namespace mcs {
+
+constexpr int RED_BLOCKS = 296;  // 2 x 148 SMs
+constexpr int RED_THREADS = 256;
+
+__device__ __forceinline__ double block_sum(double v) {
+  __shared__ double ws[RED_THREADS / 32];
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_down_sync(0xffffffffu, v, o);
+  const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
+  if (l == 0) ws[w] = v;
+  __syncthreads();
+  double s = 0.0;
+  if (w == 0) {
+    s = l < RED_THREADS / 32 ? ws[l] : 0.0;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) s += __shfl_down_sync(0xffffffffu, s, o);
+  }
+  return s;  // valid in thread 0
+}
+
+// last block: sum partials[0..RED_BLOCKS) in order -> *out
+__device__ __forceinline__ void finish(double part, double* partials, unsigned* counter,
+                                       double* out) {
+  __shared__ bool last;
+  if (threadIdx.x == 0) {
+    partials[blockIdx.x] = part;
+    __threadfence();
+    last = atomicAdd(counter, 1u) == gridDim.x - 1;
+  }
+  __syncthreads();
+  if (!last) return;
+  __threadfence();
+  if (threadIdx.x < 32) {
+    double s = 0.0;
+    for (int b = threadIdx.x; b < (int)gridDim.x; b += 32) s += ((volatile double*)partials)[b];
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) s += __shfl_down_sync(0xffffffffu, s, o);
+    if (threadIdx.x == 0) {
+      *out = s;
+      *counter = 0u;
+    }
+  }
+}
+
+__global__ void __launch_bounds__(RED_THREADS)
+    dot_kernel(int64_t n, const double* __restrict__ x, const double* __restrict__ y,
+               double* partials, unsigned* counter, double* out) {
+  double s = 0.0;
+  for (int64_t i = (int64_t)blockIdx.x * RED_THREADS + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * RED_THREADS)
+    s = fma(x[i], y[i], s);
+  s = block_sum(s);
+  finish(s, partials, counter, out);
+}
+
+// alpha = sc[rz]/sc[pap];  x += alpha p;  r -= alpha Ap;  sc[rr] = r.r
+__global__ void __launch_bounds__(RED_THREADS)
+    cg_update_kernel(int64_t n, double* __restrict__ x, double* __restrict__ r,
+                     const double* __restrict__ p, const double* __restrict__ Ap, double* sc,
+                     int rz, int pap, int rr, double* partials, unsigned* counter) {
+  const double alpha = sc[rz] / sc[pap];
+  double s = 0.0;
+  for (int64_t i = (int64_t)blockIdx.x * RED_THREADS + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * RED_THREADS) {
+    x[i] = fma(alpha, p[i], x[i]);
+    const double ri = fma(-alpha, Ap[i], r[i]);
+    r[i] = ri;
+    s = fma(ri, ri, s);
+  }
+  s = block_sum(s);
+  finish(s, partials, counter, sc + rr);
+}
+
+// p = z + (sc[num]/sc[den]) p
+__global__ void xpby_kernel(int64_t n, const double* __restrict__ z, double* __restrict__ p,
+                            const double* sc, int num, int den) {
+  const double beta = sc[num] / sc[den];
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x)
+    p[i] = fma(beta, p[i], z[i]);
+}
+
+// y = a x + b y
+__global__ void axpby_kernel(int64_t n, double a, const double* __restrict__ x, double b,
+                             double* __restrict__ y) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x)
+    y[i] = b == 0.0 ? a * x[i] : fma(a, x[i], b * y[i]);
+}
+
+static int grid_for(int64_t n) {
+  const int64_t g = (n + 255) / 256;
+  return (int)(g < 4 * 148 ? (g < 1 ? 1 : g) : 4 * 148);
+}
+
+}  // namespace mcs
+
+using namespace mcs;
+
+MCS_API int mcs_reduce_workspace_len() { return RED_BLOCKS; }
+
+MCS_API int mcs_dot(int64_t n, const double* x, const double* y, double* partials, unsigned* counter,
+                    double* out, void* stream) {
+  auto st = static_cast<cudaStream_t>(stream);
+  dot_kernel<<<RED_BLOCKS, RED_THREADS, 0, st>>>(n, x, y, partials, counter, out);
+  return launch_status();
+}
+
+MCS_API int mcs_cg_update(int64_t n, double* x, double* r, const double* p, const double* Ap, double* sc,
+                          int rz, int pap, int rr, double* partials, unsigned* counter, void* stream) {
+  auto st = static_cast<cudaStream_t>(stream);
+  cg_update_kernel<<<RED_BLOCKS, RED_THREADS, 0, st>>>(n, x, r, p, Ap, sc, rz, pap, rr, partials,
+                                                      counter);
+  return launch_status();
+}
+
+MCS_API int mcs_xpby(int64_t n, const double* z, double* p, const double* sc, int num, int den,
+                     void* stream) {
+  auto st = static_cast<cudaStream_t>(stream);
+  xpby_kernel<<<grid_for(n), 256, 0, st>>>(n, z, p, sc, num, den);
+  return launch_status();
+}
+
+MCS_API int mcs_axpby(int64_t n, double a, const double* x, double b, double* y, void* stream) {
+  if (n <= 0) return 0;
+  auto st = static_cast<cudaStream_t>(stream);
+  axpby_kernel<<<grid_for(n), 256, 0, st>>>(n, a, x, b, y);
+  return launch_status();
+}

@@ -1,0 +1,371 @@
+"""Drop-in auxiliary-space preconditioner for the condensed velocity block.
+
+Reference: `preconditioners.py:27-378` with `driver.py:82-102`.  The GPU path
+covers the north-star configuration: target "Sd", smoother "jacobi",
+composition "additive" or "multiplicative" (any `steps`).  Gauss-Seidel and
+l1 are sequential / out of scope and are rejected with the
+reference's exception types.
+
+Per application everything runs in CUDA kernels on free-dof vectors:
+  ExtendedAsp   mcs_ext_restrict -> mcs_gather_sub -> inner -> mcs_scatter
+                -> mcs_ext_prolong                                   (A8)
+  Jacobi        mcs_jacobi_apply over SoA packed facet-block inverses (A9)
+  E_c, E_c^T    mcs_csr_spmv (transpose stored explicitly)           (A10)
+  coarse        exact: dense inverse (small) or multifrontal (A11)
+  S_d apply     mcs_apply_elem (multiplicative composition)          (A6)
+Host work is setup only (index maps, E_c, the P1 coarse matrix and its
+exact factorisation).
+"""
+
+from __future__ import annotations
+
+from dataclasses import dataclass
+from typing import List
+
+import numpy as np
+import scipy.sparse as sp
+
+from . import _abi, engine
+from .basis import shifted_legendre
+from .coarse import CoarseSolver, factorize_coarse
+from .maps import facet_slots, free_index
+from .operators import SdOperator, as_device, axpby, empty, workspace
+
+
+# ----------------------------------------------------------------- embedding
+
+def _facet_moments(fes):
+    """m[iv, q] = int_0^1 hat_iv L_q over the edge rule (hat_0 = 1-s)."""
+    qe = fes.quad_edge
+    leg = shifted_legendre(fes.k, qe.points)
+    hat = np.vstack([1.0 - qe.points, qe.points])
+    return np.array([[np.sum(qe.weights * hat[iv] * leg[q]) for q in range(fes.k + 1)]
+                     for iv in range(2)])
+
+
+def embedding_facet_coo(fes):
+    """Facet rows of E (reference `preconditioners.py:40-63`), vectorised:
+    V normal moments |F| m[iv,q] n_F[c] and Vhat tangential moments
+    m[iv,q] t_F[c] (zero rows on Gamma_Ntilde)."""
+    m, k = fes.mesh, fes.k
+    nf = m.num_facets
+    mom = _facet_moments(fes)
+    ends = np.stack([m.facet_start, m.facet_end()], axis=1)       # (nf, 2)
+    rows, cols, vals = [], [], []
+    F = np.arange(nf)
+    for iv in range(2):
+        for q in range(k + 1):
+            mv = m.facet_length * mom[iv, q]
+            keep = np.abs(mv) >= 1e-15
+            for c in range(2):
+                rows.append(F[keep] * (k + 1) + q)
+                cols.append(2 * ends[keep, iv] + c)
+                vals.append(mv[keep] * m.facet_normal[keep, c])
+        tilde = np.zeros(nf, dtype=bool)
+        tilde[list(fes.regions.tilde_neumann_facets)] = True
+        for q in range(k):
+            if abs(mom[iv, q]) < 1e-15:
+                continue
+            keep = ~tilde
+            for c in range(2):
+                rows.append(fes.n_v + F[keep] * k + q)
+                cols.append(2 * ends[keep, iv] + c)
+                vals.append(mom[iv, q] * m.facet_tangent[keep, c])
+    return np.concatenate(rows), np.concatenate(cols), np.concatenate(vals)
+
+
+def _interior_coo(fes, Ef):
+    """Interior bubble rows of E (reference `preconditioners.py:66-91`):
+    per element the L2 fit of the P1 field against the facet part,
+    vectorised over elements with batched solves."""
+    k = fes.k
+    n_em, n_int = 3 * (k + 1), (k + 1) * (k - 1)
+    w = fes.quad_tri.weights
+    U = fes.tab_u                                                 # (nu, nq, 2)
+    JtJ = np.einsum("tci,tcj->tij", fes.J, fes.J)
+    G = np.einsum("upi,p,vpj->ijuv", U, w, U)                     # (2,2,nu,nu)
+    gram = np.einsum("tij,ijuv->tuv", JtJ, G) / fes.detJ[:, None, None]
+    lam = np.stack([1 - fes.quad_tri.points[:, 0] - fes.quad_tri.points[:, 1],
+                    fes.quad_tri.points[:, 0], fes.quad_tri.points[:, 1]])
+    Mref = np.einsum("upj,p,lp->ulj", U[n_em:], w, lam)            # (n_int,3,2)
+    mom = np.einsum("tcj,ulj->tulc", fes.J, Mref)                 # (nt,n_int,3,2)
+    lg = fes.dof_v.loc2glob[:, :n_em]
+    sg = fes.dof_v.signs[:, :n_em]
+    tri = fes.mesh.triangles
+    nt = len(tri)
+    rows, cols, vals = [], [], []
+    gii, gie = gram[:, n_em:, n_em:], gram[:, n_em:, :n_em]
+    for lv in range(3):
+        v = tri[:, lv]
+        for c in range(2):
+            col = 2 * v + c
+            ced = np.asarray(Ef[lg.ravel(), np.repeat(col, n_em)]).reshape(nt, n_em) * sg
+            rhs = mom[:, :, lv, c] - np.einsum("tie,te->ti", gie, ced)
+            cint = np.linalg.solve(gii, rhs[:, :, None])[:, :, 0]
+            keep = np.abs(cint) > 1e-14
+            tt, ii = np.nonzero(keep)
+            rows.append(fes.dof_v.loc2glob[tt, n_em + ii])
+            cols.append(col[tt])
+            vals.append(cint[keep])
+    return np.concatenate(rows), np.concatenate(cols), np.concatenate(vals)
+
+
+def build_embedding(fes, interior: bool = True) -> sp.csr_matrix:
+    """E: Vbar -> (V, Vhat) (reference `preconditioners.py:27-94`)."""
+    r, c, v = embedding_facet_coo(fes)
+    shape = (fes.n_vv, fes.dof_vbar.ndof)
+    Ef = sp.coo_matrix((v, (r, c)), shape=shape).tocsr()
+    if not interior:
+        return Ef
+    ri, ci, vi = _interior_coo(fes, Ef)
+    return sp.coo_matrix((np.concatenate([v, vi]), (np.concatenate([r, ri]),
+                          np.concatenate([c, ci]))), shape=shape).tocsr()
+
+
+def embedding_free(fes, E):
+    return E[fes.vv_free][:, fes.dof_vbar.is_free].tocsr()
+
+
+def embedding_cpl(fes, sys_, E=None) -> sp.csr_matrix:
+    """E restricted to free coupling rows and free P1 columns
+    (reference `preconditioners.py:101-105`).  Only facet rows survive, so
+    E may be the facet-only embedding."""
+    if E is None:
+        E = build_embedding(fes, interior=False)
+    free_cpl = sys_.free_mask_cpl()
+    return E[sys_.vv_of_cpl][:, fes.dof_vbar.is_free][free_cpl].tocsr()
+
+
+# -------------------------------------------------------------- coarse space
+
+def coarse_matrix(fes, nu, penalty_C=4.0):
+    """Conforming P1 strain form + Gamma_Ntilde tangential penalty on free
+    P1 dofs (reference `preconditioners.py:121-165`), vectorised."""
+    m, k = fes.mesh, fes.k
+    dl = np.array([[-1.0, -1.0], [1.0, 0.0], [0.0, 1.0]])
+    dlam = np.einsum("la,tab->tlb", dl, fes.Jinv)                  # (nt,3,2)
+    nt = m.num_triangles
+    g = np.zeros((nt, 6, 2, 2))
+    for lv in range(3):
+        for c in range(2):
+            g[:, 2 * lv + c, c, :] = dlam[:, lv]
+    eps = 0.5 * (g + np.swapaxes(g, 2, 3))
+    blk = nu * (0.5 * fes.detJ)[:, None, None] * np.einsum("taij,tbij->tab", eps, eps)
+    lg = fes.dof_vbar.loc2glob
+    rows = [np.repeat(lg, 6, axis=1).ravel()]
+    cols = [np.tile(lg, (1, 6)).ravel()]
+    vals = [blk.ravel()]
+    if penalty_C > 0 and fes.regions.tilde_neumann_facets:
+        Fs = np.array(sorted(fes.regions.tilde_neumann_facets))
+        a, b = m.facet_start[Fs], m.facet_end()[Fs]
+        tF, ln = m.facet_tangent[Fs], m.facet_length[Fs]
+        wgt = nu * penalty_C * k * k / ln
+        mass = np.array([[1 / 3, 1 / 6], [1 / 6, 1 / 3]])
+        dofs = np.stack([2 * a, 2 * a + 1, 2 * b, 2 * b + 1], axis=1)
+        tt = np.einsum("fi,fj->fij", tF, tF)
+        B = np.zeros((len(Fs), 4, 4))
+        for i in range(2):
+            for j in range(2):
+                B[:, 2 * i:2 * i + 2, 2 * j:2 * j + 2] = \
+                    (wgt * ln * mass[i, j])[:, None, None] * tt
+        rows.append(np.repeat(dofs, 4, axis=1).ravel())
+        cols.append(np.tile(dofs, (1, 4)).ravel())
+        vals.append(B.ravel())
+    n = fes.dof_vbar.ndof
+    A = sp.coo_matrix((np.concatenate(vals), (np.concatenate(rows), np.concatenate(cols))),
+                      shape=(n, n)).tocsr()
+    free = fes.dof_vbar.is_free
+    return A[free][:, free].tocsr()
+
+
+def build_coarse(fes, nu: float, penalty_C: float = 4.0, scale: float = 1.0) -> CoarseSolver:
+    """Exactly factorised P1 coarse problem (reference `:121-171`)."""
+    A = coarse_matrix(fes, nu, penalty_C)
+    xy = fes.mesh.vertices[np.flatnonzero(fes.dof_vbar.is_free) // 2]
+    return factorize_coarse(A, xy, scale=scale)
+
+
+# ------------------------------------------------------------------ smoother
+
+def facet_blocks_schur(fes, sys_) -> List[np.ndarray]:
+    """Host list of the S_d facet blocks (reference `:266-280`), for
+    compatibility; the GPU smoother builds its blocks from `facet_slots`."""
+    k = fes.k
+    idx = free_index(sys_.free_mask_cpl())
+    out = []
+    for f in range(fes.mesh.num_facets):
+        d = [sys_.cpl_of_vv[f * (k + 1) + q] for q in range(k + 1)]
+        d += [sys_.cpl_of_vv[fes.n_v + f * k + q] for q in range(k)]
+        b = idx[np.array(d)]
+        b = b[b >= 0]
+        if len(b):
+            out.append(np.unique(b))
+    return out
+
+
+class FacetBlockSmoother:
+    """Facet-block Jacobi on S_d with packed block inverses in HBM
+    (reference `:177-206`, variant "jacobi")."""
+
+    def __init__(self, A, blocks=None, variant: str = "gauss_seidel"):
+        if variant not in ("jacobi", "gauss_seidel", "l1"):
+            raise ValueError(f"unknown smoother variant {variant!r}")
+        if variant != "jacobi":
+            raise NotImplementedError(
+                f"smoother {variant!r} is sequential / out of the GPU scope (SURVEY §2)")
+        if not isinstance(A, SdOperator):
+            raise TypeError("the GPU smoother is built from an SdOperator")
+        torch = __import__("torch")
+        self.A, self.variant = A, variant
+        sys_ = A.sys
+        fes = sys_.fes
+        k = fes.k
+        slots, self.facets = facet_slots(fes, sys_.maps)
+        self.nblk = len(slots)
+        B = 2 * k + 1
+        self.binv = torch.empty((B * (B + 1) // 2, self.nblk), dtype=torch.float64, device="cuda")
+        self.bidx = torch.empty((B, self.nblk), dtype=torch.int32, device="cuda")
+        self.bsize = torch.empty(self.nblk, dtype=torch.int32, device="cuda")
+        info = torch.empty(self.nblk, dtype=torch.int32, device="cuda")
+        m = sys_.dev_maps()
+        _abi.call("mcs_jacobi_setup", k, self.nblk, _abi.ptr(sys_.Sd_dev),
+                  sys_.Sd_dev.shape[1], _abi.ptr(m["cpl_codes"]),
+                  _abi.ptr(engine.to_dev(slots)), _abi.ptr(self.binv), _abi.ptr(self.bidx),
+                  _abi.ptr(self.bsize), _abi.ptr(info), _abi.stream())
+        bad = np.flatnonzero(info.cpu().numpy())
+        if len(bad):
+            raise RuntimeError(f"facet block {int(self.facets[bad[0]])} not SPD")
+        self.k = k
+        self.blocks = blocks
+
+    def jacobi_apply(self, r, out=None, scale_inv=1.0, stream=None):
+        rd, host = as_device(r)
+        x = out if out is not None else empty(rd.numel())
+        _abi.call("mcs_jacobi_apply", self.k, self.nblk, _abi.ptr(self.binv),
+                  _abi.ptr(self.bidx), _abi.ptr(rd), _abi.ptr(x), float(scale_inv),
+                  _abi.stream(stream))
+        return x.cpu().numpy() if host else x
+
+    apply_symmetric = jacobi_apply
+
+
+class _DevCsr:
+    def __init__(self, A: sp.csr_matrix):
+        A = A.tocsr()
+        A.sort_indices()
+        self.shape = A.shape
+        self.ptr = engine.to_dev(A.indptr.astype(np.int32))
+        self.col = engine.to_dev(A.indices.astype(np.int32))
+        self.val = engine.to_dev(A.data.astype(np.float64))
+        avg = A.nnz / max(A.shape[0], 1)
+        self.lanes = 1 if avg <= 6 else (4 if avg <= 16 else 8)
+
+    def mv(self, x, y, alpha=1.0, beta=0.0, stream=None):
+        _abi.call("mcs_csr_spmv", self.shape[0], _abi.ptr(self.ptr), _abi.ptr(self.col),
+                  _abi.ptr(self.val), _abi.ptr(x), _abi.ptr(y), float(alpha), float(beta),
+                  self.lanes, _abi.stream(stream))
+        return y
+
+
+class AspPreconditioner:
+    """Smoother + embedded exact coarse correction (reference `:286-336`)."""
+
+    def __init__(self, A, smoother, E, coarse, mode: str = "multiplicative",
+                 steps: int = 1):
+        if mode not in ("additive", "multiplicative"):
+            raise ValueError(f"unknown composition mode {mode!r}")
+        self.A, self.smoother, self.coarse, self.mode, self.steps = A, smoother, coarse, mode, steps
+        self.E = _DevCsr(E)
+        self.Et = _DevCsr(E.T.tocsr())
+        n, nc = E.shape
+        self.n = n
+        self._t, self._w = empty(n), empty(n)
+        self._u, self._v = empty(nc), empty(nc)
+        self.jacobi_scale = 1.0
+        if mode == "multiplicative":
+            self.jacobi_scale = self._estimate_smoother_bound()
+
+    def _estimate_smoother_bound(self, iters=20, seed=1234):
+        """1.1 x the largest Ritz value of J A by 20 power steps from
+        default_rng(1234) (reference `:304-314`), on the GPU."""
+        ws = workspace()
+        x = as_device(np.random.default_rng(seed).standard_normal(self.n))[0]
+        y = empty(self.n)
+        lam = 1.0
+        for _ in range(iters):
+            self.A.apply(x, out=self._t)
+            self.smoother.jacobi_apply(self._t, out=y)
+            lam = float(np.sqrt(ws.dot_host(y, y)))
+            axpby(1.0 / lam, y, 0.0, x)
+        return 1.1 * lam
+
+    def coarse_correction(self, r, x, beta):
+        """x = beta*x + E C^-1 E^T r."""
+        self.Et.mv(r, self._u)
+        self.coarse.solve_dev(self._u, self._v)
+        self.E.mv(self._v, x, 1.0, beta)
+        return x
+
+    def apply(self, r, out=None):
+        rd, host = as_device(r)
+        x = out if out is not None else empty(self.n)
+        if self.mode == "additive":
+            self.smoother.jacobi_apply(rd, out=x)
+            self.coarse_correction(rd, x, 1.0)
+        else:
+            s_inv = 1.0 / self.jacobi_scale
+            t, w = self._t, self._w
+            # pre-smoothing: first step has x = 0, so r - A x = r exactly
+            self.smoother.jacobi_apply(rd, out=x, scale_inv=s_inv)
+            for _ in range(self.steps - 1):
+                self._residual(rd, x, t)
+                self.smoother.jacobi_apply(t, out=w, scale_inv=s_inv)
+                axpby(1.0, w, 1.0, x)
+            self._residual(rd, x, t)
+            self.coarse_correction(t, x, 1.0)
+            for _ in range(self.steps):
+                self._residual(rd, x, t)
+                self.smoother.jacobi_apply(t, out=w, scale_inv=s_inv)
+                axpby(1.0, w, 1.0, x)
+        return x.cpu().numpy() if host else x
+
+    def _residual(self, r, x, t):
+        self.A.apply(x, out=t)
+        axpby(1.0, r, -1.0, t)
+
+
+class ExtendedAsp:
+    """S_d preconditioner lifted to S through the exact block factorisation
+    (reference `:339-378`)."""
+
+    def __init__(self, sys_, inner):
+        if sys_.Sd_dev is None:
+            raise ValueError("double_schur() must be run first")
+        self.sys, self.inner = sys_, inner
+        m = sys_.maps
+        self.n, self.nc = m.n_vv_free, m.n_cpl_free
+        nt = sys_.S_dev.shape[0]
+        self.nt = nt
+        self.bubble = empty(nt * sys_.z["n_int"])
+        self.acc, self.wc = empty(self.nc), empty(self.nc)
+        self.zc = empty(self.nc)
+
+    def apply(self, r_free, out=None, stream=None):
+        s = self.sys
+        rd, host = as_device(r_free)
+        out = out if out is not None else empty(self.n)
+        m = s.dev_maps()
+        st = _abi.stream(stream)
+        _abi.call("mcs_ext_restrict", s.k, self.nt, _abi.ptr(s.ext_dev), _abi.ptr(m["bubble_idx"]),
+                  _abi.ptr(m["cpl_codes"]), _abi.ptr(rd), _abi.ptr(self.bubble),
+                  _abi.ptr(self.acc), self.nc, st)
+        _abi.call("mcs_gather_sub", self.nc, _abi.ptr(rd), _abi.ptr(m["c2v"]),
+                  _abi.ptr(self.acc), _abi.ptr(self.wc), st)
+        self.inner.apply(self.wc, out=self.zc)
+        _abi.call("mcs_scatter", self.nc, _abi.ptr(self.zc), _abi.ptr(m["c2v"]), _abi.ptr(out), st)
+        _abi.call("mcs_ext_prolong", s.k, self.nt, _abi.ptr(s.ext_dev), _abi.ptr(m["bubble_idx"]),
+                  _abi.ptr(m["cpl_codes"]), _abi.ptr(self.zc), _abi.ptr(self.bubble),
+                  _abi.ptr(out), st)
+        return out.cpu().numpy() if host else out
+
+    __call__ = apply

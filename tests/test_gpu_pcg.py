@@ -1,0 +1,124 @@
+"""GPU parity of the PCG hot path (operator apply, ExtendedAsp/ASP
+preconditioner, PCG) against the reference's golden outputs and the oracle.
+North star: operator applies <= 1e-10 relative l2; PCG iteration count +-1
+at rtol 1e-8."""
+import numpy as np
+import pytest
+
+from conftest import golden, rel
+from oracle import mcs_oracle as O
+from paper_2207_08481_b200 import preconditioners as pc
+from paper_2207_08481_b200.condensation import condense_sigma_omega, double_schur
+from paper_2207_08481_b200.dofmap import FeSystem
+from paper_2207_08481_b200.driver import (SolverOptions, condensed_rhs,
+                                           velocity_preconditioner)
+from paper_2207_08481_b200.krylov import NegativeCurvatureError, cg
+from paper_2207_08481_b200.operators import SdOperator, SOperator
+from paper_2207_08481_b200.problems import baseline_config
+
+pytestmark = pytest.mark.gpu
+CASES = ["c1_n2", "c2_n3", "c3_n2", "cfg1"]
+
+
+def _system(g):
+    prob = baseline_config(int(g["cfg"]), int(g["n"]))
+    fes = FeSystem(prob.mesh, prob.regions, prob.k)
+    sys_ = double_schur(condense_sigma_omega(fes, prob.nu, prob.body_force))
+    return prob, fes, sys_
+
+
+@pytest.mark.parametrize("name", CASES)
+def test_operator_apply_matches_reference(cuda, name):
+    g = golden(name)
+    prob, fes, sys_ = _system(g)
+    got = SOperator(sys_)(g["probe_v"])
+    assert rel(got, g["probe_Sv"]) <= 1e-10
+    assert rel(condensed_rhs(fes, sys_), g["rhs_u"]) <= 1e-12
+
+
+@pytest.mark.parametrize("name", ["c1_n2", "c2_n3", "c3_n2"])
+def test_double_schur_apply_matches_reference(cuda, name):
+    import scipy.sparse as sp
+    g = golden(name)
+    prob, fes, sys_ = _system(g)
+    Sd = sp.csr_matrix((g["Sd_data"], g["Sd_indices"], g["Sd_indptr"]),
+                       shape=tuple(g["Sd_shape"]))
+    fc = sys_.free_mask_cpl()
+    Sdf = Sd[fc][:, fc]
+    v = np.random.default_rng(3).standard_normal(Sdf.shape[0])
+    assert rel(SdOperator(sys_)(v), Sdf @ v) <= 1e-10
+    # per-element X against the reference's ext list
+    X = np.array(sys_.ext)
+    assert rel(X, g["ext"]) <= 1e-10
+
+
+@pytest.mark.parametrize("name", CASES)
+@pytest.mark.parametrize("comp", ["additive", "multiplicative"])
+def test_preconditioner_apply_matches_reference(cuda, name, comp):
+    g = golden(name)
+    prob, fes, sys_ = _system(g)
+    M = velocity_preconditioner(fes, sys_, prob.nu, SolverOptions(composition=comp))
+    assert M.inner.jacobi_scale == pytest.approx(float(g[f"jacobi_scale_{comp}"]), rel=1e-10)
+    assert rel(M(g["probe_v"]), g[f"probe_M_{comp}"]) <= 1e-10
+
+
+@pytest.mark.parametrize("name", CASES)
+@pytest.mark.parametrize("comp", ["additive", "multiplicative"])
+def test_pcg_iterations_match_reference(cuda, name, comp):
+    g = golden(name)
+    prob, fes, sys_ = _system(g)
+    M = velocity_preconditioner(fes, sys_, prob.nu, SolverOptions(composition=comp))
+    x, rep = cg(SOperator(sys_), condensed_rhs(fes, sys_), M, rtol=1e-8, maxit=2000)
+    ref_it = int(g[f"cg_{comp}_iters"])
+    assert rep.converged
+    assert abs(rep.iterations - ref_it) <= 1
+    assert rel(x, g[f"cg_{comp}_x"]) <= 1e-7
+    # residual history tracks the reference's to many digits
+    n = min(len(rep.residuals), len(g[f"cg_{comp}_res"]))
+    assert np.allclose(rep.residuals[:n], g[f"cg_{comp}_res"][:n], rtol=1e-6, atol=1e-12)
+
+
+def test_cg_negative_curvature(cuda):
+    import torch
+    A = np.diag([1.0, -1.0, 2.0])
+
+    def apply_A(v):
+        return torch.from_numpy(A @ v.cpu().numpy()).cuda()
+
+    with pytest.raises(NegativeCurvatureError):
+        cg(apply_A, np.array([1.0, 1.0, 1.0]))
+
+
+def test_cg_zero_rhs(cuda):
+    x, rep = cg(lambda v: v, np.zeros(7))
+    assert rep.converged and rep.iterations == 0 and not np.any(x)
+
+
+def test_pcg_bitwise_reproducible(cuda):
+    """Run-to-run bitwise identity (the reference's test_cli.py:122-129 idea;
+    deterministic scatter + fixed-order reductions)."""
+    g = golden("c2_n3")
+    prob, fes, sys_ = _system(g)
+    M = velocity_preconditioner(fes, sys_, prob.nu, SolverOptions(composition="additive"))
+    b = condensed_rhs(fes, sys_)
+    x1, r1 = cg(SOperator(sys_), b, M, rtol=1e-8)
+    x2, r2 = cg(SOperator(sys_), b, M, rtol=1e-8)
+    assert r1.residuals == r2.residuals
+    assert np.array_equal(x1, x2)
+
+
+@pytest.mark.parametrize("cfg,n,leaf", [(1, 16, 48), (2, 40, 128), (3, 24, 96)])
+def test_multifrontal_coarse_solve_exact(cuda, cfg, n, leaf):
+    """GPU multifrontal triangular solves vs a direct sparse solve."""
+    import scipy.sparse.linalg as spla
+    from paper_2207_08481_b200 import coarse as co
+    prob = baseline_config(cfg, n)
+    fes = FeSystem(prob.mesh, prob.regions, prob.k)
+    A = pc.coarse_matrix(fes, prob.nu)
+    xy = fes.mesh.vertices[np.flatnonzero(fes.dof_vbar.is_free) // 2]
+    cs = co.factorize_coarse(A, xy, kind="multifrontal", leaf=leaf)
+    b = np.random.default_rng(1).standard_normal(A.shape[0])
+    ref = spla.spsolve(A.tocsc(), b)
+    assert rel(cs.solve(b), ref) <= 1e-12
+    # deterministic
+    assert np.array_equal(cs.solve(b), cs.solve(b))
