@@ -1,0 +1,497 @@
+#!/usr/bin/env python
+"""Benchmark of the B200 condensation + PCG hot path (one JSON line).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+
+Workload (BASELINE.json configs[1]): N=128 grid, 32,768
+jittered triangles, k=4, nu=1e-2, Fourier body force seed 0.  One *step* is
+one condensation pass over all elements on the GPU: element blocks from the
+geometry (A1) -> sigma/omega elimination (A3) -> double Schur (A4).
+`value` = elements condensed per second, inputs resident in HBM, L2 flushed
+before every timed step, device time by CUDA events.  The same run also
+measures the condensed-operator apply (DOF/s, A6), the full PCG solve to
+rtol 1e-8 (both compositions) and the config-5 SPD-Schur microbench, and
+reports the CPU oracle on a bounded sample as `cpu_baseline`.
+
+`--impl reference` times the reference algorithm's CPU restatement
+(oracle/mcs_oracle.py: quadrature blocks + LU condensation + double Schur,
+condensation.py:159-224 / assembly.py:49-91) on the host cores, process
+parallel over elements, on the same workload and metric.
+
+Multi-GPU (torchrun, N>1): replicas only - every rank condenses
+its own copy of the workload; value = all ranks' elements / max-over-ranks
+time.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = ("elements condensed/s and condensed-apply DOF/s at 1 GPU; "
+          "% FP64/HBM roofline")
+WORKLOAD = ("cfg2: unit square N=128 (32,768 triangles, jitter 0.2h seed 1), k=4, "
+            "nu=1e-2, Fourier force seed 0; step = A1 element blocks + A3 "
+            "sigma/omega condensation + A4 double Schur over all elements")
+
+
+def flops_per_element(k):
+    z = dict(ns=3 * (k + 1) * (k + 2) // 2 - 3, nw=k * (k + 1) // 2,
+             nloc=(k + 1) * (k + 2) + 3 * k, nint=(k + 1) * (k - 1))
+    ns, nw, nl, ni = z["ns"], z["nw"], z["nloc"], z["nint"]
+    nc = nl - ni
+    f_cond = (ns ** 3 / 3 + ns ** 2 * (nl + nw) + nw ** 2 * ns + nw ** 3 / 3
+              + 2 * nw * ns * nl + nw ** 2 * nl + nl ** 2 * ns + nl ** 2 * nw)
+    f_ds = ni ** 3 / 3 + ni ** 2 * nc + nc ** 2 * ni
+    return f_cond, f_ds
+
+
+# ------------------------------------------------------------------ clocks
+
+class ClockSampler:
+    """nvidia-smi sampling DURING the timed region (B200_PROFILING.md)."""
+    Q = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index=0):
+        self.index, self.proc, self.lines = index, None, []
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.Q}",
+                 "--format=csv,noheader,nounits", "-lms", "50"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except OSError:
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def stop(self):
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except subprocess.TimeoutExpired:
+            self.proc.kill()
+        sm, mx, reasons, power = [], [], set(), []
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            f = [x.strip() for x in ln.split(",")]
+            if len(f) < 8:
+                continue
+            try:
+                sm.append(float(f[0]))
+                mx.append(float(f[1]))
+                power.append(float(f[2]))
+            except ValueError:
+                continue
+            for nm, v in zip(names, f[4:8]):
+                if v.lower() == "active":
+                    reasons.add(nm)
+        return {"sm_mhz": float(np.median(sm)) if sm else None,
+                "sm_max_mhz": max(mx) if mx else None,
+                "power_w_max": max(power) if power else None,
+                "samples": len(sm), "reasons": sorted(reasons)}
+
+
+# -------------------------------------------------------------- our arm
+
+def load_peaks():
+    peaks = {"hbm_gbs": None, "fp64_tflops": None}
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as fh:
+            peaks["hbm_gbs"] = json.load(fh).get("hbm_gbs")
+    except OSError:
+        pass
+    try:
+        with open(os.path.join(ROOT, "profiles", "fp64_peak_r01.json")) as fh:
+            d = json.load(fh)
+            peaks["fp64_tflops"] = max(d["dfma_tflops"], d["dmma_m8n8k4_tflops"])
+    except OSError:
+        pass
+    if peaks["hbm_gbs"] is None:
+        peaks["hbm_gbs"] = 6650.0
+    return peaks
+
+
+def ncu_traffic(name):
+    """dram bytes per launch from the committed ncu summary, if any."""
+    try:
+        with open(os.path.join(ROOT, "profiles", "ncu_summary_r01.json")) as fh:
+            d = json.load(fh)
+        return d.get(name, {}).get("dram_bytes")
+    except OSError:
+        return None
+
+
+def run_ours(args, rank, world):
+    import torch
+    from paper_2207_08481_b200 import _abi, engine, refblocks
+    from paper_2207_08481_b200.condensation import condense_sigma_omega, double_schur
+    from paper_2207_08481_b200.dofmap import FeSystem
+    from paper_2207_08481_b200.driver import (SolverOptions, condensed_rhs,
+                                               velocity_preconditioner)
+    from paper_2207_08481_b200.krylov import cg
+    from paper_2207_08481_b200.operators import SOperator
+    from paper_2207_08481_b200.problems import baseline_config
+
+    dev = torch.device("cuda", int(os.environ.get("LOCAL_RANK", 0)))
+    torch.cuda.set_device(dev)
+    _abi.lib()
+    prob = baseline_config(2, args.n)
+    fes = FeSystem(prob.mesh, prob.regions, prob.k)
+    k, nt = prob.k, prob.mesh.num_triangles
+    refs = refblocks.build_refs(fes)
+    W_h = refblocks.element_weights(fes, prob.nu)
+    W = engine.to_dev(W_h)
+    prog = [engine.to_dev(a) for a in engine.block_program(refs)]
+    L = engine.record_layout(k)
+    rec = torch.empty((nt, L["len"]), dtype=torch.float64, device=dev)
+    ST = torch.empty((nt, engine.st_stride(k)), dtype=torch.float64, device=dev)
+    ext = torch.empty((nt, _abi.call("mcs_ext_stride", k)), dtype=torch.float64, device=dev)
+    Sd = torch.empty((nt, _abi.call("mcs_sd_stride", k)), dtype=torch.float64, device=dev)
+    info = torch.empty(nt, dtype=torch.int32, device=dev)
+    flush = torch.empty(256 * 2 ** 20 // 8, dtype=torch.float64, device=dev)
+    stream = torch.cuda.current_stream()
+    st = _abi.stream(stream)
+
+    def step(ev=None):
+        if ev:
+            ev[0].record(stream)
+        engine.element_records(nt, W, prog, k, out=rec, stream=stream)
+        if ev:
+            ev[1].record(stream)
+        _abi.call("mcs_condense", k, nt, _abi.ptr(rec), _abi.ptr(ST), _abi.ptr(info), st)
+        if ev:
+            ev[2].record(stream)
+        _abi.call("mcs_double_schur", k, nt, _abi.ptr(ST), _abi.ptr(ext), _abi.ptr(Sd),
+                  _abi.ptr(info), st)
+        if ev:
+            ev[3].record(stream)
+
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+    if int(info.abs().sum().item()):
+        raise RuntimeError("condensation reported failing elements")
+    evs = [[torch.cuda.Event(enable_timing=True) for _ in range(4)] for _ in range(args.steps)]
+    clocks = ClockSampler(dev.index)
+    if world > 1:
+        torch.distributed.barrier()
+    torch.cuda.synchronize()
+    clocks.start()
+    time.sleep(0.2)
+    for i in range(args.steps):
+        flush.fill_(float(i))                 # L2 flush (256 MiB write), untimed
+        step(evs[i])
+    torch.cuda.synchronize()
+    t_a1 = np.array([e[0].elapsed_time(e[1]) for e in evs])
+    t_a3 = np.array([e[1].elapsed_time(e[2]) for e in evs])
+    t_a4 = np.array([e[2].elapsed_time(e[3]) for e in evs])
+    t_step = t_a1 + t_a3 + t_a4
+    ms_per_step = float(t_step.mean())
+    if world > 1:
+        t = torch.tensor([ms_per_step], device=dev)
+        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+        ms_per_step = float(t.item())
+    value = world * nt / (ms_per_step * 1e-3)
+
+    # ---- condensed-operator apply (A6) and PCG (A8-A13), same run
+    sys_ = double_schur(condense_sigma_omega(fes, prob.nu, prob.body_force))
+    S = SOperator(sys_)
+    n_free = sys_.maps.n_vv_free
+    x = torch.randn(n_free, dtype=torch.float64, device=dev)
+    y = torch.empty_like(x)
+    for _ in range(5):
+        S.apply(x, out=y)
+    napp = max(20, args.steps)
+    ev_a = [[torch.cuda.Event(enable_timing=True) for _ in range(2)] for _ in range(napp)]
+    for i in range(napp):
+        flush.fill_(float(i))
+        ev_a[i][0].record(stream)
+        S.apply(x, out=y)
+        ev_a[i][1].record(stream)
+    torch.cuda.synchronize()
+    t_apply = float(np.mean([e[0].elapsed_time(e[1]) for e in ev_a]))
+    z = refblocks.local_sizes(k)
+    apply_bytes = nt * 8 * z["nloc"] * (z["nloc"] + 1) / 2 + 16 * n_free
+    pcg = {}
+    for comp in ("additive", "multiplicative"):
+        t0 = time.perf_counter()
+        M = velocity_preconditioner(fes, sys_, prob.nu, SolverOptions(composition=comp))
+        torch.cuda.synchronize()
+        t_sup = time.perf_counter() - t0
+        b_h = condensed_rhs(fes, sys_)
+        b = torch.from_numpy(b_h).to(dev)
+        cg(S, b, M, rtol=1e-8, maxit=2000)      # warm-up
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        xs, rep = cg(S, b, M, rtol=1e-8, maxit=2000)
+        e1.record(stream)
+        torch.cuda.synchronize()
+        pcg[comp] = {"iterations": rep.iterations, "final_res": rep.residuals[-1],
+                     "solve_ms": e0.elapsed_time(e1), "precond_setup_s": round(t_sup, 3),
+                     "jacobi_scale": M.inner.jacobi_scale}
+    clk = clocks.stop()
+
+    # ---- e2e through the C ABI with host buffers: H2D weights, D2H results
+    W_pin = torch.from_numpy(W_h).pin_memory()
+    out_bytes = (ST.numel() + Sd.numel() + ext.numel()) * 8
+    ST_h = torch.empty(ST.shape, dtype=torch.float64).pin_memory()
+    Sd_h = torch.empty(Sd.shape, dtype=torch.float64).pin_memory()
+    ext_h = torch.empty(ext.shape, dtype=torch.float64).pin_memory()
+    e2e_times = []
+    for i in range(max(3, min(args.steps, 20)) + 2):
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        W.copy_(W_pin, non_blocking=True)
+        step()
+        ST_h.copy_(ST, non_blocking=True)
+        Sd_h.copy_(Sd, non_blocking=True)
+        ext_h.copy_(ext, non_blocking=True)
+        e1.record(stream)
+        torch.cuda.synchronize()
+        if i >= 2:
+            e2e_times.append(e0.elapsed_time(e1))
+    e2e_ms = float(np.mean(e2e_times))
+
+    # ---- config-5 microbench (SPD Schur S = B^T A^-1 B, n_s=60, n_c=36)
+    micro = run_microbench(args, dev) if args.micro else None
+
+    peaks = load_peaks()
+    f_cond, f_ds = flops_per_element(k)
+    achieved = f_cond * nt / (t_a3.mean() * 1e-3) / 1e12
+    out = {
+        "metric": METRIC, "value": value, "unit": "elements/s", "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_per_step,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+        "dtype": "f64", "data": "synthetic (seeded SURVEY §8d generators)",
+        "config": {"workload": WORKLOAD, "elements": nt, "k": k,
+                   "parallelism": "replicas" if world > 1 else "single-gpu",
+                   "l2": "flushed (256 MiB write) before every timed step"},
+        "breakdown_ms": {"A1_blocks": float(t_a1.mean()), "A3_condense": float(t_a3.mean()),
+                         "A4_double_schur": float(t_a4.mean())},
+        "apply_dof_per_s": n_free / (t_apply * 1e-3), "apply_ms": t_apply,
+        "apply_roofline": {"bound": "hbm", "achieved": apply_bytes / (t_apply * 1e-3) / 1e9,
+                           "peak": peaks["hbm_gbs"], "unit": "GB/s",
+                           "frac": apply_bytes / (t_apply * 1e-3) / 1e9 / peaks["hbm_gbs"],
+                           "traffic": ncu_traffic("elem_apply")},
+        "pcg": pcg,
+        "roofline": {"bound": "fp64", "kernel": "condense_kernel<4,8> (A3)",
+                     "achieved": achieved, "peak": peaks["fp64_tflops"], "unit": "TFLOP/s",
+                     "frac": achieved / peaks["fp64_tflops"] if peaks["fp64_tflops"] else None,
+                     "flops_per_element": f_cond,
+                     "traffic": ncu_traffic("condense"),
+                     "peak_source": "profiles/fp64_peak_r01.json (measured DMMA/DFMA max)"},
+        "e2e": {"value": world * nt / (e2e_ms * 1e-3), "unit": "elements/s",
+                "h2d_bytes_per_step": W_h.nbytes, "d2h_bytes_per_step": out_bytes,
+                "ms_per_step": e2e_ms},
+        "gpu_launches": 3 * args.steps,
+        "clocks": clk,
+    }
+    if micro:
+        out["microbench"] = micro
+    return out
+
+
+def run_microbench(args, dev):
+    import torch
+    from paper_2207_08481_b200 import engine
+    n, m = 60, 36
+    count = args.micro_count
+    g = torch.Generator(device=dev)
+    g.manual_seed(3)
+    Ap = torch.empty((count, n * (n + 1) // 2), dtype=torch.float64, device=dev)
+    B = torch.empty((count, n, m), dtype=torch.float64, device=dev)
+    r, c = torch.tril_indices(n, n, device=dev)
+    chunk = 65536
+    for s in range(0, count, chunk):
+        e = min(count, s + chunk)
+        G = torch.randn((e - s, n, n), dtype=torch.float64, device=dev, generator=g)
+        B[s:e] = torch.randn((e - s, n, m), dtype=torch.float64, device=dev, generator=g)
+        A = torch.bmm(G, G.transpose(1, 2)) + n * torch.eye(n, dtype=torch.float64, device=dev)
+        Ap[s:e] = A[:, r, c]
+        del G, A
+    S = torch.empty((count, m * (m + 1) // 2), dtype=torch.float64, device=dev)
+    info = torch.empty(count, dtype=torch.int32, device=dev)
+    for _ in range(3):
+        engine.spd_schur(n, m, Ap, B, out=S, info=info)
+    torch.cuda.synchronize()
+    ts = []
+    for _ in range(5):
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        engine.spd_schur(n, m, Ap, B, out=S, info=info)
+        e1.record()
+        torch.cuda.synchronize()
+        ts.append(e0.elapsed_time(e1))
+    t = float(np.mean(ts))
+    flops = n ** 3 / 3 + n * n * m + m * m * n
+    # parity on a sample vs the CPU oracle
+    from oracle import mcs_oracle as O
+    idx = np.random.default_rng(4).choice(count, 64, replace=False)
+    A_s = Ap[idx].cpu().numpy()
+    B_s = B[idx].cpu().numpy()
+    S_s = engine.unpack_sym(S[idx].cpu().numpy(), m)
+    worst = 0.0
+    for i in range(len(idx)):
+        Af = engine.unpack_sym(A_s[i], n)
+        ref = O.spd_schur(Af, B_s[i])
+        worst = max(worst, np.linalg.norm(S_s[i] - ref) / np.linalg.norm(ref))
+    bytes_el = 8 * (n * (n + 1) // 2 + n * m + m * (m + 1) // 2)
+    peaks = load_peaks()
+    return {"elements": count, "ms": t, "elements_per_s": count / (t * 1e-3),
+            "tflops": flops * count / (t * 1e-3) / 1e12,
+            "frac_fp64_peak": flops * count / (t * 1e-3) / 1e12 / peaks["fp64_tflops"],
+            "hbm_gbs": bytes_el * count / (t * 1e-3) / 1e9,
+            "max_rel_frob_err_vs_oracle": worst, "failed": int((info != 0).sum().item())}
+
+
+# ----------------------------------------------------------- CPU baselines
+
+_WORKER = {}
+
+
+def _cpu_init(n):
+    import threadpoolctl
+    sys.path.insert(0, ROOT)
+    from paper_2207_08481_b200.dofmap import FeSystem
+    from paper_2207_08481_b200.problems import baseline_config
+    _WORKER["limits"] = threadpoolctl.threadpool_limits(1)
+    prob = baseline_config(2, n)
+    _WORKER["prob"] = prob
+    _WORKER["fes"] = FeSystem(prob.mesh, prob.regions, prob.k)
+
+
+def _cpu_worker(elems):
+    """Condense a slice of elements with the oracle (reference algorithm)."""
+    from oracle import mcs_oracle as O
+    prob, fes = _WORKER["prob"], _WORKER["fes"]
+    t0 = time.perf_counter()
+    for t in elems:
+        blocks = O.element_blocks(fes, t, prob.nu, None)
+        S_T, _ = O.condense_element(*blocks[:5])
+        O.double_schur_element(S_T, prob.k)
+    return time.perf_counter() - t0, len(elems)
+
+
+class CpuCondenser:
+    """The reference algorithm on `procs` host processes; rate = elements /
+    wall time of the slowest worker (setup excluded)."""
+
+    def __init__(self, n, procs):
+        from concurrent.futures import ProcessPoolExecutor
+        self.n, self.procs = n, procs
+        self.pool = None
+        if procs > 1:
+            self.pool = ProcessPoolExecutor(procs, initializer=_cpu_init, initargs=(n,))
+        else:
+            _cpu_init(n)
+        self.rng = np.random.default_rng(5)
+
+    def rate(self, sample):
+        nt = 2 * self.n * self.n
+        elems = np.sort(self.rng.choice(nt, size=min(sample, nt), replace=False))
+        parts = [elems[i::self.procs] for i in range(self.procs)]
+        if self.pool is None:
+            dt, cnt = _cpu_worker(parts[0])
+            return cnt / dt, cnt
+        res = list(self.pool.map(_cpu_worker, parts))
+        return len(elems) / max(r[0] for r in res), len(elems)
+
+    def close(self):
+        if self.pool is not None:
+            self.pool.shutdown()
+
+
+def run_reference(args, rank, world):
+    """--impl reference: the reference's CPU algorithm (oracle port)."""
+    if rank != 0:
+        return None
+    procs = os.cpu_count() or 1
+    cc = CpuCondenser(args.n, procs)
+    vals = []
+    for _ in range(args.warmup):
+        cc.rate(4 * procs)
+    for _ in range(args.steps):
+        v, cnt = cc.rate(args.ref_sample_per_core * procs)
+        vals.append(v)
+    cc.close()
+    value = float(np.mean(vals))
+    sample = (f"{args.ref_sample_per_core * procs} random elements of cfg2 per step "
+              f"(quadrature blocks + LU condensation + double Schur, oracle/mcs_oracle.py)")
+    return {"metric": METRIC, "value": value, "unit": "elements/s", "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": 1e3 * 32768 / value,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+            "dtype": "f64", "data": "synthetic (seeded SURVEY §8d generators)",
+            "config": {"workload": WORKLOAD, "elements": 32768, "k": 4,
+                       "parallelism": f"{procs} host processes"},
+            "impl": "reference",
+            "cpu_baseline": {"value": value, "unit": "elements/s", "cores": procs,
+                             "kind": "port", "sample": sample},
+            "e2e": {"value": value, "unit": "elements/s", "h2d_bytes_per_step": 0,
+                    "d2h_bytes_per_step": 0}}
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=50)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--n", type=int, default=128)
+    ap.add_argument("--no-micro", dest="micro", action="store_false")
+    ap.add_argument("--micro-count", type=int, default=1 << 20)
+    ap.add_argument("--cpu-sample", type=int, default=3072)
+    ap.add_argument("--ref-sample-per-core", type=int, default=32)
+    args = ap.parse_args()
+    args.warmup = max(args.warmup, 3)
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    if args.impl == "reference":
+        out = run_reference(args, rank, world)
+        if out is not None:
+            print(json.dumps(out), flush=True)
+        return
+    if world > 1:
+        import torch
+        import torch.distributed as dist
+        torch.cuda.set_device(int(os.environ.get("LOCAL_RANK", 0)))
+        dist.init_process_group("nccl")
+    out = run_ours(args, rank, world)
+    if rank == 0:
+        # CPU baseline: the reference algorithm (oracle port), 1 core, bounded sample
+        cc = CpuCondenser(args.n, 1)
+        v, cnt = cc.rate(args.cpu_sample)
+        out["cpu_baseline"] = {"value": v, "unit": "elements/s", "cores": 1, "kind": "port",
+                               "sample": f"{cnt} random cfg2 elements, quadrature blocks + "
+                                         "LU condensation + double Schur, 1 thread"}
+        print(json.dumps(out), flush=True)
+    if world > 1:
+        import torch.distributed as dist
+        dist.barrier()
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()
