@@ -1,12 +1,10 @@
 // Per-element static condensation on B200.
 //
 // One CTA owns one element at a time (persistent over elements).  The
-// element's symmetric augmented saddle matrix lives in REGISTERS: the lower
-// triangle is cut into TBxTB tiles, one tile per thread, and eliminated
-// right-looking without pivoting.  Each pivot step broadcasts the current
-// pivot column through shared memory (double buffered, one __syncthreads per
-// pivot) and every thread applies the rank-1 update to its register tile
-// with TB*TB DFMAs against 2*TB shared-memory (broadcast) loads.
+// element's symmetric augmented saddle matrix is padded to a multiple of 8
+// (dummy unit pivots / zero trailing rows), held in registers as 8x8 DMMA
+// accumulator tiles spread over the CTA's warps, and eliminated block by
+// block on the FP64 tensor cores (elim_dmma.cuh):
 //
 //   microbench (A5):   K = [[A, B], [B^T, 0]]  -> eliminate the n_s (positive)
 //                      pivots -> trailing block = -B^T A^-1 B = -S
@@ -17,101 +15,100 @@
 //                      [bws, 0]] then adiv - Bsig M^-1 Bsig^T), proved equal in
 //                      DESIGN.md §3.
 //
-// The next element's input is prefetched into shared memory with one 1-D
-// bulk async copy (TMA engine, cp.async.bulk + mbarrier) issued as soon as
-// the current element's tiles are in registers, so HBM traffic overlaps the
-// FP64 elimination of the current element.
-#include "common.cuh"
+// The next element's input is prefetched into shared memory with a 1-D bulk
+// async copy (TMA engine, cp.async.bulk + mbarrier) issued as soon as the
+// current element's tiles are in registers, so HBM traffic overlaps the
+// elimination of the current element.
+#include "elim_dmma.cuh"
 
 namespace mcs {
 
-template <int N, int TB>
-struct Grid2 {
-  static constexpr int NB = (N + TB - 1) / TB;
-  static constexpr int NT = NB * (NB + 1) / 2;
-  static constexpr int THREADS = (NT + 31) / 32 * 32;
-  static constexpr int NPAD = NB * TB;
+__host__ __device__ constexpr int ceil8(int n) { return (n + 7) / 8 * 8; }
+
+// padded layout of an augmented matrix with NP pivots and NC trailing rows
+template <int NP, int NC, int W>
+struct Pad {
+  static constexpr int NPP = ceil8(NP), NCP = ceil8(NC);
+  static constexpr int NB = (NPP + NCP) / 8, NPB = NPP / 8;
+  using E = Elim<NB, NPB, W>;
 };
 
-__device__ __forceinline__ void tile_of(int t, int& bi, int& bj) {
-  int i = 0;
-  while ((i + 1) * (i + 2) / 2 <= t) ++i;
-  bi = i;
-  bj = t - i * (i + 1) / 2;
+// load the lane's tiles: entry(i, j) is called with real indices i >= j
+template <class P, int NP, int NC, class F>
+__device__ __forceinline__ void load_tiles(double (&acc)[P::E::TPW][2], int (&tij)[P::E::TPW],
+                                           F entry) {
+  using E = typename P::E;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int gr = lane >> 2, tg = lane & 3;
+#pragma unroll
+  for (int t = 0; t < E::TPW; ++t) {
+    const int g = warp + t * E::W;
+    int bi = 0, bj = 0;
+    if (g < E::NT) E::tile_of(g, bi, bj);
+    tij[t] = bi | (bj << 8);
+#pragma unroll
+    for (int q = 0; q < 2; ++q) {
+      int i = bi * 8 + gr, j = bj * 8 + 2 * tg + q;
+      if (i < j) { const int s = i; i = j; j = s; }
+      // padded -> real
+      const bool di = (i < P::NPP) ? (i >= NP) : (i - P::NPP >= NC);
+      const bool dj = (j < P::NPP) ? (j >= NP) : (j - P::NPP >= NC);
+      const int ri = i < P::NPP ? i : NP + (i - P::NPP);
+      const int rj = j < P::NPP ? j : NP + (j - P::NPP);
+      double v;
+      if (g >= E::NT) v = 0.0;
+      else if (di || dj) v = (i == j && i < P::NPP) ? 1.0 : 0.0;
+      else v = entry(ri, rj);
+      acc[t][q] = v;
+    }
+  }
 }
 
-// Eliminate pivots [P0, P1); pivots < PSIGN must be > 0, the rest < 0.
-// Records the first offending pivot (1-based) in *bad (shared).
-template <int N, int TB, int P0, int P1, int PSIGN>
-__device__ __forceinline__ void eliminate(double (&a)[TB][TB], int bi, int bj, bool act,
-                                          double (*col)[Grid2<N, TB>::NPAD], int* bad) {
-  for (int pb = P0 / TB; pb <= (P1 - 1) / TB; ++pb) {
+// write -trailing (lower packed, NC x NC) to out
+template <class P, int NC>
+__device__ __forceinline__ void store_trailing(const double (&acc)[P::E::TPW][2],
+                                               const int (&tij)[P::E::TPW], double* out) {
+  using E = typename P::E;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int gr = lane >> 2, tg = lane & 3;
 #pragma unroll
-    for (int cj = 0; cj < TB; ++cj) {
-      const int j = pb * TB + cj;
-      if (j < P0 || j >= P1) continue;
-      double* cb = col[j & 1];
-      if (act && bj == pb) {
+  for (int t = 0; t < E::TPW; ++t) {
+    const int g = warp + t * E::W;
+    const int bi = tij[t] & 0xff, bj = tij[t] >> 8;
+    if (g < E::NT && bj >= E::NPB) {
 #pragma unroll
-        for (int r = 0; r < TB; ++r) cb[bi * TB + r] = a[r][cj];
-      }
-      __syncthreads();
-      const double d = cb[j];
-      if (threadIdx.x == 0) {
-        const bool ok = (j < PSIGN) ? (d > 0.0) : (d < 0.0);
-        if (!ok && *bad == 0) *bad = j + 1;
-      }
-      if (act && bj >= pb) {
-        const double inv = 1.0 / d;
-        double li[TB], lc[TB];
-        const double2* rp = reinterpret_cast<const double2*>(cb + bi * TB);
-        const double2* cp = reinterpret_cast<const double2*>(cb + bj * TB);
-#pragma unroll
-        for (int r = 0; r < TB / 2; ++r) {
-          double2 v = rp[r];
-          li[2 * r] = v.x * inv;
-          li[2 * r + 1] = v.y * inv;
-          double2 w = cp[r];
-          lc[2 * r] = w.x;
-          lc[2 * r + 1] = w.y;
-        }
-        if (bj > pb) {
-#pragma unroll
-          for (int r = 0; r < TB; ++r)
-#pragma unroll
-            for (int c = 0; c < TB; ++c) a[r][c] = fma(-li[r], lc[c], a[r][c]);
-        } else {
-#pragma unroll
-          for (int r = 0; r < TB; ++r)
-#pragma unroll
-            for (int c = cj + 1; c < TB; ++c) a[r][c] = fma(-li[r], lc[c], a[r][c]);
-        }
+      for (int q = 0; q < 2; ++q) {
+        const int i = bi * 8 + gr - P::NPP, j = bj * 8 + 2 * tg + q - P::NPP;
+        if (j <= i && i < NC) out[pk(i, j)] = -acc[t][q];
       }
     }
   }
 }
 
+// expected pivot signs: [0, npos) > 0, [npos, np) < 0, padding unchecked
+__device__ __forceinline__ void init_expect(signed char* ex, int npp, int npos, int np) {
+  for (int i = threadIdx.x; i < npp; i += blockDim.x) ex[i] = i < npos ? 1 : (i < np ? -1 : 0);
+}
+
 // --------------------------------------------------------------- A5: microbench
 
-template <int NS, int NC, int TB>
-__global__ void __launch_bounds__(Grid2<NS + NC, TB>::THREADS)
+template <int NS, int NC, int W, int MINB = 1>
+__global__ void __launch_bounds__(32 * W, MINB)
     spd_schur_kernel(const double* __restrict__ A, const double* __restrict__ B,
                      double* __restrict__ S, int* __restrict__ info, int64_t batch) {
-  constexpr int N = NS + NC;
-  using G = Grid2<N, TB>;
+  using P = Pad<NS, NC, W>;
+  using E = typename P::E;
   constexpr int LA = npk(NS), LB = NS * NC, LS = npk(NC);
   static_assert((LA % 2) == 0 && (LB % 2) == 0, "16-byte bulk copies");
   extern __shared__ __align__(128) double smem[];
   double* sA = smem;
   double* sB = smem + LA;
-  __shared__ __align__(16) double col[2][G::NPAD];
+  double* work = smem + LA + LB;
   __shared__ __align__(8) uint64_t bar;
   __shared__ int bad;
-
-  int bi = 0, bj = 0;
-  const bool act = threadIdx.x < G::NT;
-  if (act) tile_of(threadIdx.x, bi, bj);
-
+  __shared__ int flag;
+  __shared__ signed char expect[P::NPP];
+  init_expect(expect, P::NPP, NS, NS);
   int64_t e = blockIdx.x;
   if (threadIdx.x == 0) {
     mbar_init(&bar, 1);
@@ -127,20 +124,15 @@ __global__ void __launch_bounds__(Grid2<NS + NC, TB>::THREADS)
   for (; e < batch; e += gridDim.x) {
     mbar_wait(&bar, phase);
     phase ^= 1;
-    double a[TB][TB];
-#pragma unroll
-    for (int r = 0; r < TB; ++r)
-#pragma unroll
-      for (int c = 0; c < TB; ++c) {
-        const int i = bi * TB + r, j = bj * TB + c;
-        double v = 0.0;
-        if (act && i < N && j <= i) {
-          if (i < NS) v = sA[pk(i, j)];
-          else if (j < NS) v = sB[j * NC + (i - NS)];
-        }
-        a[r][c] = v;
-      }
-    if (threadIdx.x == 0) bad = 0;
+    double acc[E::TPW][2];
+    int tij[E::TPW];
+    load_tiles<P, NS, NC>(acc, tij, [&](int i, int j) {
+      return i < NS ? sA[pk(i, j)] : (j < NS ? sB[j * NC + (i - NS)] : 0.0);
+    });
+    if (threadIdx.x == 0) {
+      bad = 0;
+      flag = -1;
+    }
     __syncthreads();
     const int64_t nxt = e + gridDim.x;
     if (threadIdx.x == 0 && nxt < batch) {   // prefetch the next element
@@ -148,16 +140,8 @@ __global__ void __launch_bounds__(Grid2<NS + NC, TB>::THREADS)
       bulk_g2s(sA, A + nxt * LA, LA * 8, &bar);
       bulk_g2s(sB, B + nxt * LB, LB * 8, &bar);
     }
-    eliminate<N, TB, 0, NS, NS>(a, bi, bj, act, col, &bad);
-    // trailing block holds -S
-    double* out = S + e * LS;
-#pragma unroll
-    for (int r = 0; r < TB; ++r)
-#pragma unroll
-      for (int c = 0; c < TB; ++c) {
-        const int i = bi * TB + r, j = bj * TB + c;
-        if (act && i < N && j >= NS && j <= i) out[pk(i - NS, j - NS)] = -a[r][c];
-      }
+    eliminate_tiles<E>(acc, tij, work, expect, &bad, &flag);
+    store_trailing<P, NC>(acc, tij, S + e * LS);
     __syncthreads();
     if (threadIdx.x == 0 && info) info[e] = bad;
   }
@@ -183,7 +167,7 @@ template <int K>
 __device__ __forceinline__ double mcs_entry(const double* rec, int i, int j) {
   using Z = Sizes<K>;
   using R = Record<K>;
-  constexpr int ns = Z::ns, nw = Z::nw, nu = Z::nu, c0 = Z::ns + Z::nw;
+  constexpr int ns = Z::ns, nu = Z::nu, c0 = Z::ns + Z::nw;
   if (i < ns) return rec[R::o_msig + i * ns + j];
   if (i < c0) return j < ns ? rec[R::o_bws + (i - ns) * ns + j] : 0.0;
   const int l = i - c0;
@@ -193,22 +177,22 @@ __device__ __forceinline__ double mcs_entry(const double* rec, int i, int j) {
   return (l < nu && m < nu) ? -rec[R::o_adiv + l * nu + m] : 0.0;
 }
 
-template <int K, int TB>
-__global__ void __launch_bounds__(Grid2<Sizes<K>::naug, TB>::THREADS)
+template <int K, int W, int MINB = 1>
+__global__ void __launch_bounds__(32 * W, MINB)
     condense_kernel(const double* __restrict__ recs, double* __restrict__ ST,
                     int* __restrict__ info, int64_t nt) {
   using Z = Sizes<K>;
   using R = Record<K>;
-  constexpr int N = Z::naug, NP = Z::ns + Z::nw;
-  using G = Grid2<N, TB>;
+  constexpr int NP = Z::ns + Z::nw, NC = Z::nloc;
+  using P = Pad<NP, NC, W>;
+  using E = typename P::E;
   extern __shared__ __align__(128) double srec[];
-  __shared__ __align__(16) double col[2][G::NPAD];
+  double* work = srec + R::len;
   __shared__ __align__(8) uint64_t bar;
   __shared__ int bad;
-
-  int bi = 0, bj = 0;
-  const bool act = threadIdx.x < G::NT;
-  if (act) tile_of(threadIdx.x, bi, bj);
+  __shared__ int flag;
+  __shared__ signed char expect[P::NPP];
+  init_expect(expect, P::NPP, Z::ns, NP);
   int64_t e = blockIdx.x;
   if (threadIdx.x == 0) {
     mbar_init(&bar, 1);
@@ -223,30 +207,21 @@ __global__ void __launch_bounds__(Grid2<Sizes<K>::naug, TB>::THREADS)
   for (; e < nt; e += gridDim.x) {
     mbar_wait(&bar, phase);
     phase ^= 1;
-    double a[TB][TB];
-#pragma unroll
-    for (int r = 0; r < TB; ++r)
-#pragma unroll
-      for (int c = 0; c < TB; ++c) {
-        const int i = bi * TB + r, j = bj * TB + c;
-        a[r][c] = (act && i < N && j <= i) ? mcs_entry<K>(srec, i, j) : 0.0;
-      }
-    if (threadIdx.x == 0) bad = 0;
+    double acc[E::TPW][2];
+    int tij[E::TPW];
+    load_tiles<P, NP, NC>(acc, tij, [&](int i, int j) { return mcs_entry<K>(srec, i, j); });
+    if (threadIdx.x == 0) {
+      bad = 0;
+      flag = -1;
+    }
     __syncthreads();
     const int64_t nxt = e + gridDim.x;
     if (threadIdx.x == 0 && nxt < nt) {
       mbar_expect_tx(&bar, R::len * 8);
       bulk_g2s(srec, recs + nxt * R::len, R::len * 8, &bar);
     }
-    eliminate<N, TB, 0, NP, Z::ns>(a, bi, bj, act, col, &bad);
-    double* out = ST + e * R::st_len;
-#pragma unroll
-    for (int r = 0; r < TB; ++r)
-#pragma unroll
-      for (int c = 0; c < TB; ++c) {
-        const int i = bi * TB + r, j = bj * TB + c;
-        if (act && i < N && j >= NP && j <= i) out[pk(i - NP, j - NP)] = -a[r][c];
-      }
+    eliminate_tiles<E>(acc, tij, work, expect, &bad, &flag);
+    store_trailing<P, NC>(acc, tij, ST + e * R::st_len);
     __syncthreads();
     if (threadIdx.x == 0 && info) info[e] = bad;
   }
@@ -291,26 +266,27 @@ static int persistent_grid(Kern k, int threads, size_t smem, int64_t n) {
   return static_cast<int>(n < g ? n : g);
 }
 
-template <int NS, int NC, int TB>
+template <int NS, int NC, int W, int MINB = 1>
 static int launch_spd_schur(const double* A, const double* B, double* S, int* info, int64_t batch,
                             cudaStream_t st) {
-  using G = Grid2<NS + NC, TB>;
-  auto kern = spd_schur_kernel<NS, NC, TB>;
-  const size_t smem = (npk(NS) + NS * NC) * sizeof(double);
+  using P = Pad<NS, NC, W>;
+  auto kern = spd_schur_kernel<NS, NC, W, MINB>;
+  const size_t smem = (npk(NS) + NS * NC + P::E::SMEM_WORK) * sizeof(double);
   cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-  const int grid = persistent_grid(kern, G::THREADS, smem, batch);
-  kern<<<grid, G::THREADS, smem, st>>>(A, B, S, info, batch);
+  const int grid = persistent_grid(kern, 32 * W, smem, batch);
+  kern<<<grid, 32 * W, smem, st>>>(A, B, S, info, batch);
   return launch_status();
 }
 
-template <int K, int TB>
+template <int K, int W, int MINB = 1>
 static int launch_condense(const double* recs, double* ST, int* info, int64_t nt, cudaStream_t st) {
-  using G = Grid2<Sizes<K>::naug, TB>;
-  auto kern = condense_kernel<K, TB>;
-  const size_t smem = Record<K>::len * sizeof(double);
+  using Z = Sizes<K>;
+  using P = Pad<Z::ns + Z::nw, Z::nloc, W>;
+  auto kern = condense_kernel<K, W, MINB>;
+  const size_t smem = (Record<K>::len + P::E::SMEM_WORK) * sizeof(double);
   cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-  const int grid = persistent_grid(kern, G::THREADS, smem, nt);
-  kern<<<grid, G::THREADS, smem, st>>>(recs, ST, info, nt);
+  const int grid = persistent_grid(kern, 32 * W, smem, nt);
+  kern<<<grid, 32 * W, smem, st>>>(recs, ST, info, nt);
   return launch_status();
 }
 
@@ -322,8 +298,8 @@ MCS_API int mcs_spd_schur_batched(int n, int m, int64_t batch, const double* A_p
                                   const double* B, double* S_packed, int* info, void* stream) {
   if (batch <= 0) return 0;
   auto st = static_cast<cudaStream_t>(stream);
-  if (n == 60 && m == 36) return launch_spd_schur<60, 36, 8>(A_packed_lower, B, S_packed, info, batch, st);
-  if (n == 8 && m == 4) return launch_spd_schur<8, 4, 4>(A_packed_lower, B, S_packed, info, batch, st);
+  if (n == 60 && m == 36) return launch_spd_schur<60, 36, 8, 2>(A_packed_lower, B, S_packed, info, batch, st);
+  if (n == 8 && m == 4) return launch_spd_schur<8, 4, 2>(A_packed_lower, B, S_packed, info, batch, st);
   return -1000;  // unsupported shape (compiled instantiations only)
 }
 
@@ -354,11 +330,11 @@ MCS_API int mcs_condense(int k, int64_t nt, const double* records, double* S_pac
   if (nt <= 0) return 0;
   auto st = static_cast<cudaStream_t>(stream);
   switch (k) {
-    case 2: return launch_condense<2, 4>(records, S_packed, info, nt, st);
-    case 3: return launch_condense<3, 8>(records, S_packed, info, nt, st);
-    case 4: return launch_condense<4, 8>(records, S_packed, info, nt, st);
-    case 5: return launch_condense<5, 8>(records, S_packed, info, nt, st);
-    case 6: return launch_condense<6, 8>(records, S_packed, info, nt, st);
+    case 2: return launch_condense<2, 4, 4>(records, S_packed, info, nt, st);
+    case 3: return launch_condense<3, 8, 2>(records, S_packed, info, nt, st);
+    case 4: return launch_condense<4, 8, 2>(records, S_packed, info, nt, st);
+    case 5: return launch_condense<5, 12>(records, S_packed, info, nt, st);
+    case 6: return launch_condense<6, 16>(records, S_packed, info, nt, st);
   }
   return -1000;
 }

@@ -1,0 +1,40 @@
+// latency of one 8x8 warp Gauss-Jordan inverse (elim_dmma.cuh)
+#include "../paper_2207_08481_b200/csrc/elim_dmma.cuh"
+#include <cstdio>
+using namespace mcs;
+__global__ void k(long long* out, int reps) {
+  __shared__ double M[8][8 * 16];
+  __shared__ double P[8][TSZ];
+  __shared__ signed char ex[8];
+  const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (threadIdx.x < 8) ex[threadIdx.x] = 1;
+  __syncthreads();
+  long long t0 = clock64();
+  int bad = 0;
+  for (int r = 0; r < reps; ++r) {
+    for (int q = lane; q < 64; q += 32) M[w][(q / 8) * 16 + q % 8] = (q / 8 == q % 8) ? 10.0 + r : 0.1 * ((q * 7) % 5);
+    __syncwarp();
+    bad += warp_inverse8(M[w], P[w], ex); __syncwarp();
+  }
+  long long t1 = clock64();
+  if (lane == 0) out[blockIdx.x * 32 + w] = (t1 - t0) / reps;
+  if (bad == 12345) out[0] = P[w][3];
+}
+__global__ void rcpk(long long* out, double x) {
+  long long t0 = clock64();
+  for (int i = 0; i < 1000; ++i) x = rcp64(x) + 1.0;
+  long long t1 = clock64();
+  out[0] = (t1 - t0) / 1000;
+  if (x == 5.0) out[1] = 1;
+}
+int main() {
+  long long* d; cudaMalloc(&d, 4096 * 8); long long h[64];
+  for (int nw : {1, 8}) {
+    k<<<1, 32 * nw>>>(d, 200); k<<<1, 32 * nw>>>(d, 200);
+    cudaMemcpy(h, d, 64 * 8, cudaMemcpyDeviceToHost);
+    printf("warps=%d: GJ8 inverse %lld clk\n", nw, h[0]);
+  }
+  rcpk<<<1, 32>>>(d, 3.0); cudaMemcpy(h, d, 16, cudaMemcpyDeviceToHost);
+  printf("rcp64+add dependent chain: %lld clk\n", h[0]);
+  printf("%s\n", cudaGetErrorString(cudaGetLastError()));
+}
