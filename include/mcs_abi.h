@@ -1,0 +1,124 @@
+/* mcs_abi.h -- C ABI of libmcsgpu.so, the B200 (sm_100a) kernels behind the
+ * condensed MCS Stokes hot path (arXiv 2207.08481; reference package
+ * `mcstokes`, pure NumPy/SciPy).
+ *
+ * Conventions
+ *   - every pointer is a DEVICE pointer owned by the caller (torch tensors);
+ *   - `stream` is a cudaStream_t; every call is asynchronous on it;
+ *   - return 0 = ok, < 0 = CUDA error (-cudaError_t) or unsupported
+ *     arguments (-1000); per-element failures go to `info[e]` (0 = ok,
+ *     otherwise the 1-based failing pivot), mapped to the reference's
+ *     exceptions by the Python layer;
+ *   - float64 everywhere; int32 index arrays;
+ *   - packed symmetric = lower triangle, row-major, (i,j) at i(i+1)/2 + j,
+ *     per-element stride padded to an even number of doubles;
+ *   - dof codes: 2*free_index + (sign < 0), or -1 for a constrained dof.
+ *
+ * No function keeps global mutable state except the coarse-solve shared
+ * memory size (mcs_mf_set_max_own, monotone).  There is no CPU fallback.
+ */
+#ifndef MCS_ABI_H
+#define MCS_ABI_H
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* ---- element blocks (replaces assembly.py:49-96 assemble_element_blocks /
+ *      all_element_blocks): rec[e][q] = sum_p W[e][widx[p]] * coef[p] over the
+ *      CSR program of refblocks.py.  W: [nt][nwgt] geometry weights. */
+int mcs_element_blocks(int64_t nt, int nwgt, const double* W, int reclen, const int* prog_ptr,
+                       const int* prog_widx, const double* prog_coef, double* records,
+                       void* stream);
+
+/* record layout / packed strides for degree k (2..6) */
+int mcs_record_len(int k);
+int mcs_st_stride(int k);
+int mcs_ext_stride(int k);
+int mcs_sd_stride(int k);
+
+/* ---- sigma/omega condensation (replaces condensation.py:159-177, the LU of
+ *      [[-msig, bws^T],[bws, 0]] and S_T = adiv - Bsig M^-1 Bsig^T per element).
+ *      records: [nt][mcs_record_len(k)], S_packed: [nt][mcs_st_stride(k)]. */
+int mcs_condense(int k, int64_t nt, const double* records, double* S_packed, int* info,
+                 void* stream);
+
+/* ---- double Schur (replaces condensation.py:207-226 double_schur per
+ *      element): ext = [X = S_oo^-1 S_oc (n_int x ncpl) | S_oo^-1 packed],
+ *      Sd_packed = S_cc - S_co X. */
+int mcs_double_schur(int k, int64_t nt, const double* S_packed, double* ext, double* Sd_packed,
+                     int* info, void* stream);
+
+/* ---- config-5 microbench SPD Schur S = B^T A^-1 B (reference idiom
+ *      condensation.py:216-224, cho_factor / cho_solve / B^T X).
+ *      A_packed_lower: [batch][n(n+1)/2], B: [batch][n][m], S: [batch][m(m+1)/2].
+ *      Compiled shapes: (60, 36), (8, 4). */
+int mcs_spd_schur_batched(int n, int m, int64_t batch, const double* A_packed_lower,
+                          const double* B, double* S_packed, int* info, void* stream);
+
+/* ---- condensed operator apply (replaces driver.py:138,144 `S_free @ v`, and
+ *      the S_d CSR of driver.py:96): y = sum_T P^T D S_T D P x over free dofs.
+ *      which = 0: S_T (codes [nt][nloc]); which = 1: Sd_T (codes [nt][ncpl]).
+ *      y (length ny) is overwritten. */
+int mcs_apply_elem(int k, int which, int64_t nt, const double* M_packed, const int* codes,
+                   const double* x, double* y, int64_t ny, void* stream);
+
+/* ---- ExtendedAsp outer factors (replaces preconditioners.py:353-378):
+ *      restrict: bubble[e] = S_oo^-1 r_o, acc = sum X^T r_o (signed; acc
+ *      overwritten, length nacc); prolong: out[bubble dofs] = bubble - X z_c. */
+int mcs_ext_restrict(int k, int64_t nt, const double* ext, const int* bubble_idx,
+                     const int* cpl_codes, const double* r, double* bubble, double* acc,
+                     int64_t nacc, void* stream);
+int mcs_ext_prolong(int k, int64_t nt, const double* ext, const int* bubble_idx,
+                    const int* cpl_codes, const double* zc, const double* bubble, double* out,
+                    void* stream);
+/* w[j] = r[map[j]] - acc[j];  out[map[j]] = z[j] */
+int mcs_gather_sub(int n, const double* r, const int* map, const double* acc, double* w,
+                   void* stream);
+int mcs_scatter(int n, const double* z, const int* map, double* out, void* stream);
+
+/* ---- facet-block Jacobi on S_d (replaces preconditioners.py:177-206 variant
+ *      "jacobi" with facet_blocks_schur :266-280).  slots: [nblk][4] =
+ *      (t0, le0, t1, le1); binv: [npk(2k+1)][nblk] SoA; bidx: [2k+1][nblk]. */
+int mcs_jacobi_setup(int k, int nblk, const double* Sd_packed, int sd_stride, const int* cpl_codes,
+                     const int* slots, double* binv, int* bidx, int* bsize, int* info,
+                     void* stream);
+int mcs_jacobi_apply(int k, int nblk, const double* binv, const int* bidx, const double* r,
+                     double* x, double scale_inv, void* stream);
+
+/* ---- CSR SpMV y = alpha A x + beta y (replaces the E_c / E_c^T products of
+ *      preconditioners.py:316-317); lanes in {1, 4, 8, 32} per row. */
+int mcs_csr_spmv(int nrows, const int* ptr, const int* col, const double* val, const double* x,
+                 double* y, double alpha, double beta, int lanes, void* stream);
+
+/* ---- exact coarse solve (replaces CoarseSolver.solve, SuperLU,
+ *      preconditioners.py:111-118,165-171): dense explicit inverse (small)
+ *      or multifrontal triangular solves (per tree level, see coarse.py). */
+int mcs_dense_gemv(int n, const double* A, const double* x, double* y, void* stream);
+int mcs_mf_set_max_own(int max_ns);
+int mcs_mf_forward_own(int ntasks, const int* tasks, const void* nodes, const double* mats,
+                       const int* src_t, const double* out, const int* perm, const double* b,
+                       double* y, void* stream);
+int mcs_mf_forward_out(int ntasks, const int* tasks, const void* nodes, const double* mats,
+                       const int* src_o, const double* y, double* out, void* stream);
+int mcs_mf_backward(int ntasks, const int* tasks, const void* nodes, const double* mats,
+                    const int* B, const double* y, const double* xp, double* s, void* stream);
+int mcs_mf_backward2(int ntasks, const int* tasks, const void* nodes, const double* mats,
+                     const double* s, const int* perm, double* xp, double* x, void* stream);
+
+/* ---- PCG vector algebra (replaces krylov.py:103-137 NumPy ops); deterministic
+ *      reductions into device scalars sc[]. */
+int mcs_reduce_workspace_len(void);
+int mcs_dot(int64_t n, const double* x, const double* y, double* partials, unsigned* counter,
+            double* out, void* stream);
+int mcs_cg_update(int64_t n, double* x, double* r, const double* p, const double* Ap, double* sc,
+                  int rz, int pap, int rr, double* partials, unsigned* counter, void* stream);
+int mcs_xpby(int64_t n, const double* z, double* p, const double* sc, int num, int den,
+             void* stream);
+int mcs_axpby(int64_t n, double a, const double* x, double b, double* y, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* MCS_ABI_H */
