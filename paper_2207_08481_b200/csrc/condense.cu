@@ -19,7 +19,7 @@
 // async copy (TMA engine, cp.async.bulk + mbarrier) issued as soon as the
 // current element's tiles are in registers, so HBM traffic overlaps the
 // elimination of the current element.
-#include "elim_dmma.cuh"
+#include "elim_v3.cuh"
 
 namespace mcs {
 
@@ -227,6 +227,109 @@ __global__ void __launch_bounds__(32 * W, MINB)
   }
 }
 
+// ------------------------------------------- v3 kernels (compile-time roles)
+
+template <int NS, int NC, int W, int MINB>
+__global__ void __launch_bounds__(32 * W, MINB)
+    spd_schur_v3(const double* __restrict__ A, const double* __restrict__ B,
+                 double* __restrict__ S, int* __restrict__ info, int64_t batch) {
+  using P = Pad<NS, NC, W>;
+  using G = v3::Geo<P::NB, P::NPB, W>;
+  constexpr int LA = npk(NS), LB = NS * NC, LS = npk(NC);
+  extern __shared__ __align__(128) double smem[];
+  __shared__ int bad;
+  __shared__ signed char expect[P::NPP];
+  init_expect(expect, P::NPP, NS, NS);
+  const v3::Smem<G> sm{smem};
+  const int warp = threadIdx.x >> 5;
+  for (int64_t e = blockIdx.x; e < batch; e += gridDim.x) {
+    if (threadIdx.x == 0) bad = 0;
+    __syncthreads();
+    const double* Ae = A + e * LA;
+    const double* Be = B + e * LB;
+    double* Se = S + e * LS;
+    auto load = [&](int i, int j) {
+      return v3::padded_entry<NS, NC, P::NPP>(i, j, [&](int ri, int rj) {
+        return ri < NS ? __ldg(Ae + pk(ri, rj)) : (rj < NS ? __ldg(Be + rj * NC + (ri - NS)) : 0.0);
+      });
+    };
+    auto store = [&](int i, int j, double v) {
+      i -= P::NPP;
+      j -= P::NPP;
+      if (j <= i && i < NC) Se[pk(i, j)] = -v;
+    };
+    v3::dispatch<G>(warp, load, store, sm, expect, &bad);
+    __syncthreads();
+    if (threadIdx.x == 0 && info) info[e] = bad;
+  }
+}
+
+template <int K, int W, int MINB>
+__global__ void __launch_bounds__(32 * W, MINB)
+    condense_v3(const double* __restrict__ recs, double* __restrict__ ST, int* __restrict__ info,
+                int64_t nt) {
+  using Z = Sizes<K>;
+  using R = Record<K>;
+  constexpr int NP = Z::ns + Z::nw, NC = Z::nloc;
+  using P = Pad<NP, NC, W>;
+  using G = v3::Geo<P::NB, P::NPB, W>;
+  extern __shared__ __align__(128) double smem[];
+  __shared__ int bad;
+  __shared__ signed char expect[P::NPP];
+  init_expect(expect, P::NPP, Z::ns, NP);
+  const v3::Smem<G> sm{smem};
+  const int warp = threadIdx.x >> 5;
+  for (int64_t e = blockIdx.x; e < nt; e += gridDim.x) {
+    if (threadIdx.x == 0) bad = 0;
+    __syncthreads();
+    const double* rec = recs + e * R::len;
+    double* Se = ST + e * R::st_len;
+    auto load = [&](int i, int j) {
+      return v3::padded_entry<NP, NC, P::NPP>(i, j, [&](int ri, int rj) {
+        return mcs_entry<K>(rec, ri, rj);
+      });
+    };
+    auto store = [&](int i, int j, double v) {
+      i -= P::NPP;
+      j -= P::NPP;
+      if (j <= i && i < NC) Se[pk(i, j)] = -v;
+    };
+    v3::dispatch<G>(warp, load, store, sm, expect, &bad);
+    __syncthreads();
+    if (threadIdx.x == 0 && info) info[e] = bad;
+  }
+}
+
+template <class Kern>
+static int persistent_grid(Kern k, int threads, size_t smem, int64_t n);
+
+template <int NS, int NC, int W, int MINB>
+static int launch_spd_schur_v3(const double* A, const double* B, double* S, int* info,
+                               int64_t batch, cudaStream_t st) {
+  using P = Pad<NS, NC, W>;
+  using G = v3::Geo<P::NB, P::NPB, W>;
+  auto kern = spd_schur_v3<NS, NC, W, MINB>;
+  const size_t smem = G::SMEM * sizeof(double);
+  cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  const int grid = persistent_grid(kern, 32 * W, smem, batch);
+  kern<<<grid, 32 * W, smem, st>>>(A, B, S, info, batch);
+  return launch_status();
+}
+
+template <int K, int W, int MINB>
+static int launch_condense_v3(const double* recs, double* ST, int* info, int64_t nt,
+                              cudaStream_t st) {
+  using Z = Sizes<K>;
+  using P = Pad<Z::ns + Z::nw, Z::nloc, W>;
+  using G = v3::Geo<P::NB, P::NPB, W>;
+  auto kern = condense_v3<K, W, MINB>;
+  const size_t smem = G::SMEM * sizeof(double);
+  cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  const int grid = persistent_grid(kern, 32 * W, smem, nt);
+  kern<<<grid, 32 * W, smem, st>>>(recs, ST, info, nt);
+  return launch_status();
+}
+
 // ---------------------------------------------- A1: element blocks on the GPU
 // rec[e][q] = sum_{p in prog[q]} W[e][widx[p]] * coef[p]   (refblocks.py)
 __global__ void element_blocks_kernel(const double* __restrict__ W, int nwgt,
@@ -258,6 +361,7 @@ static int num_sms() {
 
 template <class Kern>
 static int persistent_grid(Kern k, int threads, size_t smem, int64_t n) {
+  // (declared above for the v3 launchers)
   int per_sm = 0;
   if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k, threads, smem) != cudaSuccess ||
       per_sm < 1)
@@ -298,7 +402,7 @@ MCS_API int mcs_spd_schur_batched(int n, int m, int64_t batch, const double* A_p
                                   const double* B, double* S_packed, int* info, void* stream) {
   if (batch <= 0) return 0;
   auto st = static_cast<cudaStream_t>(stream);
-  if (n == 60 && m == 36) return launch_spd_schur<60, 36, 8, 2>(A_packed_lower, B, S_packed, info, batch, st);
+  if (n == 60 && m == 36) return launch_spd_schur_v3<60, 36, 2, 4>(A_packed_lower, B, S_packed, info, batch, st);
   if (n == 8 && m == 4) return launch_spd_schur<8, 4, 2>(A_packed_lower, B, S_packed, info, batch, st);
   return -1000;  // unsupported shape (compiled instantiations only)
 }
@@ -330,9 +434,9 @@ MCS_API int mcs_condense(int k, int64_t nt, const double* records, double* S_pac
   if (nt <= 0) return 0;
   auto st = static_cast<cudaStream_t>(stream);
   switch (k) {
-    case 2: return launch_condense<2, 4, 4>(records, S_packed, info, nt, st);
-    case 3: return launch_condense<3, 8, 2>(records, S_packed, info, nt, st);
-    case 4: return launch_condense<4, 8, 2>(records, S_packed, info, nt, st);
+    case 2: return launch_condense_v3<2, 2, 6>(records, S_packed, info, nt, st);
+    case 3: return launch_condense_v3<3, 2, 4>(records, S_packed, info, nt, st);
+    case 4: return launch_condense_v3<4, 2, 4>(records, S_packed, info, nt, st);
     case 5: return launch_condense<5, 12>(records, S_packed, info, nt, st);
     case 6: return launch_condense<6, 16>(records, S_packed, info, nt, st);
   }

@@ -38,7 +38,7 @@ struct Elim {
   static constexpr int TPW = (NT + W - 1) / W;
   static constexpr int THREADS = 32 * W;
   // dynamic shared memory (doubles) besides the input stage
-  static constexpr int SMEM_WORK = 4 * NB * TSZ + 2 * TSZ + 128;
+  static constexpr int SMEM_WORK = 4 * NB * TSZ + 2 * TSZ + 8 * 18;
 
   // column-major lower tile order: g -> (bi, bj)
   __device__ static void tile_of(int g, int& bi, int& bj) {
@@ -69,42 +69,68 @@ __device__ __forceinline__ double rcp64(double x) {
   return fma(fma(-x, y, 1.0), y, y);
 }
 
-// Invert the 8x8 diagonal block staged in M[r*16 + c] (c < 8) by one warp
-// with Gauss-Jordan on the augmented [M | I] held in REGISTERS (lane = row r,
-// a quarter of the 16 columns); pivots, multipliers and pivot rows travel by
-// shuffles, so each of the 8 steps is one short dependency chain
-// (shuffle -> reciprocal -> FMA) with no shared-memory traffic.  Writes the
-// inverse to P (stride TROW).  expect[j] in {+1, -1, 0}: required pivot sign
-// (0 = padding, only non-zero checked).  Returns the first offending pivot
-// (1-based) or 0.
-__device__ __forceinline__ int warp_inverse8(const double* M, double* P, const signed char* expect) {
+// Invert the 8x8 diagonal block held by one warp in the DMMA accumulator
+// layout (v0, v1 = entries (lane/4, 2*(lane%4) + {0,1})).  Gauss-Jordan on
+// the augmented [Q | I] in the fraction-free (Bareiss) form
+//     R_i <- (p_j R_i - R_i[j] R_j) / p_{j-1}      (i != j),
+// lane = row r and a quarter of the 16 columns, rows exchanged through a
+// small padded shared-memory scratch W (8 x GJS doubles).  The dependency
+// chain per pivot is load -> FMA -> multiply -> store: the reciprocal of p_j
+// is formed one step ahead, off the chain, and the pivot-sign checks run
+// after the loop.  The pivot ratios p_j / p_{j-1} are the LDL^T pivots
+// (checked against expect[j] in {+1, -1, 0}); at the end the left block is
+// p_7 I and Q^-1 = right / p_7.  Writes Q^-1 to P (stride TROW); returns the
+// first offending pivot (1-based) or 0.
+constexpr int GJS = 18;   // scratch row stride (doubles)
+
+__device__ __forceinline__ int warp_inverse8(double v0, double v1, double* W, double* P,
+                                             const signed char* expect) {
   const int lane = threadIdx.x & 31;
-  const int r = lane >> 2, qd = lane & 3;
+  const int r = lane >> 2, qd = lane & 3, c0 = 4 * qd;
+  // C layout -> scratch (left block), identity on the right
+  W[r * GJS + 2 * qd] = v0;
+  W[r * GJS + 2 * qd + 1] = v1;
+  W[r * GJS + 8 + 2 * qd] = (2 * qd == r) ? 1.0 : 0.0;
+  W[r * GJS + 8 + 2 * qd + 1] = (2 * qd + 1 == r) ? 1.0 : 0.0;
+  __syncwarp();
   double m[4];
 #pragma unroll
-  for (int q = 0; q < 4; ++q) m[q] = qd < 2 ? M[r * 16 + 4 * qd + q] : (4 * (qd - 2) + q == r ? 1.0 : 0.0);
-  int badj = 0;
+  for (int q = 0; q < 4; ++q) m[q] = W[r * GJS + c0 + q];
+  double piv[8];
+  double inv_prev = 1.0;
 #pragma unroll
   for (int j = 0; j < 8; ++j) {
-    const int src = 4 * j;                      // lanes holding row j
-    const double piv = __shfl_sync(0xffffffffu, m[j & 3], src + (j >> 2));
-    const double mr = __shfl_sync(0xffffffffu, m[j & 3], (lane & ~3) + (j >> 2));
+    const double p = W[j * GJS + j];
+    const double mr = W[r * GJS + j];
     double rj[4];
 #pragma unroll
-    for (int q = 0; q < 4; ++q) rj[q] = __shfl_sync(0xffffffffu, m[q], src + qd);
-    const int s = expect[j];
-    const bool ok = s > 0 ? piv > 0.0 : (s < 0 ? piv < 0.0 : piv != 0.0);
-    if (!ok && badj == 0) badj = j + 1;
-    const double inv = rcp64(piv);
+    for (int q = 0; q < 4; ++q) rj[q] = W[j * GJS + c0 + q];
+    piv[j] = p;
+    __syncwarp();
+    const bool keep = (r == j);
 #pragma unroll
     for (int q = 0; q < 4; ++q) {
-      const double v = rj[q] * inv;
-      m[q] = (r == j) ? v : fma(-mr, v, m[q]);
+      const double u = fma(p, m[q], -mr * rj[q]) * inv_prev;
+      m[q] = keep ? m[q] : u;
+      W[r * GJS + c0 + q] = m[q];
     }
+    inv_prev = rcp64(p);
+    __syncwarp();
+  }
+  int badj = 0;
+  bool neg_prev = false;
+#pragma unroll
+  for (int j = 0; j < 8; ++j) {
+    const bool neg = piv[j] < 0.0;
+    const bool pos_ratio = (neg == neg_prev) && piv[j] != 0.0;
+    const int s = expect[j];
+    const bool ok = s > 0 ? pos_ratio : (s < 0 ? (!pos_ratio && piv[j] != 0.0) : piv[j] != 0.0);
+    if (!ok && badj == 0) badj = j + 1;
+    neg_prev = neg;
   }
   if (qd >= 2) {
 #pragma unroll
-    for (int q = 0; q < 4; ++q) P[r * TROW + 4 * (qd - 2) + q] = m[q];
+    for (int q = 0; q < 4; ++q) P[r * TROW + c0 - 8 + q] = m[q] * inv_prev;
   }
   __syncwarp();
   return badj;
@@ -146,7 +172,7 @@ __device__ __forceinline__ void eliminate_tiles(double (&acc)[E::TPW][2], const 
   double* Rb = work;                       // [2][NB] tiles
   double* Zb = work + 2 * E::NB * TSZ;     // [2][NB] tiles
   double* Pb = Zb + 2 * E::NB * TSZ;       // [2] tiles
-  double* Mw = Pb + 2 * TSZ;               // 8 x 16 (Gauss-Jordan scratch)
+  double* Gw = Pb + 2 * TSZ;               // 8 x GJS Gauss-Jordan scratch
 #ifdef MCS_PHASE_PROF
   long long prof[8] = {0, 0, 0, 0, 0, 0, 0, 0};
   long long tprev = pclock();
@@ -155,15 +181,15 @@ __device__ __forceinline__ void eliminate_tiles(double (&acc)[E::TPW][2], const 
   auto Z_ = [&](int p, int i) { return Zb + ((p & 1) * E::NB + i) * TSZ; };
   auto P_ = [&](int p) { return Pb + (p & 1) * TSZ; };
 
-  // stage the diagonal tile of column c (C layout -> M rows, stride 16)
+  // the diagonal tile of column c, kept aside by its owner until inversion
+  double dv0 = 0.0, dv1 = 0.0;
   auto stage_diag = [&](double v0, double v1) {
-    Mw[gr * 16 + 2 * tg] = v0;
-    Mw[gr * 16 + 2 * tg + 1] = v1;
+    dv0 = v0;
+    dv1 = v1;
   };
-  // owner warp: invert the staged block, publish Pinv_c, raise the flag
+  // owner warp: invert the diagonal tile, publish Pinv_c, release the others
   auto diag_inverse = [&](int c) {
-    __syncwarp();
-    const int b = warp_inverse8(Mw, P_(c), expect_all + 8 * c);
+    const int b = warp_inverse8(dv0, dv1, Gw, P_(c), expect_all + 8 * c);
     if (lane == 0 && b && *bad == 0) *bad = 8 * c + b;
     __threadfence_block();
     named_arrive(1, E::THREADS);       // Pinv_c published

@@ -12,9 +12,9 @@ __global__ void k(long long* out, int reps) {
   long long t0 = clock64();
   int bad = 0;
   for (int r = 0; r < reps; ++r) {
-    for (int q = lane; q < 64; q += 32) M[w][(q / 8) * 16 + q % 8] = (q / 8 == q % 8) ? 10.0 + r : 0.1 * ((q * 7) % 5);
-    __syncwarp();
-    bad += warp_inverse8(M[w], P[w], ex); __syncwarp();
+    const int g = lane >> 2, t2 = 2 * (lane & 3);
+    double v0 = (g == t2) ? 10.0 + r : 0.1 * ((g * 8 + t2) % 5), v1 = (g == t2 + 1) ? 10.0 + r : 0.1 * ((g * 8 + t2 + 1) % 5);
+    bad += warp_inverse8(v0, v1, &M[w][0], P[w], ex);
   }
   long long t1 = clock64();
   if (lane == 0) out[blockIdx.x * 32 + w] = (t1 - t0) / reps;
