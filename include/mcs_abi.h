@@ -14,8 +14,7 @@
  *     per-element stride padded to an even number of doubles;
  *   - dof codes: 2*free_index + (sign < 0), or -1 for a constrained dof.
  *
- * No function keeps global mutable state except the coarse-solve shared
- * memory size (mcs_mf_set_max_own, monotone).  There is no CPU fallback.
+ * No function keeps global mutable state.  There is no CPU fallback.
  */
 #ifndef MCS_ABI_H
 #define MCS_ABI_H
@@ -96,16 +95,19 @@ int mcs_csr_spmv(int nrows, const int* ptr, const int* col, const double* val, c
  *      preconditioners.py:111-118,165-171): dense explicit inverse (small)
  *      or multifrontal triangular solves (per tree level, see coarse.py). */
 int mcs_dense_gemv(int n, const double* A, const double* x, double* y, void* stream);
-int mcs_mf_set_max_own(int max_ns);
-int mcs_mf_forward_own(int ntasks, const int* tasks, const void* nodes, const double* mats,
-                       const int* src_t, const double* out, const int* perm, const double* b,
-                       double* y, void* stream);
-int mcs_mf_forward_out(int ntasks, const int* tasks, const void* nodes, const double* mats,
-                       const int* src_o, const double* y, double* out, void* stream);
-int mcs_mf_backward(int ntasks, const int* tasks, const void* nodes, const double* mats,
-                    const int* B, const double* y, const double* xp, double* s, void* stream);
-int mcs_mf_backward2(int ntasks, const int* tasks, const void* nodes, const double* mats,
-                     const double* s, const int* perm, double* xp, double* x, void* stream);
+/* one kernel per separator-tree level and direction, one CTA per node
+ * (node table, packed factors and gather sources built by coarse.py) */
+int mcs_mf_forward(int nnodes, const int* level_nodes, const void* nodes, const double* mats,
+                   const int* src_t, const int* src_o, const int* perm, const double* b,
+                   double* y, double* out, void* stream);
+int mcs_mf_backward(int nnodes, const int* level_nodes, const void* nodes, const double* mats,
+                    const int* B, const int* perm, const double* y, double* xp, double* x,
+                    void* stream);
+/* top of the tree (t dofs): g = b_T - frontier updates, x_T = Sinv g with the
+ * dense inverse of the top Schur complement (= (A^-1)_TT) */
+int mcs_mf_top(int t, const int* T, const int* perm, const double* b, const int* ptr,
+               const int* src, const double* out, double* g, const double* Sinv, double* xp,
+               double* x, void* stream);
 
 /* ---- PCG vector algebra (replaces krylov.py:103-137 NumPy ops); deterministic
  *      reductions into device scalars sc[]. */

@@ -15,10 +15,10 @@ host once per mesh and runs both triangular solves on the GPU:
   Linv = L_SS^-1 and W (and their transposes), so every solve step is a
   dense, coalesced GEMV (warp per row) instead of a latency-bound triangular
   recurrence;
-* GPU schedule: per tree level 2 kernels forward (y_S = Linv (b_S - child
-  updates); out_B = W y_S + pass-through) and 2 backward
-  (s = y_S - W^T x_B; x_S = Linv^T s); child contributions are gathered in a
-  fixed order, so the solve is deterministic.
+* GPU schedule: one kernel per tree level and direction, one CTA per node:
+  forward y_S = Linv (b_S - child updates), out_B = W y_S + pass-through;
+  backward s = y_S - W^T x_B, x_S = Linv^T s.  Child contributions are
+  gathered in a fixed order, so the solve is deterministic.
 
 Small problems (n <= DENSE_MAX) use an explicit dense inverse instead.
 """
@@ -35,8 +35,8 @@ import scipy.sparse as sp
 from . import _abi, engine
 
 DENSE_MAX = 1024
-LEAF = 384
-ROWS_PER_TASK = 64
+LEAF = 96
+TOP_MAX = 4096      # dofs of the separator-tree top handled by a dense inverse
 
 
 @dataclass
@@ -94,6 +94,7 @@ class MultifrontalFactor:
     perm: np.ndarray                 # elimination position -> original dof
     nodes: list
     levels: list                     # node indices per height
+    A: object = None                 # the matrix (original dof order)
     dev: dict = None
 
 
@@ -146,43 +147,49 @@ def multifrontal_factor(A: sp.csr_matrix, xy: np.ndarray, leaf: int = LEAF) -> M
         if nb:
             updates[id(nd)] = F[ns:, ns:] - W @ W.T
         nd.Linv = sla.solve_triangular(L, np.eye(ns), lower=True, check_finite=False) if ns else L
+        nd.L = L
         nd.W = W
     H = max(heights) + 1
     levels = [[i for i, h in enumerate(heights) if h == lv] for lv in range(H)]
-    return MultifrontalFactor(n=n, perm=perm, nodes=nodes, levels=levels)
+    return MultifrontalFactor(n=n, perm=perm, nodes=nodes, levels=levels, A=A)
 
 
 def _upload_multifrontal(F: MultifrontalFactor):
-    """Flatten the factor into device arrays + per-level task lists."""
+    """Flatten the factor into device arrays + per-level node lists.
+
+    Per node: Linv packed lower (row-major), Linv^T packed upper (row-major),
+    W (nb x ns) and W^T (ns x nb); gather sources: for every own position
+    and every boundary row, the (<= 2) child update entries that land there.
+    """
     nodes = F.nodes
+    if max(len(nd.own) for nd in nodes) > 2048:
+        raise ValueError("separator larger than the kernel's 2048-dof shared buffer")
     idx = {id(nd): i for i, nd in enumerate(nodes)}
-    parent = [-1] * len(nodes)
-    for i, nd in enumerate(nodes):
-        for c in nd.children:
-            parent[idx[id(c)]] = i
     mats, off = [], 0
     out_off, oo = [], 0
-    b_off, bo = [], 0
+    bo = 0
     node_tab = np.zeros((len(nodes), 10), dtype=np.int64)
     Bcat = []
     for i, nd in enumerate(nodes):
         ns, nb = len(nd.own), len(nd.B)
-        o_L = off; mats.append(nd.Linv.ravel()); off += ns * ns
-        o_LT = off; mats.append(nd.Linv.T.ravel()); off += ns * ns
+        r, c = np.tril_indices(ns)
+        lo = nd.Linv[r, c]                                  # packed lower, row-major
+        ru, cu = np.triu_indices(ns)
+        up = nd.Linv.T[ru, cu]                              # packed upper, row-major
+        o_L = off; mats.append(lo); off += len(lo)
+        o_LT = off; mats.append(up); off += len(up)
         o_W = off; mats.append(nd.W.ravel()); off += nb * ns
-        o_WT = off; mats.append(nd.W.T.ravel()); off += nb * ns
+        o_WT = off; mats.append(np.ascontiguousarray(nd.W.T).ravel()); off += nb * ns
         node_tab[i] = [nd.s0, ns, nb, o_L, o_LT, o_W, o_WT, oo, bo, 0]
-        out_off.append(oo); oo += nb
-        b_off.append(bo); bo += nb
+        out_off.append(oo)
+        oo += nb
+        bo += nb
         Bcat.append(nd.B)
-    # child -> parent gather sources, per parent own row / boundary row
-    src_t = -np.ones((F.n, 2), dtype=np.int64)           # per elimination position in S
-    src_o = -np.ones((max(oo, 1), 2), dtype=np.int64)    # per boundary row of each node
+    src_t = -np.ones((F.n, 2), dtype=np.int64)
+    src_o = -np.ones((max(oo, 1), 2), dtype=np.int64)
     for i, nd in enumerate(nodes):
         ns = len(nd.own)
-        loc = {}
-        for r, p in enumerate(nd.B):
-            loc[int(p)] = r
+        loc = {int(p): r for r, p in enumerate(nd.B)}
         for slot, c in enumerate(nd.children):
             ci = idx[id(c)]
             for e, p in enumerate(c.B):
@@ -192,35 +199,83 @@ def _upload_multifrontal(F: MultifrontalFactor):
                     src_t[p, slot] = src
                 else:
                     src_o[out_off[i] + loc[p], slot] = src
-    tasks = []
-    for lv in F.levels:
-        ft, fo = [], []
-        for i in lv:
-            ns, nb = node_tab[i, 1], node_tab[i, 2]
-            for r0 in range(0, ns, ROWS_PER_TASK):
-                ft.append((i, r0, min(ns, r0 + ROWS_PER_TASK)))
-            for r0 in range(0, nb, ROWS_PER_TASK):
-                fo.append((i, r0, min(nb, r0 + ROWS_PER_TASK)))
-        tasks.append((np.array(ft, dtype=np.int32).reshape(-1, 3),
-                      np.array(fo, dtype=np.int32).reshape(-1, 3)))
     torch = __import__("torch")
-    dev = dict(
+    H, top = _top_split(F)
+    top_dev = None
+    if top is not None:
+        T, ptr, src, Sinv = top
+        top_dev = dict(t=len(T), T=engine.to_dev(T.astype(np.int32)),
+                       ptr=engine.to_dev(ptr.astype(np.int32)),
+                       src=engine.to_dev(src.astype(np.int32) if len(src) else np.zeros(1, np.int32)),
+                       Sinv=engine.to_dev(Sinv),
+                       g=torch.empty(len(T), dtype=torch.float64, device="cuda"))
+    F.dev = dict(
+        top=top_dev, H=H,
         mats=engine.to_dev(np.concatenate(mats) if mats else np.zeros(1)),
         nodes=engine.to_dev(node_tab),
         B=engine.to_dev(np.concatenate(Bcat).astype(np.int32) if oo else np.zeros(1, np.int32)),
         src_t=engine.to_dev(src_t.astype(np.int32)),
         src_o=engine.to_dev(src_o.astype(np.int32)),
         perm=engine.to_dev(F.perm.astype(np.int32)),
-        tasks=[(engine.to_dev(a) if len(a) else None, engine.to_dev(b) if len(b) else None,
-                len(a), len(b)) for a, b in tasks],
+        levels=[(engine.to_dev(np.array(lv, dtype=np.int32)), len(lv)) for lv in F.levels[:H]],
         y=torch.empty(F.n, dtype=torch.float64, device="cuda"),
-        s=torch.empty(F.n, dtype=torch.float64, device="cuda"),
         xp=torch.empty(F.n, dtype=torch.float64, device="cuda"),
         out=torch.empty(max(oo, 1), dtype=torch.float64, device="cuda"),
+        bytes=8 * off,
     )
-    F.dev = dev
-    _abi.call("mcs_mf_set_max_own", int(max([len(nd.own) for nd in nodes] + [1])))
     return F
+
+
+def _top_split(F: MultifrontalFactor, top_max: int = None):
+    """Cut the separator tree at height H: nodes at height >= H (their own
+    dofs T, at most top_max) are solved with the dense inverse of their
+    Schur complement, which equals the T x T block of A^-1.  Returns H and
+    (T positions, CSR gather sources of the frontier updates, Sinv)."""
+    top_max = TOP_MAX if top_max is None else top_max
+    nodes, levels = F.nodes, F.levels
+    H = len(levels)
+    size = 0
+    while H > 0 and size + sum(len(nodes[i].own) for i in levels[H - 1]) <= top_max:
+        H -= 1
+        size += sum(len(nodes[i].own) for i in levels[H])
+    if H == len(levels):
+        raise ValueError("top separator larger than TOP_MAX")
+    top_ids = [i for lv in levels[H:] for i in lv]
+    T = np.sort(np.concatenate([np.arange(nodes[i].s0, nodes[i].s0 + len(nodes[i].own))
+                                for i in top_ids]))
+    tpos = -np.ones(F.n, dtype=np.int64)
+    tpos[T] = np.arange(len(T))
+    idx = {id(nd): i for i, nd in enumerate(nodes)}
+    out_off, oo = [], 0
+    for nd in nodes:
+        out_off.append(oo)
+        oo += len(nd.B)
+    top_set = set(top_ids)
+    lists = [[] for _ in range(len(T))]
+    for i in top_ids:
+        for c in nodes[i].children:
+            ci = idx[id(c)]
+            if ci in top_set:
+                continue
+            for e, p in enumerate(c.B):          # frontier node: B_c is inside T
+                lists[tpos[int(p)]].append(out_off[ci] + e)
+    ptr = np.zeros(len(T) + 1, dtype=np.int64)
+    ptr[1:] = np.cumsum([len(l) for l in lists])
+    src = np.array([s_ for l in lists for s_ in l], dtype=np.int64)
+    # The top nodes' blocks form the Cholesky factor of the top Schur
+    # complement S_T in the elimination order of T: L_T[S, S] = L_SS and
+    # L_T[B, S] = W.  Then (A^-1)_TT = S_T^-1 = L_T^-T L_T^-1 (dense, t^3/3).
+    Lt = np.zeros((len(T), len(T)))
+    for i in top_ids:
+        nd = nodes[i]
+        S = tpos[np.arange(nd.s0, nd.s0 + len(nd.own))]
+        Lt[np.ix_(S, S)] = nd.L
+        if len(nd.B):
+            Lt[np.ix_(tpos[nd.B], S)] = nd.W
+    Li = sla.solve_triangular(Lt, np.eye(len(T)), lower=True, check_finite=False)
+    Sinv = Li.T @ Li
+    Sinv = 0.5 * (Sinv + Sinv.T)
+    return H, (T, ptr, src, np.ascontiguousarray(Sinv))
 
 
 class CoarseSolver:
@@ -238,23 +293,19 @@ class CoarseSolver:
             _abi.call("mcs_dense_gemv", self.n, _abi.ptr(self.data), _abi.ptr(b), _abi.ptr(x), st)
         else:
             d = self.data.dev
-            for ft, fo, nft, nfo in d["tasks"]:
-                if nft:
-                    _abi.call("mcs_mf_forward_own", nft, _abi.ptr(ft), _abi.ptr(d["nodes"]),
-                              _abi.ptr(d["mats"]), _abi.ptr(d["src_t"]), _abi.ptr(d["out"]),
-                              _abi.ptr(d["perm"]), _abi.ptr(b), _abi.ptr(d["y"]), st)
-                if nfo:
-                    _abi.call("mcs_mf_forward_out", nfo, _abi.ptr(fo), _abi.ptr(d["nodes"]),
-                              _abi.ptr(d["mats"]), _abi.ptr(d["src_o"]), _abi.ptr(d["y"]),
-                              _abi.ptr(d["out"]), st)
-            for ft, fo, nft, nfo in reversed(d["tasks"]):
-                if nft:
-                    _abi.call("mcs_mf_backward", nft, _abi.ptr(ft), _abi.ptr(d["nodes"]),
-                              _abi.ptr(d["mats"]), _abi.ptr(d["B"]), _abi.ptr(d["y"]),
-                              _abi.ptr(d["xp"]), _abi.ptr(d["s"]), st)
-                    _abi.call("mcs_mf_backward2", nft, _abi.ptr(ft), _abi.ptr(d["nodes"]),
-                              _abi.ptr(d["mats"]), _abi.ptr(d["s"]), _abi.ptr(d["perm"]),
-                              _abi.ptr(d["xp"]), _abi.ptr(x), st)
+            for ln, cnt in d["levels"]:                    # bottom levels, forward
+                _abi.call("mcs_mf_forward", cnt, _abi.ptr(ln), _abi.ptr(d["nodes"]),
+                          _abi.ptr(d["mats"]), _abi.ptr(d["src_t"]), _abi.ptr(d["src_o"]),
+                          _abi.ptr(d["perm"]), _abi.ptr(b), _abi.ptr(d["y"]), _abi.ptr(d["out"]),
+                          st)
+            tp = d["top"]                                  # dense top Schur complement
+            _abi.call("mcs_mf_top", tp["t"], _abi.ptr(tp["T"]), _abi.ptr(d["perm"]), _abi.ptr(b),
+                      _abi.ptr(tp["ptr"]), _abi.ptr(tp["src"]), _abi.ptr(d["out"]),
+                      _abi.ptr(tp["g"]), _abi.ptr(tp["Sinv"]), _abi.ptr(d["xp"]), _abi.ptr(x), st)
+            for ln, cnt in reversed(d["levels"]):          # bottom levels, backward
+                _abi.call("mcs_mf_backward", cnt, _abi.ptr(ln), _abi.ptr(d["nodes"]),
+                          _abi.ptr(d["mats"]), _abi.ptr(d["B"]), _abi.ptr(d["perm"]),
+                          _abi.ptr(d["y"]), _abi.ptr(d["xp"]), _abi.ptr(x), st)
         if self.scale != 1.0:
             from .operators import axpby
             axpby(1.0 / self.scale, x, 0.0, x, stream)

@@ -26,50 +26,78 @@ struct WarpRing {
   uint64_t bar[2];
 };
 
-template <int N, int STRIDE>
-__global__ void __launch_bounds__(WARPS * 32)
+// Signed gather x_loc[j] = sign * x[idx] (0 for constrained dofs).
+__device__ __forceinline__ double gather_signed(const double* x, int c) {
+  return c >= 0 ? code_sign(c) * __ldg(x + code_index(c)) : 0.0;
+}
+
+// y = sum_T P^T D M_T D P x, warp per element, W warps per CTA, NST bulk-copy
+// stages per warp.  The dof codes and x values of the next elements are
+// prefetched into registers two / one element ahead, so neither the
+// 1-D bulk copy of the packed matrix nor the dependent index -> x gather is
+// on the per-element critical path.
+template <int N, int STRIDE, int W, int NST>
+__global__ void __launch_bounds__(W * 32)
     elem_apply_kernel(const double* __restrict__ M, const int* __restrict__ codes,
                       const double* __restrict__ x, double* __restrict__ y, int64_t nt) {
+  constexpr int R = (N + 31) / 32;
   extern __shared__ __align__(128) double sm[];
-  __shared__ __align__(8) WarpRing ring[WARPS];
-  __shared__ double xs[WARPS][N];
+  __shared__ __align__(8) uint64_t bars[W][NST];
+  __shared__ double xs[W][N];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  double* stage = sm + (size_t)warp * 2 * STRIDE;
-  uint64_t* bar = ring[warp].bar;
-  const int64_t gw = (int64_t)blockIdx.x * WARPS + warp;
-  const int64_t nw = (int64_t)gridDim.x * WARPS;
+  double* stage = sm + (size_t)warp * NST * STRIDE;
+  uint64_t* bar = bars[warp];
+  const int64_t gw = (int64_t)blockIdx.x * W + warp;
+  const int64_t nw = (int64_t)gridDim.x * W;
   if (lane == 0) {
-    mbar_init(&bar[0], 1);
-    mbar_init(&bar[1], 1);
+    for (int q = 0; q < NST; ++q) mbar_init(&bar[q], 1);
     fence_barrier_init();
   }
   __syncwarp();
   if (lane == 0) {
-    for (int s = 0; s < 2; ++s) {
-      const int64_t e = gw + s * nw;
+    for (int q = 0; q < NST; ++q) {
+      const int64_t e = gw + q * nw;
       if (e < nt) {
-        mbar_expect_tx(&bar[s], STRIDE * 8);
-        bulk_g2s(stage + s * STRIDE, M + e * STRIDE, STRIDE * 8, &bar[s]);
+        mbar_expect_tx(&bar[q], STRIDE * 8);
+        bulk_g2s(stage + q * STRIDE, M + e * STRIDE, STRIDE * 8, &bar[q]);
       }
     }
   }
+  // prefetch pipeline: codes of e and e+nw, x values of e
+  int cd0[R], cd1[R];
+  double xv[R];
+#pragma unroll
+  for (int r = 0; r < R; ++r) {
+    const int j = lane + 32 * r;
+    const int64_t e0 = gw, e1 = gw + nw;
+    cd0[r] = (j < N && e0 < nt) ? __ldg(codes + e0 * N + j) : -1;
+    cd1[r] = (j < N && e1 < nt) ? __ldg(codes + e1 * N + j) : -1;
+  }
+#pragma unroll
+  for (int r = 0; r < R; ++r) xv[r] = gather_signed(x, cd0[r]);
   int it = 0;
   for (int64_t e = gw; e < nt; e += nw, ++it) {
-    const int s = it & 1;
-    int cd[(N + 31) / 32];
+    const int s = it % NST;
 #pragma unroll
-    for (int r = 0; r < (N + 31) / 32; ++r) {
+    for (int r = 0; r < R; ++r) {
       const int j = lane + 32 * r;
-      if (j < N) {
-        const int c = codes[e * N + j];
-        cd[r] = c;
-        xs[warp][j] = c >= 0 ? code_sign(c) * x[code_index(c)] : 0.0;
-      }
+      if (j < N) xs[warp][j] = xv[r];
+    }
+    int cd[R];
+#pragma unroll
+    for (int r = 0; r < R; ++r) cd[r] = cd0[r];
+    // next element's x gather and the codes two ahead
+    const int64_t e2 = e + 2 * nw;
+#pragma unroll
+    for (int r = 0; r < R; ++r) {
+      const int j = lane + 32 * r;
+      xv[r] = gather_signed(x, cd1[r]);
+      cd0[r] = cd1[r];
+      cd1[r] = (j < N && e2 < nt) ? __ldg(codes + e2 * N + j) : -1;
     }
     __syncwarp();
-    mbar_wait(&bar[s], (it >> 1) & 1);
+    mbar_wait(&bar[s], (it / NST) & 1);
     const double* P = stage + s * STRIDE;
-    constexpr int R = (N + 31) / 32;
     double acc[R];
     int rowb[R];
 #pragma unroll
@@ -88,135 +116,220 @@ __global__ void __launch_bounds__(WARPS * 32)
         acc[r] = fma(P[j <= i ? rowb[r] + j : cb + i], xj, acc[r]);
       }
     }
-#pragma unroll
-    for (int r = 0; r < R; ++r) {
-      const int i = lane + 32 * r;
-      if (i < N) {
-        const int c = cd[r];
-        if (c >= 0) atomicAdd(&y[code_index(c)], code_sign(c) * acc[r]);
-      }
-    }
     __syncwarp();
-    const int64_t nxt = e + 2 * nw;
+    const int64_t nxt = e + NST * nw;
     if (lane == 0 && nxt < nt) {
       mbar_expect_tx(&bar[s], STRIDE * 8);
       bulk_g2s(stage + s * STRIDE, M + nxt * STRIDE, STRIDE * 8, &bar[s]);
     }
+#pragma unroll
+    for (int r = 0; r < R; ++r) {
+      const int i = lane + 32 * r;
+      if (i < N && cd[r] >= 0) atomicAdd(&y[code_index(cd[r])], code_sign(cd[r]) * acc[r]);
+    }
   }
 }
 
-// ExtendedAsp F1^-1 (restrict) and F2^-1 (prolong); ext record = [X | Soo^-1 packed]
-template <int K, int LEN>
-__global__ void __launch_bounds__(WARPS * 32)
+// ExtendedAsp F1^-1 (restrict) and F2^-1 (prolong); ext record = [X | Soo^-1 packed].
+// Same pipeline as the apply: bulk-copied records, register prefetch of the
+// next element's indices and gathered vector entries.
+template <int K, int LEN, int W, int NST>
+__global__ void __launch_bounds__(W * 32)
     ext_restrict_kernel(const double* __restrict__ ext, const int* __restrict__ bidx,
                         const int* __restrict__ ccodes, const double* __restrict__ r,
                         double* __restrict__ bubble, double* __restrict__ acc, int64_t nt) {
   using Z = Sizes<K>;
   constexpr int NI = Z::n_int, NC = Z::ncpl, XL = NI * NC;
+  constexpr int RI = (NI + 31) / 32, RC = (NC + 31) / 32;
   extern __shared__ __align__(128) double sm[];
-  __shared__ __align__(8) WarpRing ring[WARPS];
-  __shared__ double ro[WARPS][NI];
+  __shared__ __align__(8) uint64_t bars[W][NST];
+  __shared__ double ro[W][NI];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  double* stage = sm + (size_t)warp * 2 * LEN;
-  uint64_t* bar = ring[warp].bar;
-  const int64_t gw = (int64_t)blockIdx.x * WARPS + warp;
-  const int64_t nw = (int64_t)gridDim.x * WARPS;
+  double* stage = sm + (size_t)warp * NST * LEN;
+  uint64_t* bar = bars[warp];
+  const int64_t gw = (int64_t)blockIdx.x * W + warp;
+  const int64_t nw = (int64_t)gridDim.x * W;
   if (lane == 0) {
-    mbar_init(&bar[0], 1);
-    mbar_init(&bar[1], 1);
+    for (int q = 0; q < NST; ++q) mbar_init(&bar[q], 1);
     fence_barrier_init();
   }
   __syncwarp();
   if (lane == 0) {
-    for (int s = 0; s < 2; ++s) {
-      const int64_t e = gw + s * nw;
+    for (int q = 0; q < NST; ++q) {
+      const int64_t e = gw + q * nw;
       if (e < nt) {
-        mbar_expect_tx(&bar[s], LEN * 8);
-        bulk_g2s(stage + s * LEN, ext + e * LEN, LEN * 8, &bar[s]);
+        mbar_expect_tx(&bar[q], LEN * 8);
+        bulk_g2s(stage + q * LEN, ext + e * LEN, LEN * 8, &bar[q]);
       }
     }
   }
+  int b1[RI], cc0[RC];
+  double rv[RI];
+#pragma unroll
+  for (int q = 0; q < RI; ++q) {
+    const int j = lane + 32 * q;
+    const int b0 = (j < NI && gw < nt) ? __ldg(bidx + gw * NI + j) : -1;
+    rv[q] = b0 >= 0 ? __ldg(r + b0) : 0.0;
+    b1[q] = (j < NI && gw + nw < nt) ? __ldg(bidx + (gw + nw) * NI + j) : -1;
+  }
+#pragma unroll
+  for (int q = 0; q < RC; ++q) {
+    const int c = lane + 32 * q;
+    cc0[q] = (c < NC && gw < nt) ? __ldg(ccodes + gw * NC + c) : -1;
+  }
   int it = 0;
   for (int64_t e = gw; e < nt; e += nw, ++it) {
-    const int s = it & 1;
-    for (int j = lane; j < NI; j += 32) ro[warp][j] = r[bidx[e * NI + j]];
+    const int s = it % NST;
+#pragma unroll
+    for (int q = 0; q < RI; ++q) {
+      const int j = lane + 32 * q;
+      if (j < NI) ro[warp][j] = rv[q];
+    }
+    int cd[RC];
+#pragma unroll
+    for (int q = 0; q < RC; ++q) cd[q] = cc0[q];
+    const int64_t e1 = e + nw, e2 = e + 2 * nw;
+#pragma unroll
+    for (int q = 0; q < RI; ++q) {
+      const int j = lane + 32 * q;
+      rv[q] = b1[q] >= 0 ? __ldg(r + b1[q]) : 0.0;
+      b1[q] = (j < NI && e2 < nt) ? __ldg(bidx + e2 * NI + j) : -1;
+    }
+#pragma unroll
+    for (int q = 0; q < RC; ++q) {
+      const int c = lane + 32 * q;
+      cc0[q] = (c < NC && e1 < nt) ? __ldg(ccodes + e1 * NC + c) : -1;
+    }
     __syncwarp();
-    mbar_wait(&bar[s], (it >> 1) & 1);
+    mbar_wait(&bar[s], (it / NST) & 1);
     const double* X = stage + s * LEN;
     const double* Sinv = X + XL;
-    for (int i = lane; i < NI; i += 32) {
-      double a = 0.0;
-      const int rowb = pk(i, 0);
-      for (int j = 0; j < NI; ++j) a = fma(Sinv[j <= i ? rowb + j : pk(j, i)], ro[warp][j], a);
-      bubble[e * NI + i] = a;
+    double a[RI];
+#pragma unroll
+    for (int q = 0; q < RI; ++q) a[q] = 0.0;
+#pragma unroll 2
+    for (int j = 0; j < NI; ++j) {
+      const double xj = ro[warp][j];
+      const int cb = pk(j, 0);
+#pragma unroll
+      for (int q = 0; q < RI; ++q) {
+        const int i = min(lane + 32 * q, NI - 1);
+        a[q] = fma(Sinv[j <= i ? pk(i, 0) + j : cb + i], xj, a[q]);
+      }
     }
-    for (int c = lane; c < NC; c += 32) {
-      double a = 0.0;
+    double c[RC];
+#pragma unroll
+    for (int q = 0; q < RC; ++q) c[q] = 0.0;
 #pragma unroll 5
-      for (int i = 0; i < NI; ++i) a = fma(X[i * NC + c], ro[warp][i], a);
-      const int cd = ccodes[e * NC + c];
-      if (cd >= 0) atomicAdd(&acc[code_index(cd)], code_sign(cd) * a);
+    for (int i = 0; i < NI; ++i) {
+      const double xi = ro[warp][i];
+#pragma unroll
+      for (int q = 0; q < RC; ++q) c[q] = fma(X[i * NC + min(lane + 32 * q, NC - 1)], xi, c[q]);
     }
     __syncwarp();
-    const int64_t nxt = e + 2 * nw;
+    const int64_t nxt = e + NST * nw;
     if (lane == 0 && nxt < nt) {
       mbar_expect_tx(&bar[s], LEN * 8);
       bulk_g2s(stage + s * LEN, ext + nxt * LEN, LEN * 8, &bar[s]);
     }
+#pragma unroll
+    for (int q = 0; q < RI; ++q) {
+      const int i = lane + 32 * q;
+      if (i < NI) bubble[e * NI + i] = a[q];
+    }
+#pragma unroll
+    for (int q = 0; q < RC; ++q) {
+      const int cc = lane + 32 * q;
+      if (cc < NC && cd[q] >= 0) atomicAdd(&acc[code_index(cd[q])], code_sign(cd[q]) * c[q]);
+    }
   }
 }
 
-template <int K, int LEN>
-__global__ void __launch_bounds__(WARPS * 32)
+template <int K, int LEN, int W, int NST>
+__global__ void __launch_bounds__(W * 32)
     ext_prolong_kernel(const double* __restrict__ ext, const int* __restrict__ bidx,
                        const int* __restrict__ ccodes, const double* __restrict__ zc,
                        const double* __restrict__ bubble, double* __restrict__ out, int64_t nt) {
   using Z = Sizes<K>;
   constexpr int NI = Z::n_int, NC = Z::ncpl, XL = NI * NC;
   constexpr int XLE = even(XL);
+  constexpr int RI = (NI + 31) / 32, RC = (NC + 31) / 32;
   extern __shared__ __align__(128) double sm[];
-  __shared__ __align__(8) WarpRing ring[WARPS];
-  __shared__ double zl[WARPS][NC];
+  __shared__ __align__(8) uint64_t bars[W][NST];
+  __shared__ double zl[W][NC];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  double* stage = sm + (size_t)warp * 2 * XLE;
-  uint64_t* bar = ring[warp].bar;
-  const int64_t gw = (int64_t)blockIdx.x * WARPS + warp;
-  const int64_t nw = (int64_t)gridDim.x * WARPS;
+  double* stage = sm + (size_t)warp * NST * XLE;
+  uint64_t* bar = bars[warp];
+  const int64_t gw = (int64_t)blockIdx.x * W + warp;
+  const int64_t nw = (int64_t)gridDim.x * W;
   if (lane == 0) {
-    mbar_init(&bar[0], 1);
-    mbar_init(&bar[1], 1);
+    for (int q = 0; q < NST; ++q) mbar_init(&bar[q], 1);
     fence_barrier_init();
   }
   __syncwarp();
   if (lane == 0) {
-    for (int s = 0; s < 2; ++s) {
-      const int64_t e = gw + s * nw;
+    for (int q = 0; q < NST; ++q) {
+      const int64_t e = gw + q * nw;
       if (e < nt) {
-        mbar_expect_tx(&bar[s], XLE * 8);
-        bulk_g2s(stage + s * XLE, ext + e * LEN, XLE * 8, &bar[s]);
+        mbar_expect_tx(&bar[q], XLE * 8);
+        bulk_g2s(stage + q * XLE, ext + e * LEN, XLE * 8, &bar[q]);
       }
     }
   }
+  int c1[RC];
+  double zv[RC];
+#pragma unroll
+  for (int q = 0; q < RC; ++q) {
+    const int c = lane + 32 * q;
+    const int c0 = (c < NC && gw < nt) ? __ldg(ccodes + gw * NC + c) : -1;
+    zv[q] = gather_signed(zc, c0);
+    c1[q] = (c < NC && gw + nw < nt) ? __ldg(ccodes + (gw + nw) * NC + c) : -1;
+  }
   int it = 0;
   for (int64_t e = gw; e < nt; e += nw, ++it) {
-    const int s = it & 1;
-    for (int c = lane; c < NC; c += 32) {
-      const int cd = ccodes[e * NC + c];
-      zl[warp][c] = cd >= 0 ? code_sign(cd) * zc[code_index(cd)] : 0.0;
+    const int s = it % NST;
+#pragma unroll
+    for (int q = 0; q < RC; ++q) {
+      const int c = lane + 32 * q;
+      if (c < NC) zl[warp][c] = zv[q];
+    }
+    const int64_t e2 = e + 2 * nw;
+#pragma unroll
+    for (int q = 0; q < RC; ++q) {
+      const int c = lane + 32 * q;
+      zv[q] = gather_signed(zc, c1[q]);
+      c1[q] = (c < NC && e2 < nt) ? __ldg(ccodes + e2 * NC + c) : -1;
+    }
+    double bub[RI];
+    int bi[RI];
+#pragma unroll
+    for (int q = 0; q < RI; ++q) {
+      const int i = lane + 32 * q;
+      bub[q] = i < NI ? __ldg(bubble + e * NI + i) : 0.0;
+      bi[q] = i < NI ? __ldg(bidx + e * NI + i) : 0;
     }
     __syncwarp();
-    mbar_wait(&bar[s], (it >> 1) & 1);
+    mbar_wait(&bar[s], (it / NST) & 1);
     const double* X = stage + s * XLE;
-    for (int i = lane; i < NI; i += 32) {
-      double a = 0.0;
-      for (int c = 0; c < NC; ++c) a = fma(X[i * NC + c], zl[warp][c], a);
-      out[bidx[e * NI + i]] = bubble[e * NI + i] - a;
+    double a[RI];
+#pragma unroll
+    for (int q = 0; q < RI; ++q) a[q] = 0.0;
+#pragma unroll 3
+    for (int c = 0; c < NC; ++c) {
+      const double zcv = zl[warp][c];
+#pragma unroll
+      for (int q = 0; q < RI; ++q) a[q] = fma(X[min(lane + 32 * q, NI - 1) * NC + c], zcv, a[q]);
     }
     __syncwarp();
-    const int64_t nxt = e + 2 * nw;
+    const int64_t nxt = e + NST * nw;
     if (lane == 0 && nxt < nt) {
       mbar_expect_tx(&bar[s], XLE * 8);
       bulk_g2s(stage + s * XLE, ext + nxt * LEN, XLE * 8, &bar[s]);
+    }
+#pragma unroll
+    for (int q = 0; q < RI; ++q) {
+      const int i = lane + 32 * q;
+      if (i < NI) out[bi[q]] = bub[q] - a[q];
     }
   }
 }
@@ -258,10 +371,19 @@ static int warp_grid(Kern k, size_t smem, int64_t nt) {
 template <int N, int STRIDE>
 static int launch_apply(const double* M, const int* codes, const double* x, double* y, int64_t nt,
                         cudaStream_t st) {
-  auto kern = elem_apply_kernel<N, STRIDE>;
-  const size_t smem = (size_t)WARPS * 2 * STRIDE * sizeof(double);
+  // one bulk stage per warp when a stage is large (k = 5, 6), two otherwise;
+  // aim for ~64-96 KB of bulk copies in flight per SM
+  constexpr int W = STRIDE * 8 > 12000 ? 8 : 8;
+  constexpr int NST = STRIDE * 8 > 12000 ? 1 : 2;
+  auto kern = elem_apply_kernel<N, STRIDE, W, NST>;
+  const size_t smem = (size_t)W * NST * STRIDE * sizeof(double);
   cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-  kern<<<warp_grid(kern, smem, nt), WARPS * 32, smem, st>>>(M, codes, x, y, nt);
+  int per_sm = 1;
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, W * 32, smem);
+  if (per_sm < 1) per_sm = 1;
+  const int64_t want = (nt + W - 1) / W;
+  const int64_t g = (int64_t)per_sm * sm_count();
+  kern<<<(int)(want < g ? want : g), W * 32, smem, st>>>(M, codes, x, y, nt);
   return launch_status();
 }
 
@@ -275,10 +397,15 @@ template <int K>
 static int launch_restrict(const double* ext, const int* bidx, const int* cc, const double* r,
                            double* bubble, double* acc, int64_t nt, cudaStream_t st) {
   constexpr int LEN = ExtLen<K>::len;
-  auto kern = ext_restrict_kernel<K, LEN>;
-  const size_t smem = (size_t)WARPS * 2 * LEN * sizeof(double);
+  constexpr int W = 8, NST = LEN * 8 > 12000 ? 1 : 2;
+  auto kern = ext_restrict_kernel<K, LEN, W, NST>;
+  const size_t smem = (size_t)W * NST * LEN * sizeof(double);
   cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-  kern<<<warp_grid(kern, smem, nt), WARPS * 32, smem, st>>>(ext, bidx, cc, r, bubble, acc, nt);
+  int per_sm = 1;
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, W * 32, smem);
+  if (per_sm < 1) per_sm = 1;
+  const int64_t want = (nt + W - 1) / W, g = (int64_t)per_sm * sm_count();
+  kern<<<(int)(want < g ? want : g), W * 32, smem, st>>>(ext, bidx, cc, r, bubble, acc, nt);
   return launch_status();
 }
 
@@ -287,10 +414,16 @@ static int launch_prolong(const double* ext, const int* bidx, const int* cc, con
                           const double* bubble, double* out, int64_t nt, cudaStream_t st) {
   constexpr int LEN = ExtLen<K>::len;
   using Z = Sizes<K>;
-  auto kern = ext_prolong_kernel<K, LEN>;
-  const size_t smem = (size_t)WARPS * 2 * even(Z::n_int * Z::ncpl) * sizeof(double);
+  constexpr int XLE = even(Z::n_int * Z::ncpl);
+  constexpr int W = 8, NST = XLE * 8 > 12000 ? 1 : 2;
+  auto kern = ext_prolong_kernel<K, LEN, W, NST>;
+  const size_t smem = (size_t)W * NST * XLE * sizeof(double);
   cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-  kern<<<warp_grid(kern, smem, nt), WARPS * 32, smem, st>>>(ext, bidx, cc, zc, bubble, out, nt);
+  int per_sm = 1;
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, W * 32, smem);
+  if (per_sm < 1) per_sm = 1;
+  const int64_t want = (nt + W - 1) / W, g = (int64_t)per_sm * sm_count();
+  kern<<<(int)(want < g ? want : g), W * 32, smem, st>>>(ext, bidx, cc, zc, bubble, out, nt);
   return launch_status();
 }
 

@@ -1,11 +1,17 @@
 // Exact coarse solve: GPU triangular solves of a host multifrontal Cholesky
 // factorisation (the reference uses SuperLU,
-// preconditioners.py:111-118,165-171).  Per separator-tree node the factor
-// is stored as dense explicit blocks (Linv = L_SS^-1, its transpose, W and
-// W^T), so each solve phase is a set of independent dense GEMVs, one warp
-// per row, over a task list (node, row range) per tree level.  Child
-// contributions are gathered through precomputed source indices in a fixed
-// order (deterministic, no atomics).
+// preconditioners.py:111-118,165-171).
+//
+// Per separator-tree node the factor is stored as dense explicit blocks:
+// Linv = L_SS^-1 (packed lower, row-major), Linv^T (packed upper,
+// row-major), W = F_BS L_SS^-T (nb x ns) and W^T.  One CTA per node and one
+// kernel per tree level and direction:
+//   forward   t = b_S - (child updates), y_S = Linv t,
+//             out_B = W y_S + (child updates passing through)
+//   backward  s = y_S - W^T x_B,  x_S = Linv^T s
+// Child contributions are gathered through precomputed source indices in a
+// fixed order (deterministic, no atomics); every GEMV is warp-per-row over
+// contiguous rows (coalesced).
 //
 // node table (int64 x 10): s0, ns, nb, off_Linv, off_LinvT, off_W, off_WT, off_out, off_B, 0
 #include "common.cuh"
@@ -24,17 +30,17 @@ __device__ __forceinline__ double warp_sum(double v) {
   return v;
 }
 
-// y_S = Linv (b_S - sum_children out)
 __global__ void __launch_bounds__(MF_THREADS)
-    mf_forward_own(const int* __restrict__ tasks, const NodeRec* __restrict__ nodes,
-                   const double* __restrict__ mats, const int* __restrict__ src_t,
-                   const double* __restrict__ out, const int* __restrict__ perm,
-                   const double* __restrict__ b, double* __restrict__ y) {
-  extern __shared__ double t[];
-  const int* tk = tasks + 3 * blockIdx.x;
-  const NodeRec nd = nodes[tk[0]];
-  const int r0 = tk[1], r1 = tk[2];
-  const int ns = (int)nd.ns;
+    mf_forward(const int* __restrict__ level_nodes, const NodeRec* __restrict__ nodes,
+               const double* __restrict__ mats, const int* __restrict__ src_t,
+               const int* __restrict__ src_o, const int* __restrict__ perm,
+               const double* __restrict__ b, double* __restrict__ y, double* __restrict__ out) {
+  extern __shared__ double sm[];
+  double* t = sm;              // ns
+  double* ys = sm + 2048;      // ns (max 2048)
+  const NodeRec nd = nodes[level_nodes[blockIdx.x]];
+  const int ns = (int)nd.ns, nb = (int)nd.nb;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   for (int j = threadIdx.x; j < ns; j += MF_THREADS) {
     const int64_t p = nd.s0 + j;
     double v = b[perm[p]];
@@ -44,31 +50,23 @@ __global__ void __launch_bounds__(MF_THREADS)
     t[j] = v;
   }
   __syncthreads();
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const double* L = mats + nd.oL;
-  for (int r = r0 + warp; r < r1; r += MF_THREADS / 32) {
+  for (int r = warp; r < ns; r += MF_THREADS / 32) {
+    const double* row = L + (int64_t)r * (r + 1) / 2;
     double s = 0.0;
-    for (int j = lane; j <= r; j += 32) s = fma(L[(int64_t)r * ns + j], t[j], s);
+    for (int j = lane; j <= r; j += 32) s = fma(row[j], t[j], s);
     s = warp_sum(s);
-    if (lane == 0) y[nd.s0 + r] = s;
+    if (lane == 0) {
+      y[nd.s0 + r] = s;
+      ys[r] = s;
+    }
   }
-}
-
-// out_B = W y_S + pass-through of children's updates
-__global__ void __launch_bounds__(MF_THREADS)
-    mf_forward_out(const int* __restrict__ tasks, const NodeRec* __restrict__ nodes,
-                   const double* __restrict__ mats, const int* __restrict__ src_o,
-                   const double* __restrict__ y, double* __restrict__ out) {
-  const int* tk = tasks + 3 * blockIdx.x;
-  const NodeRec nd = nodes[tk[0]];
-  const int r0 = tk[1], r1 = tk[2];
-  const int ns = (int)nd.ns;
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  __syncthreads();
   const double* W = mats + nd.oW;
-  const double* ys = y + nd.s0;
-  for (int r = r0 + warp; r < r1; r += MF_THREADS / 32) {
+  for (int r = warp; r < nb; r += MF_THREADS / 32) {
+    const double* row = W + (int64_t)r * ns;
     double s = 0.0;
-    for (int j = lane; j < ns; j += 32) s = fma(W[(int64_t)r * ns + j], ys[j], s);
+    for (int j = lane; j < ns; j += 32) s = fma(row[j], ys[j], s);
     s = warp_sum(s);
     if (lane == 0) {
       const int64_t q = nd.oo + r;
@@ -80,44 +78,31 @@ __global__ void __launch_bounds__(MF_THREADS)
   }
 }
 
-// s_S = y_S - W^T x_B
 __global__ void __launch_bounds__(MF_THREADS)
-    mf_backward(const int* __restrict__ tasks, const NodeRec* __restrict__ nodes,
+    mf_backward(const int* __restrict__ level_nodes, const NodeRec* __restrict__ nodes,
                 const double* __restrict__ mats, const int* __restrict__ B,
-                const double* __restrict__ y, const double* __restrict__ xp,
-                double* __restrict__ s) {
-  const int* tk = tasks + 3 * blockIdx.x;
-  const NodeRec nd = nodes[tk[0]];
-  const int r0 = tk[1], r1 = tk[2];
-  const int nb = (int)nd.nb;
+                const int* __restrict__ perm, const double* __restrict__ y,
+                double* __restrict__ xp, double* __restrict__ x) {
+  extern __shared__ double sm[];
+  double* s = sm;
+  const NodeRec nd = nodes[level_nodes[blockIdx.x]];
+  const int ns = (int)nd.ns, nb = (int)nd.nb;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const double* WT = mats + nd.oWT;
   const int* Bp = B + nd.ob;
-  for (int r = r0 + warp; r < r1; r += MF_THREADS / 32) {
+  for (int r = warp; r < ns; r += MF_THREADS / 32) {
+    const double* row = WT + (int64_t)r * nb;
     double a = 0.0;
-    for (int j = lane; j < nb; j += 32) a = fma(WT[(int64_t)r * nb + j], xp[Bp[j]], a);
+    for (int j = lane; j < nb; j += 32) a = fma(row[j], xp[Bp[j]], a);
     a = warp_sum(a);
-    if (lane == 0) s[nd.s0 + r] = y[nd.s0 + r] - a;
+    if (lane == 0) s[r] = y[nd.s0 + r] - a;
   }
-}
-
-// x_S = Linv^T s_S ; scatter to the caller's ordering
-__global__ void __launch_bounds__(MF_THREADS)
-    mf_backward2(const int* __restrict__ tasks, const NodeRec* __restrict__ nodes,
-                 const double* __restrict__ mats, const double* __restrict__ s,
-                 const int* __restrict__ perm, double* __restrict__ xp, double* __restrict__ x) {
-  extern __shared__ double ss[];
-  const int* tk = tasks + 3 * blockIdx.x;
-  const NodeRec nd = nodes[tk[0]];
-  const int r0 = tk[1], r1 = tk[2];
-  const int ns = (int)nd.ns;
-  for (int j = threadIdx.x; j < ns; j += MF_THREADS) ss[j] = s[nd.s0 + j];
   __syncthreads();
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const double* LT = mats + nd.oLT;
-  for (int r = r0 + warp; r < r1; r += MF_THREADS / 32) {
+  const double* LT = mats + nd.oLT;     // packed upper, row r holds columns r..ns-1
+  for (int r = warp; r < ns; r += MF_THREADS / 32) {
+    const double* row = LT + (int64_t)r * ns - (int64_t)r * (r - 1) / 2 - r;
     double a = 0.0;
-    for (int j = r + lane; j < ns; j += 32) a = fma(LT[(int64_t)r * ns + j], ss[j], a);
+    for (int j = r + lane; j < ns; j += 32) a = fma(row[j], s[j], a);
     a = warp_sum(a);
     if (lane == 0) {
       xp[nd.s0 + r] = a;
@@ -126,52 +111,76 @@ __global__ void __launch_bounds__(MF_THREADS)
   }
 }
 
-static int g_max_ns = 0;
-
 }  // namespace mcs
 
 using namespace mcs;
 
-// shared memory is sized from the largest node (set once per factor)
-MCS_API int mcs_mf_set_max_own(int max_ns) {
-  if (max_ns > g_max_ns) g_max_ns = max_ns;
-  const int bytes = g_max_ns * (int)sizeof(double);
-  cudaFuncSetAttribute(mf_forward_own, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
-  cudaFuncSetAttribute(mf_backward2, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
+MCS_API int mcs_mf_forward(int nnodes, const int* level_nodes, const void* nodes,
+                           const double* mats, const int* src_t, const int* src_o,
+                           const int* perm, const double* b, double* y, double* out,
+                           void* stream) {
+  if (nnodes <= 0) return 0;
+  auto st = static_cast<cudaStream_t>(stream);
+  const size_t smem = 2 * 2048 * sizeof(double);
+  cudaFuncSetAttribute(mf_forward, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  mf_forward<<<nnodes, MF_THREADS, smem, st>>>(level_nodes, static_cast<const NodeRec*>(nodes),
+                                               mats, src_t, src_o, perm, b, y, out);
   return launch_status();
 }
 
-MCS_API int mcs_mf_forward_own(int ntasks, const int* tasks, const void* nodes, const double* mats,
-                               const int* src_t, const double* out, const int* perm, const double* b,
-                               double* y, void* stream) {
+MCS_API int mcs_mf_backward(int nnodes, const int* level_nodes, const void* nodes,
+                            const double* mats, const int* B, const int* perm, const double* y,
+                            double* xp, double* x, void* stream) {
+  if (nnodes <= 0) return 0;
   auto st = static_cast<cudaStream_t>(stream);
-  mf_forward_own<<<ntasks, MF_THREADS, g_max_ns * sizeof(double), st>>>(
-      tasks, static_cast<const NodeRec*>(nodes), mats, src_t, out, perm, b, y);
+  const size_t smem = 2048 * sizeof(double);
+  mf_backward<<<nnodes, MF_THREADS, smem, st>>>(level_nodes, static_cast<const NodeRec*>(nodes),
+                                                mats, B, perm, y, xp, x);
   return launch_status();
 }
 
-MCS_API int mcs_mf_forward_out(int ntasks, const int* tasks, const void* nodes, const double* mats,
-                               const int* src_o, const double* y, double* out, void* stream) {
-  auto st = static_cast<cudaStream_t>(stream);
-  mf_forward_out<<<ntasks, MF_THREADS, 0, st>>>(tasks, static_cast<const NodeRec*>(nodes), mats,
-                                                src_o, y, out);
-  return launch_status();
+// ---- top of the separator tree: dense explicit inverse of its Schur complement
+namespace mcs {
+
+// g[q] = b[perm[T[q]]] - sum_{p in src[ptr[q]..ptr[q+1])} out[p]   (fixed order)
+__global__ void mf_top_gather(int t, const int* __restrict__ T, const int* __restrict__ perm,
+                              const double* __restrict__ b, const int* __restrict__ ptr,
+                              const int* __restrict__ src, const double* __restrict__ out,
+                              double* __restrict__ g) {
+  const int q = blockIdx.x * blockDim.x + threadIdx.x;
+  if (q >= t) return;
+  double v = b[perm[T[q]]];
+  for (int k = ptr[q]; k < ptr[q + 1]; ++k) v -= out[src[k]];
+  g[q] = v;
 }
 
-MCS_API int mcs_mf_backward(int ntasks, const int* tasks, const void* nodes, const double* mats,
-                            const int* B, const double* y, const double* xp, double* s,
-                            void* stream) {
-  auto st = static_cast<cudaStream_t>(stream);
-  mf_backward<<<ntasks, MF_THREADS, 0, st>>>(tasks, static_cast<const NodeRec*>(nodes), mats, B,
-                                             y, xp, s);
-  return launch_status();
+// x_T = Sinv g (dense t x t, warp per row), scattered to xp[T[q]] and x[perm[T[q]]]
+__global__ void mf_top_solve(int t, const double* __restrict__ Sinv, const double* __restrict__ g,
+                             const int* __restrict__ T, const int* __restrict__ perm,
+                             double* __restrict__ xp, double* __restrict__ x) {
+  const int w = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
+  if (w >= t) return;
+  const double* row = Sinv + (int64_t)w * t;
+  double s = 0.0;
+  for (int j = lane; j < t; j += 32) s = fma(row[j], g[j], s);
+  s = warp_sum(s);
+  if (lane == 0) {
+    xp[T[w]] = s;
+    x[perm[T[w]]] = s;
+  }
 }
 
-MCS_API int mcs_mf_backward2(int ntasks, const int* tasks, const void* nodes, const double* mats,
-                             const double* s, const int* perm, double* xp, double* x,
-                             void* stream) {
+}  // namespace mcs
+
+MCS_API int mcs_mf_top(int t, const int* T, const int* perm, const double* b, const int* ptr,
+                       const int* src, const double* out, double* g, const double* Sinv,
+                       double* xp, double* x, void* stream) {
+  if (t <= 0) return 0;
   auto st = static_cast<cudaStream_t>(stream);
-  mf_backward2<<<ntasks, MF_THREADS, g_max_ns * sizeof(double), st>>>(
-      tasks, static_cast<const NodeRec*>(nodes), mats, s, perm, xp, x);
+  mf_top_gather<<<(t + 127) / 128, 128, 0, st>>>(t, T, perm, b, ptr, src, out, g);
+  int rc = launch_status();
+  if (rc) return rc;
+  const int64_t threads = (int64_t)t * 32;
+  mf_top_solve<<<(int)((threads + 255) / 256), 256, 0, st>>>(t, Sinv, g, T, perm, xp, x);
   return launch_status();
 }

@@ -73,6 +73,7 @@ def axpby(a, x, b, y, stream=None):
 
 class _ElemOperator:
     which = 0
+    graphable = True          # pure stream-ordered kernels: CUDA-graph capturable
 
     def __init__(self, sys_, M_dev, codes_dev, n):
         self.sys, self.k = sys_, sys_.k

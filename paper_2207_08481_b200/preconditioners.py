@@ -338,6 +338,8 @@ class ExtendedAsp:
     """S_d preconditioner lifted to S through the exact block factorisation
     (reference `:339-378`)."""
 
+    graphable = True          # every stage is a stream-ordered kernel
+
     def __init__(self, sys_, inner):
         if sys_.Sd_dev is None:
             raise ValueError("double_schur() must be run first")

@@ -7,7 +7,7 @@ import scipy.sparse as sp
 import scipy.sparse.linalg as spla
 
 from conftest import golden, rel
-from mf_emulate import emulate_solve
+from mf_emulate import emulate_hybrid, emulate_solve
 from oracle import mcs_oracle as O
 from paper_2207_08481_b200 import coarse as co
 from paper_2207_08481_b200 import engine, refblocks
@@ -143,3 +143,11 @@ def test_multifrontal_factor_exact(cfg, n, leaf):
     x = emulate_solve(F, b)
     ref = spla.spsolve(A.tocsc(), b)
     assert np.abs(x - ref).max() <= 1e-12 * np.abs(ref).max()
+    # with the dense top of the tree (what the GPU runs), small top budget
+    co_top = co.TOP_MAX
+    try:
+        co.TOP_MAX = 200
+        xh = emulate_hybrid(F, b)
+    finally:
+        co.TOP_MAX = co_top
+    assert np.abs(xh - ref).max() <= 1e-11 * np.abs(ref).max()
