@@ -168,6 +168,17 @@ class CondensedSystem:
             raise RuntimeError(f"{what} on element {int(bad[0])}")
 
 
+_PROGRAMS = {}
+
+
+def _device_program(k, refs):
+    """Block-generation program of degree k on the device (the reference
+    matrices depend on k only; built once per process)."""
+    if k not in _PROGRAMS:
+        _PROGRAMS[k] = [engine.to_dev(a) for a in engine.block_program(refs)]
+    return _PROGRAMS[k]
+
+
 def condense_sigma_omega(fes, nu: float, body_force=None, blocks=None,
                          stream=None) -> CondensedSystem:
     """Eliminate (sigma, omega) element-wise on the GPU (reference
@@ -187,7 +198,7 @@ def condense_sigma_omega(fes, nu: float, body_force=None, blocks=None,
         loads = np.array([b.load for b in blocks])
     else:
         W = engine.to_dev(element_weights(fes, nu))
-        prog = [engine.to_dev(a) for a in engine.block_program(refs)]
+        prog = _device_program(k, refs)
         records = engine.element_records(nt, W, prog, k, stream=stream)
         loads = load_vectors(fes, refs, body_force)
     S_dev, info = engine.condense(k, records, stream=stream)
@@ -196,7 +207,8 @@ def condense_sigma_omega(fes, nu: float, body_force=None, blocks=None,
     nu_l = refs.bus_vol.shape[0]
     np.add.at(load, maps.vv_l2g[:, :nu_l].ravel(),
               (loads * maps.vv_signs[:, :nu_l]).ravel())
-    sys_ = CondensedSystem(fes, nu, S_dev, load, maps, refs, records)
+    sys_ = CondensedSystem(fes, nu, S_dev, load, maps, refs, None)
+    del records                                   # blocks are not kept (1.3 GB at cfg2)
     sys_.check_info(info, "singular local stress block")
     return sys_
 

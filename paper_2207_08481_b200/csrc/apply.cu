@@ -373,8 +373,11 @@ static int launch_apply(const double* M, const int* codes, const double* x, doub
                         cudaStream_t st) {
   // one bulk stage per warp when a stage is large (k = 5, 6), two otherwise;
   // aim for ~64-96 KB of bulk copies in flight per SM
-  constexpr int W = STRIDE * 8 > 12000 ? 8 : 8;
-  constexpr int NST = STRIDE * 8 > 12000 ? 1 : 2;
+  // measured on B200 (tools/apply_variants.cu): warps in flight matter more
+  // than per-warp ring depth; one stage per warp, 8 warps, fills the SM
+  // (3 CTAs/SM at k = 4: 66% of HBM; k = 6: 69%)
+  constexpr int W = 8;
+  constexpr int NST = 1;
   auto kern = elem_apply_kernel<N, STRIDE, W, NST>;
   const size_t smem = (size_t)W * NST * STRIDE * sizeof(double);
   cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
@@ -397,7 +400,7 @@ template <int K>
 static int launch_restrict(const double* ext, const int* bidx, const int* cc, const double* r,
                            double* bubble, double* acc, int64_t nt, cudaStream_t st) {
   constexpr int LEN = ExtLen<K>::len;
-  constexpr int W = 8, NST = LEN * 8 > 12000 ? 1 : 2;
+  constexpr int W = 8, NST = 1;
   auto kern = ext_restrict_kernel<K, LEN, W, NST>;
   const size_t smem = (size_t)W * NST * LEN * sizeof(double);
   cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
@@ -415,7 +418,7 @@ static int launch_prolong(const double* ext, const int* bidx, const int* cc, con
   constexpr int LEN = ExtLen<K>::len;
   using Z = Sizes<K>;
   constexpr int XLE = even(Z::n_int * Z::ncpl);
-  constexpr int W = 8, NST = XLE * 8 > 12000 ? 1 : 2;
+  constexpr int W = 8, NST = 1;
   auto kern = ext_prolong_kernel<K, LEN, W, NST>;
   const size_t smem = (size_t)W * NST * XLE * sizeof(double);
   cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);

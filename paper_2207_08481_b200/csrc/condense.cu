@@ -332,18 +332,35 @@ static int launch_condense_v3(const double* recs, double* ST, int* info, int64_t
 
 // ---------------------------------------------- A1: element blocks on the GPU
 // rec[e][q] = sum_{p in prog[q]} W[e][widx[p]] * coef[p]   (refblocks.py)
-__global__ void element_blocks_kernel(const double* __restrict__ W, int nwgt,
-                                      const int* __restrict__ ptr, const int* __restrict__ widx,
-                                      const double* __restrict__ coef, int reclen,
-                                      double* __restrict__ recs, int64_t nt) {
-  extern __shared__ double sw[];
-  for (int64_t e = blockIdx.x; e < nt; e += gridDim.x) {
-    for (int r = threadIdx.x; r < nwgt; r += blockDim.x) sw[r] = W[e * nwgt + r];
+// A CTA handles EB elements at once so every program entry fetched from
+// L1/L2 serves EB elements; record writes are coalesced along q.
+constexpr int EB = 8;
+
+__global__ void __launch_bounds__(256)
+    element_blocks_kernel(const double* __restrict__ W, int nwgt, const int* __restrict__ ptr,
+                          const int* __restrict__ widx, const double* __restrict__ coef,
+                          int reclen, double* __restrict__ recs, int64_t nt) {
+  extern __shared__ double sw[];          // [EB][nwgt]
+  for (int64_t base = (int64_t)blockIdx.x * EB; base < nt; base += (int64_t)gridDim.x * EB) {
+    for (int r = threadIdx.x; r < EB * nwgt; r += blockDim.x) {
+      const int64_t e = base + r / nwgt;
+      sw[r] = e < nt ? W[e * nwgt + r % nwgt] : 0.0;
+    }
     __syncthreads();
     for (int q = threadIdx.x; q < reclen; q += blockDim.x) {
-      double s = 0.0;
-      for (int p = ptr[q]; p < ptr[q + 1]; ++p) s = fma(sw[widx[p]], coef[p], s);
-      recs[e * reclen + q] = s;
+      double acc[EB];
+#pragma unroll
+      for (int b = 0; b < EB; ++b) acc[b] = 0.0;
+      const int p1 = __ldg(ptr + q + 1);
+      for (int p = __ldg(ptr + q); p < p1; ++p) {
+        const int w = __ldg(widx + p);
+        const double c = __ldg(coef + p);
+#pragma unroll
+        for (int b = 0; b < EB; ++b) acc[b] = fma(sw[b * nwgt + w], c, acc[b]);
+      }
+#pragma unroll
+      for (int b = 0; b < EB; ++b)
+        if (base + b < nt) recs[(base + b) * reclen + q] = acc[b];
     }
     __syncthreads();
   }
@@ -448,8 +465,9 @@ MCS_API int mcs_element_blocks(int64_t nt, int nwgt, const double* W, int reclen
                                void* stream) {
   if (nt <= 0) return 0;
   auto st = static_cast<cudaStream_t>(stream);
-  const int grid = static_cast<int>(nt < 148 * 16 ? nt : 148 * 16);
-  element_blocks_kernel<<<grid, 256, nwgt * sizeof(double), st>>>(W, nwgt, prog_ptr, prog_widx,
-                                                                   prog_coef, reclen, records, nt);
+  const int64_t want = (nt + EB - 1) / EB;
+  const int grid = static_cast<int>(want < 148 * 8 ? want : 148 * 8);
+  element_blocks_kernel<<<grid, 256, EB * nwgt * sizeof(double), st>>>(
+      W, nwgt, prog_ptr, prog_widx, prog_coef, reclen, records, nt);
   return launch_status();
 }

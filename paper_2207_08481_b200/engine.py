@@ -7,7 +7,7 @@ record that a single 1-D bulk async copy can move):
   each segment padded to an even length (`record_layout`);
 * packed symmetric matrices: lower triangle, row-major, stride padded to an
   even length (S_T: `st_stride(k)`);
-* geometry weights [nt][38] (`refblocks.element_weights`).
+* geometry weights [nt][N_WEIGHTS] (`refblocks.element_weights`).
 """
 
 from __future__ import annotations
@@ -110,8 +110,8 @@ def block_program(refs: BlockRefs, rel_drop: float = 1e-15):
     add(L["msig"], refs.msig, [W_MSIG + r for r in range(6)])
     add(L["bws"], refs.bws, [W_BWS + a for a in range(3)])
     add(L["bus"], refs.bus_vol[None], [W_ONE])
-    add(L["bus"], refs.bus_edge.reshape(18, *refs.bus_vol.shape),
-        [W_BUSE + r for r in range(18)])
+    add(L["bus"], refs.bus_edge.reshape(9, *refs.bus_vol.shape),
+        [W_BUSE + r for r in range(9)])
     ns = refs.bhs.shape[-1]
     for e in range(3):
         # rows of edge e: bhs[e*k:(e+1)*k, :]

@@ -7,7 +7,7 @@ element geometry (J, detJ, the outward edge normals and the facet frames):
 
   msig = detJ/nu * sum_{a<=b} G_ab(J) Msym^{ab}         G_ab = T_a : T_b
   bws  = detJ * sum_a kappa_a(J) W^a                    kappa_a = skew(T_a)
-  bus  = Bvol + sum_{e,a,i} w^{bus}_{e,a,i} E^{e,a,i}   (edge term -<s_nn, u_n>)
+  bus  = Bvol + sum_{e,a} w^{bus}_{e,a} E^{e,a}         (edge term -<s_nn, u_n>)
   bhs  = sum_{e,a} w^{bhs}_{e,a} H^{e,a}                (rows of edge e only)
   adiv = nu/(2 detJ) * Adiv
   bpu  = Bpu                                            (J-invariant)
@@ -30,8 +30,8 @@ import numpy as np
 from .basis import DEV_COMPONENTS
 
 # weight table layout (per element)
-W_MSIG, W_BWS, W_BUSE, W_BHS, W_ADIV, W_ONE = 0, 6, 9, 27, 36, 37
-N_WEIGHTS = 38
+W_MSIG, W_BWS, W_BUSE, W_BHS, W_ADIV, W_ONE = 0, 6, 9, 18, 27, 28
+N_WEIGHTS = 30                      # 29 used, padded to an even count
 _PAIRS = ((0, 0), (1, 1), (2, 2), (0, 1), (0, 2), (1, 2))
 
 
@@ -53,7 +53,7 @@ class BlockRefs:
     msig: np.ndarray      # (6, ns, ns)
     bws: np.ndarray       # (3, nw, ns)
     bus_vol: np.ndarray   # (nu, ns)
-    bus_edge: np.ndarray  # (3, 3, 2, nu, ns)   [edge, a, i]
+    bus_edge: np.ndarray  # (3, 3, nu, ns)      [edge, a]
     bhs: np.ndarray       # (3, 3, k, ns)       [edge, a]
     adiv: np.ndarray      # (nu, nu)
     bpu: np.ndarray       # (nq, nu)
@@ -72,7 +72,11 @@ def build_refs(fes) -> BlockRefs:
     bws = np.einsum("wp,p,spa->aws", fes.tab_w, w, c)
     bus_vol = np.einsum("upi,p,spi->us", fes.tab_u, w, fes.tab_sigma_div)
     ue = fes.tab_u_edge                             # (nu, 3, nqe, 2)
-    bus_edge = np.einsum("uepi,p,sepa->eaius", ue, we, ce)
+    # u_n = (u_hat . J^T n_out) / detJ and J^T n_out = n_hat_e / |J^-T n_hat_e|,
+    # so only the reference normal component of u_hat enters
+    from .quadrature import REF_NORMALS
+    un_hat = np.einsum("uepi,ei->uep", ue, REF_NORMALS)
+    bus_edge = np.einsum("uep,p,sepa->eaus", un_hat, we, ce)
     leg = fes.tab_leg_edge[:k]
     bhs = np.einsum("hp,p,sepa->eahs", leg, we, ce)
     adiv = np.einsum("up,p,vp->uv", fes.tab_u_div, w, fes.tab_u_div)
@@ -95,10 +99,10 @@ def element_weights(fes, nu: float) -> np.ndarray:
     n = fes.edge_normal_out                          # (nt, 3, 2)
     ln = fes.edge_len                                # (nt, 3)
     snn = np.einsum("tei,taij,tej->tea", n, T, n)    # (nt, 3, 3)
-    JTn = np.einsum("tji,tej->tei", J, n)            # (nt, 3, 2)  (J^T n)_i
-    we = -(ln / det[:, None])[:, :, None, None] * snn[:, :, :, None] \
-        * JTn[:, :, None, :]                         # (nt, e, a, i)
-    W[:, W_BUSE:W_BUSE + 18] = we.reshape(nt, 18)
+    from .quadrature import REF_NORMALS
+    rho = np.linalg.norm(np.einsum("tji,ej->tei", fes.Jinv, REF_NORMALS), axis=2)  # |J^-T n_hat|
+    we = -(ln / (det[:, None] * rho))[:, :, None] * snn      # (nt, e, a)
+    W[:, W_BUSE:W_BUSE + 9] = we.reshape(nt, 9)
     nF = fes.mesh.facet_normal[fes.edge_facet]
     tF = fes.mesh.facet_tangent[fes.edge_facet]
     tsn = np.einsum("tei,taij,tej->tea", tF, T, nF)
@@ -116,7 +120,7 @@ def dense_blocks(refs: BlockRefs, W: np.ndarray):
     msig = np.einsum("tr,rij->tij", W[:, W_MSIG:W_MSIG + 6], refs.msig)
     bws = np.einsum("ta,awj->twj", W[:, W_BWS:W_BWS + 3], refs.bws)
     bus = refs.bus_vol[None] + np.einsum(
-        "tr,rus->tus", W[:, W_BUSE:W_BUSE + 18], refs.bus_edge.reshape(18, *refs.bus_vol.shape))
+        "tr,rus->tus", W[:, W_BUSE:W_BUSE + 9], refs.bus_edge.reshape(9, *refs.bus_vol.shape))
     wh = W[:, W_BHS:W_BHS + 9].reshape(-1, 3, 3)
     bhs = np.einsum("tea,eahs->tehs", wh, refs.bhs).reshape(len(W), 3 * k, -1)
     adiv = W[:, W_ADIV, None, None] * refs.adiv[None]
