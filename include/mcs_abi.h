@@ -99,10 +99,10 @@ int mcs_dense_gemv(int n, const double* A, const double* x, double* y, void* str
  * (node table, packed factors and gather sources built by coarse.py) */
 int mcs_mf_forward(int nnodes, const int* level_nodes, const void* nodes, const double* mats,
                    const int* src_t, const int* src_o, const int* perm, const double* b,
-                   double* y, double* out, void* stream);
+                   double* y, double* out, int max_ns, int max_nb, void* stream);
 int mcs_mf_backward(int nnodes, const int* level_nodes, const void* nodes, const double* mats,
                     const int* B, const int* perm, const double* y, double* xp, double* x,
-                    void* stream);
+                    int max_ns, int max_nb, void* stream);
 /* top of the tree (t dofs): g = b_T - frontier updates, x_T = Sinv g with the
  * dense inverse of the top Schur complement (= (A^-1)_TT) */
 int mcs_mf_top(int t, const int* T, const int* perm, const double* b, const int* ptr,

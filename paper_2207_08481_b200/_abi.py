@@ -41,8 +41,8 @@ SIGNATURES = {
     "mcs_csr_spmv": [_i, _p, _p, _p, _p, _p, _d, _d, _i, _p],
     "mcs_dense_gemv": [_i, _p, _p, _p, _p],
     # coarse.cu
-    "mcs_mf_forward": [_i, _p, _p, _p, _p, _p, _p, _p, _p, _p, _p],
-    "mcs_mf_backward": [_i, _p, _p, _p, _p, _p, _p, _p, _p, _p],
+    "mcs_mf_forward": [_i, _p, _p, _p, _p, _p, _p, _p, _p, _p, _i, _i, _p],
+    "mcs_mf_backward": [_i, _p, _p, _p, _p, _p, _p, _p, _p, _i, _i, _p],
     "mcs_mf_top": [_i, _p, _p, _p, _p, _p, _p, _p, _p, _p, _p, _p],
     # blas1.cu
     "mcs_reduce_workspace_len": [],

@@ -217,7 +217,9 @@ def _upload_multifrontal(F: MultifrontalFactor):
         src_t=engine.to_dev(src_t.astype(np.int32)),
         src_o=engine.to_dev(src_o.astype(np.int32)),
         perm=engine.to_dev(F.perm.astype(np.int32)),
-        levels=[(engine.to_dev(np.array(lv, dtype=np.int32)), len(lv)) for lv in F.levels[:H]],
+        levels=[(engine.to_dev(np.array(lv, dtype=np.int32)), len(lv),
+                 max(len(nodes[i].own) for i in lv), max(len(nodes[i].B) for i in lv))
+                for lv in F.levels[:H]],
         y=torch.empty(F.n, dtype=torch.float64, device="cuda"),
         xp=torch.empty(F.n, dtype=torch.float64, device="cuda"),
         out=torch.empty(max(oo, 1), dtype=torch.float64, device="cuda"),
@@ -293,19 +295,19 @@ class CoarseSolver:
             _abi.call("mcs_dense_gemv", self.n, _abi.ptr(self.data), _abi.ptr(b), _abi.ptr(x), st)
         else:
             d = self.data.dev
-            for ln, cnt in d["levels"]:                    # bottom levels, forward
+            for ln, cnt, mns, mnb in d["levels"]:          # bottom levels, forward
                 _abi.call("mcs_mf_forward", cnt, _abi.ptr(ln), _abi.ptr(d["nodes"]),
                           _abi.ptr(d["mats"]), _abi.ptr(d["src_t"]), _abi.ptr(d["src_o"]),
                           _abi.ptr(d["perm"]), _abi.ptr(b), _abi.ptr(d["y"]), _abi.ptr(d["out"]),
-                          st)
+                          mns, mnb, st)
             tp = d["top"]                                  # dense top Schur complement
             _abi.call("mcs_mf_top", tp["t"], _abi.ptr(tp["T"]), _abi.ptr(d["perm"]), _abi.ptr(b),
                       _abi.ptr(tp["ptr"]), _abi.ptr(tp["src"]), _abi.ptr(d["out"]),
                       _abi.ptr(tp["g"]), _abi.ptr(tp["Sinv"]), _abi.ptr(d["xp"]), _abi.ptr(x), st)
-            for ln, cnt in reversed(d["levels"]):          # bottom levels, backward
+            for ln, cnt, mns, mnb in reversed(d["levels"]):  # bottom levels, backward
                 _abi.call("mcs_mf_backward", cnt, _abi.ptr(ln), _abi.ptr(d["nodes"]),
                           _abi.ptr(d["mats"]), _abi.ptr(d["B"]), _abi.ptr(d["perm"]),
-                          _abi.ptr(d["y"]), _abi.ptr(d["xp"]), _abi.ptr(x), st)
+                          _abi.ptr(d["y"]), _abi.ptr(d["xp"]), _abi.ptr(x), mns, mnb, st)
         if self.scale != 1.0:
             from .operators import axpby
             axpby(1.0 / self.scale, x, 0.0, x, stream)

@@ -30,31 +30,45 @@ __device__ __forceinline__ double warp_sum(double v) {
   return v;
 }
 
+// shared layout per node: [t or s : ns][ys : ns][pass or xb : nb]
 __global__ void __launch_bounds__(MF_THREADS)
     mf_forward(const int* __restrict__ level_nodes, const NodeRec* __restrict__ nodes,
                const double* __restrict__ mats, const int* __restrict__ src_t,
                const int* __restrict__ src_o, const int* __restrict__ perm,
-               const double* __restrict__ b, double* __restrict__ y, double* __restrict__ out) {
+               const double* __restrict__ b, double* __restrict__ y, double* __restrict__ out,
+               int max_ns) {
   extern __shared__ double sm[];
-  double* t = sm;              // ns
-  double* ys = sm + 2048;      // ns (max 2048)
   const NodeRec nd = nodes[level_nodes[blockIdx.x]];
   const int ns = (int)nd.ns, nb = (int)nd.nb;
+  double* t = sm;
+  double* ys = sm + max_ns;
+  double* pass = sm + 2 * max_ns;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  for (int j = threadIdx.x; j < ns; j += MF_THREADS) {
-    const int64_t p = nd.s0 + j;
-    double v = b[perm[p]];
-    const int a = src_t[2 * p], c = src_t[2 * p + 1];
-    if (a >= 0) v -= out[a];
-    if (c >= 0) v -= out[c];
-    t[j] = v;
+  // all gathers up front, in parallel: own right-hand side and the child
+  // updates that pass through to the boundary
+  for (int j = threadIdx.x; j < ns + nb; j += MF_THREADS) {
+    if (j < ns) {
+      const int64_t p = nd.s0 + j;
+      double v = __ldg(b + __ldg(perm + p));
+      const int a = __ldg(src_t + 2 * p), c = __ldg(src_t + 2 * p + 1);
+      if (a >= 0) v -= out[a];
+      if (c >= 0) v -= out[c];
+      t[j] = v;
+    } else {
+      const int64_t q = nd.oo + (j - ns);
+      const int a = __ldg(src_o + 2 * q), c = __ldg(src_o + 2 * q + 1);
+      double v = 0.0;
+      if (a >= 0) v += out[a];
+      if (c >= 0) v += out[c];
+      pass[j - ns] = v;
+    }
   }
   __syncthreads();
   const double* L = mats + nd.oL;
   for (int r = warp; r < ns; r += MF_THREADS / 32) {
     const double* row = L + (int64_t)r * (r + 1) / 2;
     double s = 0.0;
-    for (int j = lane; j <= r; j += 32) s = fma(row[j], t[j], s);
+    for (int j = lane; j <= r; j += 32) s = fma(__ldg(row + j), t[j], s);
     s = warp_sum(s);
     if (lane == 0) {
       y[nd.s0 + r] = s;
@@ -66,15 +80,9 @@ __global__ void __launch_bounds__(MF_THREADS)
   for (int r = warp; r < nb; r += MF_THREADS / 32) {
     const double* row = W + (int64_t)r * ns;
     double s = 0.0;
-    for (int j = lane; j < ns; j += 32) s = fma(row[j], ys[j], s);
+    for (int j = lane; j < ns; j += 32) s = fma(__ldg(row + j), ys[j], s);
     s = warp_sum(s);
-    if (lane == 0) {
-      const int64_t q = nd.oo + r;
-      const int a = src_o[2 * q], c = src_o[2 * q + 1];
-      if (a >= 0) s += out[a];
-      if (c >= 0) s += out[c];
-      out[q] = s;
-    }
+    if (lane == 0) out[nd.oo + r] = s + pass[r];
   }
 }
 
@@ -82,27 +90,30 @@ __global__ void __launch_bounds__(MF_THREADS)
     mf_backward(const int* __restrict__ level_nodes, const NodeRec* __restrict__ nodes,
                 const double* __restrict__ mats, const int* __restrict__ B,
                 const int* __restrict__ perm, const double* __restrict__ y,
-                double* __restrict__ xp, double* __restrict__ x) {
+                double* __restrict__ xp, double* __restrict__ x, int max_ns) {
   extern __shared__ double sm[];
-  double* s = sm;
   const NodeRec nd = nodes[level_nodes[blockIdx.x]];
   const int ns = (int)nd.ns, nb = (int)nd.nb;
+  double* s = sm;
+  double* xb = sm + 2 * max_ns;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const double* WT = mats + nd.oWT;
   const int* Bp = B + nd.ob;
+  for (int j = threadIdx.x; j < nb; j += MF_THREADS) xb[j] = xp[__ldg(Bp + j)];
+  __syncthreads();
+  const double* WT = mats + nd.oWT;
   for (int r = warp; r < ns; r += MF_THREADS / 32) {
     const double* row = WT + (int64_t)r * nb;
     double a = 0.0;
-    for (int j = lane; j < nb; j += 32) a = fma(row[j], xp[Bp[j]], a);
+    for (int j = lane; j < nb; j += 32) a = fma(__ldg(row + j), xb[j], a);
     a = warp_sum(a);
-    if (lane == 0) s[r] = y[nd.s0 + r] - a;
+    if (lane == 0) s[r] = __ldg(y + nd.s0 + r) - a;
   }
   __syncthreads();
   const double* LT = mats + nd.oLT;     // packed upper, row r holds columns r..ns-1
   for (int r = warp; r < ns; r += MF_THREADS / 32) {
     const double* row = LT + (int64_t)r * ns - (int64_t)r * (r - 1) / 2 - r;
     double a = 0.0;
-    for (int j = r + lane; j < ns; j += 32) a = fma(row[j], s[j], a);
+    for (int j = r + lane; j < ns; j += 32) a = fma(__ldg(row + j), s[j], a);
     a = warp_sum(a);
     if (lane == 0) {
       xp[nd.s0 + r] = a;
@@ -117,25 +128,26 @@ using namespace mcs;
 
 MCS_API int mcs_mf_forward(int nnodes, const int* level_nodes, const void* nodes,
                            const double* mats, const int* src_t, const int* src_o,
-                           const int* perm, const double* b, double* y, double* out,
-                           void* stream) {
+                           const int* perm, const double* b, double* y, double* out, int max_ns,
+                           int max_nb, void* stream) {
   if (nnodes <= 0) return 0;
   auto st = static_cast<cudaStream_t>(stream);
-  const size_t smem = 2 * 2048 * sizeof(double);
+  const size_t smem = (2 * (size_t)max_ns + max_nb) * sizeof(double);
   cudaFuncSetAttribute(mf_forward, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   mf_forward<<<nnodes, MF_THREADS, smem, st>>>(level_nodes, static_cast<const NodeRec*>(nodes),
-                                               mats, src_t, src_o, perm, b, y, out);
+                                               mats, src_t, src_o, perm, b, y, out, max_ns);
   return launch_status();
 }
 
 MCS_API int mcs_mf_backward(int nnodes, const int* level_nodes, const void* nodes,
                             const double* mats, const int* B, const int* perm, const double* y,
-                            double* xp, double* x, void* stream) {
+                            double* xp, double* x, int max_ns, int max_nb, void* stream) {
   if (nnodes <= 0) return 0;
   auto st = static_cast<cudaStream_t>(stream);
-  const size_t smem = 2048 * sizeof(double);
+  const size_t smem = (2 * (size_t)max_ns + max_nb) * sizeof(double);
+  cudaFuncSetAttribute(mf_backward, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   mf_backward<<<nnodes, MF_THREADS, smem, st>>>(level_nodes, static_cast<const NodeRec*>(nodes),
-                                                mats, B, perm, y, xp, x);
+                                                mats, B, perm, y, xp, x, max_ns);
   return launch_status();
 }
 
