@@ -155,7 +155,7 @@ def run_ours(args, rank, world):
     dev = torch.device("cuda", int(os.environ.get("LOCAL_RANK", 0)))
     torch.cuda.set_device(dev)
     _abi.lib()
-    prob = baseline_config(2, args.n)
+    prob = baseline_config(args.cfg, args.n)
     fes = FeSystem(prob.mesh, prob.regions, prob.k)
     k, nt = prob.k, prob.mesh.num_triangles
     refs = refblocks.build_refs(fes)
@@ -291,7 +291,8 @@ def run_ours(args, rank, world):
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_per_step,
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
         "dtype": "f64", "data": "synthetic (seeded SURVEY §8d generators)",
-        "config": {"workload": WORKLOAD, "elements": nt, "k": k,
+        "config": {"workload": WORKLOAD if args.cfg == 2 else f"cfg{args.cfg} (see problems.py)",
+                   "elements": nt, "k": k,
                    "parallelism": "replicas" if world > 1 else "single-gpu",
                    "l2": "flushed (256 MiB write) before every timed step"},
         "breakdown_ms": {"A1_blocks": float(t_a1.mean()), "A3_condense": float(t_a3.mean()),
@@ -302,7 +303,7 @@ def run_ours(args, rank, world):
                            "frac": apply_bytes / (t_apply * 1e-3) / 1e9 / peaks["hbm_gbs"],
                            "traffic": ncu_traffic("elem_apply")},
         "pcg": pcg,
-        "roofline": {"bound": "fp64", "kernel": "condense_kernel<4,8> (A3)",
+        "roofline": {"bound": "fp64", "kernel": f"condense (A3), k={k}",
                      "achieved": achieved, "peak": peaks["fp64_tflops"], "unit": "TFLOP/s",
                      "frac": achieved / peaks["fp64_tflops"] if peaks["fp64_tflops"] else None,
                      "flops_per_element": f_cond,
@@ -377,13 +378,13 @@ def run_microbench(args, dev):
 _WORKER = {}
 
 
-def _cpu_init(n):
+def _cpu_init(cfg, n):
     import threadpoolctl
     sys.path.insert(0, ROOT)
     from paper_2207_08481_b200.dofmap import FeSystem
     from paper_2207_08481_b200.problems import baseline_config
     _WORKER["limits"] = threadpoolctl.threadpool_limits(1)
-    prob = baseline_config(2, n)
+    prob = baseline_config(cfg, n)
     _WORKER["prob"] = prob
     _WORKER["fes"] = FeSystem(prob.mesh, prob.regions, prob.k)
 
@@ -404,14 +405,15 @@ class CpuCondenser:
     """The reference algorithm on `procs` host processes; rate = elements /
     wall time of the slowest worker (setup excluded)."""
 
-    def __init__(self, n, procs):
+    def __init__(self, cfg, n, procs):
         from concurrent.futures import ProcessPoolExecutor
+        n = n or {1: 16, 2: 128, 3: 256}[cfg]
         self.n, self.procs = n, procs
         self.pool = None
         if procs > 1:
-            self.pool = ProcessPoolExecutor(procs, initializer=_cpu_init, initargs=(n,))
+            self.pool = ProcessPoolExecutor(procs, initializer=_cpu_init, initargs=(cfg, n))
         else:
-            _cpu_init(n)
+            _cpu_init(cfg, n)
         self.rng = np.random.default_rng(5)
 
     def rate(self, sample):
@@ -434,7 +436,7 @@ def run_reference(args, rank, world):
     if rank != 0:
         return None
     procs = os.cpu_count() or 1
-    cc = CpuCondenser(args.n, procs)
+    cc = CpuCondenser(args.cfg, args.n, procs)
     vals = []
     for _ in range(args.warmup):
         cc.rate(4 * procs)
@@ -443,14 +445,15 @@ def run_reference(args, rank, world):
         vals.append(v)
     cc.close()
     value = float(np.mean(vals))
-    sample = (f"{args.ref_sample_per_core * procs} random elements of cfg2 per step "
+    sample = (f"{args.ref_sample_per_core * procs} random elements of cfg{args.cfg} per step "
               f"(quadrature blocks + LU condensation + double Schur, oracle/mcs_oracle.py)")
     return {"metric": METRIC, "value": value, "unit": "elements/s", "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup,
-            "ms_per_step": 1e3 * 32768 / value,
+            "ms_per_step": 1e3 * 2 * cc.n * cc.n / value,
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
             "dtype": "f64", "data": "synthetic (seeded SURVEY §8d generators)",
-            "config": {"workload": WORKLOAD, "elements": 32768, "k": 4,
+            "config": {"workload": WORKLOAD if args.cfg == 2 else f"cfg{args.cfg} (see problems.py)",
+                       "elements": 2 * cc.n * cc.n, "k": {1: 2, 2: 4, 3: 6}[args.cfg],
                        "parallelism": f"{procs} host processes"},
             "impl": "reference",
             "cpu_baseline": {"value": value, "unit": "elements/s", "cores": procs,
@@ -465,7 +468,9 @@ def main():
     ap.add_argument("--steps", type=int, default=50)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--n", type=int, default=128)
+    ap.add_argument("--n", type=int, default=None, help="grid size (default: the config's)")
+    ap.add_argument("--cfg", type=int, default=2, choices=[1, 2, 3],
+                    help="BASELINE config of the bench workload (default 2 = configs[1])")
     ap.add_argument("--no-micro", dest="micro", action="store_false")
     ap.add_argument("--micro-count", type=int, default=1 << 20)
     ap.add_argument("--cpu-sample", type=int, default=3072)
@@ -487,7 +492,7 @@ def main():
     out = run_ours(args, rank, world)
     if rank == 0:
         # CPU baseline: the reference algorithm (oracle port), 1 core, bounded sample
-        cc = CpuCondenser(args.n, 1)
+        cc = CpuCondenser(args.cfg, args.n, 1)
         v, cnt = cc.rate(args.cpu_sample)
         out["cpu_baseline"] = {"value": v, "unit": "elements/s", "cores": 1, "kind": "port",
                                "sample": f"{cnt} random cfg2 elements, quadrature blocks + "

@@ -11,7 +11,7 @@
 // SYRK-like product.  Outputs:
 //   ext record  [X (n_int x ncpl, row-major) | S_oo^-1 (lower packed)]  (even stride)
 //   Sd_T        lower packed (even stride)
-#include "common.cuh"
+#include "elim_v3.cuh"
 
 namespace mcs {
 
@@ -127,6 +127,77 @@ __global__ void __launch_bounds__(THREADS)
   }
 }
 
+// ---- v3: the same DMMA blocked elimination engine as the condensation, on
+// K = [[S_oo, S_oc, I], [S_co, S_cc, 0], [I, 0, 0]]  (o = interior bubbles,
+// c = coupling dofs).  Eliminating the n_int (positive) o pivots leaves
+//   [[S_cc - S_co S_oo^-1 S_oc, -(S_oo^-1 S_oc)^T], [-S_oo^-1 S_oc, -S_oo^-1]]
+// = [[Sd_T, -X^T], [-X, -S_oo^-1]] as the trailing block, i.e. all three
+// outputs of the reference's double_schur in one elimination.
+template <int K, int W, int MINB>
+__global__ void __launch_bounds__(32 * W, MINB)
+    double_schur_v3(const double* __restrict__ ST, double* __restrict__ ext,
+                    double* __restrict__ Sd, int* __restrict__ info, int64_t nt) {
+  using Z = Sizes<K>;
+  using L = ExtLayout<K>;
+  constexpr int NI = Z::n_int, NC = Z::ncpl, NP = NI, NTR = NC + NI;
+  constexpr int NPP = (NP + 7) / 8 * 8, NCP = (NTR + 7) / 8 * 8;
+  using G = v3::Geo<(NPP + NCP) / 8, NPP / 8, W>;
+  extern __shared__ __align__(128) double smem[];
+  __shared__ int bad;
+  __shared__ signed char expect[NPP];
+  for (int i = threadIdx.x; i < NPP; i += blockDim.x) expect[i] = i < NP ? 1 : 0;
+  const v3::Smem<G> sm{smem};
+  const int warp = threadIdx.x >> 5;
+  for (int64_t e = blockIdx.x; e < nt; e += gridDim.x) {
+    if (threadIdx.x == 0) bad = 0;
+    __syncthreads();
+    const double* S = ST + e * L::st_len;
+    double* xo = ext + e * L::len;
+    double* so = Sd + e * L::sd_len;
+    // real index -> local S_T index: o rows, then c rows; E rows return -1
+    auto loc = [](int r) { return r < NI ? Z::n_em + r : (r < NI + NC ? cpl_local<K>(r - NI) : -1); };
+    auto load = [&](int i, int j) {
+      return v3::padded_entry<NP, NTR, NPP>(i, j, [&](int ri, int rj) {
+        const int li = loc(ri), lj = loc(rj);
+        if (li >= 0 && lj >= 0) return __ldg(S + (li >= lj ? pk(li, lj) : pk(lj, li)));
+        // E rows: identity against the o columns
+        if (li < 0 && lj >= 0) return (rj < NI && ri - NI - NC == rj) ? 1.0 : 0.0;
+        return 0.0;
+      });
+    };
+    auto store = [&](int i, int j, double v) {
+      i -= NPP;
+      j -= NPP;
+      if (j > i || i >= NTR) return;
+      if (i < NC) so[pk(i, j)] = v;                                  // Sd_T
+      else if (j < NC) xo[(i - NC) * NC + j] = -v;                    // X
+      else xo[L::x_len + pk(i - NC, j - NC)] = -v;                    // S_oo^-1
+    };
+    v3::dispatch<G>(warp, load, store, sm, expect, &bad);
+    __syncthreads();
+    if (threadIdx.x == 0 && info) info[e] = bad;
+  }
+}
+
+template <int K, int W, int MINB>
+static int launch_double_schur_v3(const double* ST, double* ext, double* Sd, int* info, int64_t nt,
+                                  cudaStream_t st) {
+  using Z = Sizes<K>;
+  constexpr int NPP = (Z::n_int + 7) / 8 * 8, NCP = (Z::ncpl + Z::n_int + 7) / 8 * 8;
+  using G = v3::Geo<(NPP + NCP) / 8, NPP / 8, W>;
+  auto kern = double_schur_v3<K, W, MINB>;
+  const size_t smem = G::SMEM * sizeof(double);
+  cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  int per_sm = 1, dev = 0, nsm = 148;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, 32 * W, smem);
+  if (per_sm < 1) per_sm = 1;
+  const int64_t g = (int64_t)per_sm * nsm;
+  kern<<<(int)(nt < g ? nt : g), 32 * W, smem, st>>>(ST, ext, Sd, info, nt);
+  return launch_status();
+}
+
 template <int K>
 static int launch_double_schur(const double* ST, double* ext, double* Sd, int* info, int64_t nt,
                                cudaStream_t st) {
@@ -179,11 +250,11 @@ MCS_API int mcs_double_schur(int k, int64_t nt, const double* S_packed, double* 
   if (nt <= 0) return 0;
   auto st = static_cast<cudaStream_t>(stream);
   switch (k) {
-    case 2: return launch_double_schur<2>(S_packed, ext, Sd_packed, info, nt, st);
-    case 3: return launch_double_schur<3>(S_packed, ext, Sd_packed, info, nt, st);
-    case 4: return launch_double_schur<4>(S_packed, ext, Sd_packed, info, nt, st);
-    case 5: return launch_double_schur<5>(S_packed, ext, Sd_packed, info, nt, st);
-    case 6: return launch_double_schur<6>(S_packed, ext, Sd_packed, info, nt, st);
+    case 2: return launch_double_schur_v3<2, 2, 6>(S_packed, ext, Sd_packed, info, nt, st);
+    case 3: return launch_double_schur_v3<3, 2, 4>(S_packed, ext, Sd_packed, info, nt, st);
+    case 4: return launch_double_schur_v3<4, 2, 4>(S_packed, ext, Sd_packed, info, nt, st);
+    case 5: return launch_double_schur_v3<5, 4, 2>(S_packed, ext, Sd_packed, info, nt, st);
+    case 6: return launch_double_schur_v3<6, 4, 2>(S_packed, ext, Sd_packed, info, nt, st);
   }
   return -1000;
 }

@@ -107,6 +107,13 @@ __device__ __forceinline__ int inverse8_to(double v0, double v1, double* W, doub
   return badj;
 }
 
+#ifdef MCS_PHASE_PROF
+__device__ unsigned long long g_v3prof[8 * 8];
+#define V3T(i) do { long long _t = pclock(); vprof[i] += _t - tprev; tprev = _t; } while (0)
+#else
+#define V3T(i) do {} while (0)
+#endif
+
 // one warp role: tiles g = ROLE + t*W
 template <class G, int ROLE>
 struct Role {
@@ -161,12 +168,17 @@ __device__ __forceinline__ void run_role(double (&acc)[Role<G, ROLE>::T][2], LOA
   using RL = Role<G, ROLE>;
   constexpr int T = RL::T;
   const int lane = threadIdx.x & 31, gr = lane >> 2, tg = lane & 3;
+#ifdef MCS_PHASE_PROF
+  long long vprof[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+  long long tprev = pclock();
+#endif
 #pragma unroll
   for (int t = 0; t < T; ++t) {
     const int i = RL::bi(t) * 8 + gr;
 #pragma unroll
     for (int q = 0; q < 2; ++q) acc[t][q] = load(i, RL::bj(t) * 8 + 2 * tg + q);
   }
+  V3T(0);
   double dv0 = 0.0, dv1 = 0.0;
   auto diag_inverse = [&](int c) {
     const int b = inverse8_to(dv0, dv1, sm.GJ(), sm.P(c), expect + 8 * c);
@@ -205,6 +217,7 @@ __device__ __forceinline__ void run_role(double (&acc)[Role<G, ROLE>::T][2], LOA
   __syncwarp();
   panel_z(0);
   __syncthreads();
+  V3T(1);
   for (int pb = 0; pb < G::NPB; ++pb) {
     const int nx = pb + 1;
     const bool look = nx < G::NPB;
@@ -225,17 +238,26 @@ __device__ __forceinline__ void run_role(double (&acc)[Role<G, ROLE>::T][2], LOA
         }
       }
     }
+    V3T(2);
     if (look && ROLE == (nx * G::NB - nx * (nx - 1) / 2) % G::W) diag_inverse(nx);
+    V3T(3);
     // C2: the rest of the trailing matrix
 #pragma unroll
     for (int t = 0; t < T; ++t)
       if (RL::bj(t) > nx) upd(true, acc[t][0], acc[t][1], sm.Z(pb, RL::bi(t)), sm.R(pb, RL::bj(t)));
+    V3T(4);
     if (look) {
       __syncwarp();
       panel_z(nx);
     }
+    V3T(5);
     __syncthreads();
+    V3T(6);
   }
+#ifdef MCS_PHASE_PROF
+  if (lane == 0 && blockIdx.x == 0)
+    for (int q = 0; q < 8; ++q) atomicAdd(&g_v3prof[8 * ROLE + q], (unsigned long long)vprof[q]);
+#endif
 }
 
 template <class G, int ROLE, class STORE>
