@@ -131,14 +131,18 @@ def load_peaks():
     return peaks
 
 
-def ncu_traffic(name):
-    """dram bytes per launch from the committed ncu summary, if any."""
+def ncu_traffic(prefix):
+    """DRAM bytes (read + write) per launch of the kernel whose name starts
+    with `prefix`, from the committed `ncu --set full` summary, if any."""
     try:
-        with open(os.path.join(ROOT, "profiles", "ncu_summary_r01.json")) as fh:
+        with open(os.path.join(ROOT, "profiles", "ncu_kernels_r01.json")) as fh:
             d = json.load(fh)
-        return d.get(name, {}).get("dram_bytes")
     except OSError:
         return None
+    for name, rec in d.items():
+        if name.startswith(prefix):
+            return rec.get("dram_bytes")
+    return None
 
 
 def run_ours(args, rank, world):
@@ -301,13 +305,13 @@ def run_ours(args, rank, world):
         "apply_roofline": {"bound": "hbm", "achieved": apply_bytes / (t_apply * 1e-3) / 1e9,
                            "peak": peaks["hbm_gbs"], "unit": "GB/s",
                            "frac": apply_bytes / (t_apply * 1e-3) / 1e9 / peaks["hbm_gbs"],
-                           "traffic": ncu_traffic("elem_apply")},
+                           "traffic": ncu_traffic(f"elem_apply_kernel<{z['nloc']},")},
         "pcg": pcg,
         "roofline": {"bound": "fp64", "kernel": f"condense (A3), k={k}",
                      "achieved": achieved, "peak": peaks["fp64_tflops"], "unit": "TFLOP/s",
                      "frac": achieved / peaks["fp64_tflops"] if peaks["fp64_tflops"] else None,
                      "flops_per_element": f_cond,
-                     "traffic": ncu_traffic("condense"),
+                     "traffic": ncu_traffic(f"condense_v3<{k},") or ncu_traffic(f"condense_kernel<{k},"),
                      "peak_source": "profiles/fp64_peak_r01.json (measured DMMA/DFMA max)"},
         "e2e": {"value": world * nt / (e2e_ms * 1e-3), "unit": "elements/s",
                 "h2d_bytes_per_step": W_h.nbytes, "d2h_bytes_per_step": out_bytes,

@@ -117,10 +117,13 @@ def cg(apply_A, b, apply_M=None, rtol=1e-8, maxit=1000, stream=None, use_graph=T
     per iteration.  The step computes z = M r before the host has seen the
     stopping test; when the test then stops the loop that z is unused, so x,
     the residual history and the iteration count are the reference loop's."""
+    import os
     bd, host = as_device(b)
     n = bd.numel()
     ws: Workspace = workspace()
     sc = ws.sc
+    # MCS_NO_GRAPH=1: eager launches (ncu launch lists; ncu does not replay graphs)
+    use_graph = use_graph and os.environ.get("MCS_NO_GRAPH", "0") != "1"
     graphable = use_graph and _graphable(apply_A) and _graphable(apply_M)
     key = (id(apply_A), id(apply_M), n)
     S = _STATES.get(key) if graphable else None
