@@ -1,25 +1,23 @@
 // Per-element static condensation on B200.
 //
 // One CTA owns one element at a time (persistent over elements).  The
-// element's symmetric augmented saddle matrix is padded to a multiple of 8
-// (dummy unit pivots / zero trailing rows), held in registers as 8x8 DMMA
-// accumulator tiles spread over the CTA's warps, and eliminated block by
-// block on the FP64 tensor cores (elim_dmma.cuh):
+// element's symmetric augmented saddle matrix, padded to a multiple of 8, is
+// eliminated on the FP64 tensor cores by the left-looking signed-Cholesky
+// engine of elim_v5.cuh (panel in shared memory, trailing block in
+// registers, one look-ahead diagonal per column):
 //
 //   microbench (A5):   K = [[A, B], [B^T, 0]]  -> eliminate the n_s (positive)
-//                      pivots -> trailing block = -B^T A^-1 B = -S
+//                      pivots -> S = B^T A^-1 B
 //   MCS (A3):          K = [[msig, bws^T, Bsig^T], [bws, 0, 0], [Bsig, 0, -adiv]]
-//                      -> n_s positive then n_w negative pivots -> trailing
-//                      block = -S_T, the reference's S_T of
-//                      condensation.py:161-176 (LU of [[-msig, bws^T],
-//                      [bws, 0]] then adiv - Bsig M^-1 Bsig^T), proved equal in
-//                      DESIGN.md §3.
+//                      -> n_s positive then n_w negative pivots -> S_T, the
+//                      reference's S_T of condensation.py:161-176 (LU of
+//                      [[-msig, bws^T], [bws, 0]] then adiv - Bsig M^-1
+//                      Bsig^T), proved equal in DESIGN.md §3.
 //
-// The next element's input is prefetched into shared memory with a 1-D bulk
-// async copy (TMA engine, cp.async.bulk + mbarrier) issued as soon as the
-// current element's tiles are in registers, so HBM traffic overlaps the
-// elimination of the current element.
-#include "elim_v3.cuh"
+// Raw block entries are read once, straight from the element record in HBM
+// into the DMMA accumulators that consume them.  The tiny (8, 4) microbench
+// shape keeps the register-tile engine of elim_dmma.cuh.
+#include "elim_v5.cuh"  // includes elim_dmma.cuh
 
 namespace mcs {
 
@@ -163,152 +161,60 @@ struct Record {
   static constexpr int st_len = even(npk(Z::nloc));   // packed S_T stride
 };
 
-template <int K>
-__device__ __forceinline__ double mcs_entry(const double* rec, int i, int j) {
-  using Z = Sizes<K>;
-  using R = Record<K>;
-  constexpr int ns = Z::ns, nu = Z::nu, c0 = Z::ns + Z::nw;
-  if (i < ns) return rec[R::o_msig + i * ns + j];
-  if (i < c0) return j < ns ? rec[R::o_bws + (i - ns) * ns + j] : 0.0;
-  const int l = i - c0;
-  if (j < ns) return l < nu ? rec[R::o_bus + l * ns + j] : rec[R::o_bhs + (l - nu) * ns + j];
-  if (j < c0) return 0.0;
-  const int m = j - c0;
-  return (l < nu && m < nu) ? -rec[R::o_adiv + l * nu + m] : 0.0;
+template <class Kern>
+static int persistent_grid(Kern k, int threads, size_t smem, int64_t n);
+
+// ------------------------------- v5 kernels (Crout signed Cholesky, elim_v5.cuh)
+
+__device__ __forceinline__ void init_signs(signed char* ex, int npp, int npos, int np) {
+  for (int i = threadIdx.x; i < npp; i += blockDim.x) ex[i] = (i < npos || i >= np) ? 1 : -1;
 }
 
-template <int K, int W, int MINB = 1>
-__global__ void __launch_bounds__(32 * W, MINB)
-    condense_kernel(const double* __restrict__ recs, double* __restrict__ ST,
-                    int* __restrict__ info, int64_t nt) {
-  using Z = Sizes<K>;
-  using R = Record<K>;
-  constexpr int NP = Z::ns + Z::nw, NC = Z::nloc;
-  using P = Pad<NP, NC, W>;
-  using E = typename P::E;
-  extern __shared__ __align__(128) double srec[];
-  double* work = srec + R::len;
-  __shared__ __align__(8) uint64_t bar;
-  __shared__ int bad;
-  __shared__ int flag;
-  __shared__ signed char expect[P::NPP];
-  init_expect(expect, P::NPP, Z::ns, NP);
-  int64_t e = blockIdx.x;
-  if (threadIdx.x == 0) {
-    mbar_init(&bar, 1);
-    fence_barrier_init();
-  }
-  __syncthreads();
-  if (threadIdx.x == 0 && e < nt) {
-    mbar_expect_tx(&bar, R::len * 8);
-    bulk_g2s(srec, recs + e * R::len, R::len * 8, &bar);
-  }
-  uint32_t phase = 0;
-  for (; e < nt; e += gridDim.x) {
-    mbar_wait(&bar, phase);
-    phase ^= 1;
-    double acc[E::TPW][2];
-    int tij[E::TPW];
-    load_tiles<P, NP, NC>(acc, tij, [&](int i, int j) { return mcs_entry<K>(srec, i, j); });
-    if (threadIdx.x == 0) {
-      bad = 0;
-      flag = -1;
-    }
-    __syncthreads();
-    const int64_t nxt = e + gridDim.x;
-    if (threadIdx.x == 0 && nxt < nt) {
-      mbar_expect_tx(&bar, R::len * 8);
-      bulk_g2s(srec, recs + nxt * R::len, R::len * 8, &bar);
-    }
-    eliminate_tiles<E>(acc, tij, work, expect, &bad, &flag);
-    store_trailing<P, NC>(acc, tij, ST + e * R::st_len);
-    __syncthreads();
-    if (threadIdx.x == 0 && info) info[e] = bad;
-  }
-}
-
-// ------------------------------------------- v3 kernels (compile-time roles)
+template <int NS, int NC, int W>
+using MicroGeo5 = v5::Geo<((NS + 7) / 8 * 8 + (NC + 7) / 8 * 8) / 8, (NS + 7) / 8, W, NS, NS>;
 
 template <int NS, int NC, int W, int MINB>
 __global__ void __launch_bounds__(32 * W, MINB)
-    spd_schur_v3(const double* __restrict__ A, const double* __restrict__ B,
+    spd_schur_v5(const double* __restrict__ A, const double* __restrict__ B,
                  double* __restrict__ S, int* __restrict__ info, int64_t batch) {
-  using P = Pad<NS, NC, W>;
-  using G = v3::Geo<P::NB, P::NPB, W>;
+  using G = MicroGeo5<NS, NC, W>;
+  constexpr int NPP = 8 * G::NPB;
   constexpr int LA = npk(NS), LB = NS * NC, LS = npk(NC);
   extern __shared__ __align__(128) double smem[];
   __shared__ int bad;
-  __shared__ signed char expect[P::NPP];
-  init_expect(expect, P::NPP, NS, NS);
-  const v3::Smem<G> sm{smem};
-  const int warp = threadIdx.x >> 5;
+  __shared__ signed char expect[NPP];
+  init_signs(expect, NPP, NS, NS);
   for (int64_t e = blockIdx.x; e < batch; e += gridDim.x) {
     if (threadIdx.x == 0) bad = 0;
     __syncthreads();
     const double* Ae = A + e * LA;
     const double* Be = B + e * LB;
     double* Se = S + e * LS;
-    auto load = [&](int i, int j) {
-      return v3::padded_entry<NS, NC, P::NPP>(i, j, [&](int ri, int rj) {
-        return ri < NS ? __ldg(Ae + pk(ri, rj)) : (rj < NS ? __ldg(Be + rj * NC + (ri - NS)) : 0.0);
-      });
+    auto entry = [&](int i, int j) -> const double* {  // padded (i, j), j < NPP
+      if (i < NS) return j <= i ? Ae + pk(i, j) : v5::zero_src();
+      if (i < NPP) return i == j ? v5::one_src() : v5::zero_src();
+      return (i - NPP < NC && j < NS) ? Be + j * NC + (i - NPP) : v5::zero_src();
     };
+    auto fetch = [&](int bi, int bj) {
+      const int lane = threadIdx.x & 31, i = 8 * bi + (lane >> 2), j = 8 * bj + 2 * (lane & 3);
+      return make_double2(__ldg(entry(i, j)), __ldg(entry(i, j + 1)));
+    };
+    auto trail = [](int, int) { return 0.0; };
     auto store = [&](int i, int j, double v) {
-      i -= P::NPP;
-      j -= P::NPP;
-      if (j <= i && i < NC) Se[pk(i, j)] = -v;
+      i -= NPP;
+      if (i < NC) Se[pk(i, j - NPP)] = v;
     };
-    v3::dispatch<G>(warp, load, store, sm, expect, &bad);
+    v5::eliminate<G>(fetch, trail, store, smem, expect, &bad);
     __syncthreads();
     if (threadIdx.x == 0 && info) info[e] = bad;
   }
 }
-
-template <int K, int W, int MINB>
-__global__ void __launch_bounds__(32 * W, MINB)
-    condense_v3(const double* __restrict__ recs, double* __restrict__ ST, int* __restrict__ info,
-                int64_t nt) {
-  using Z = Sizes<K>;
-  using R = Record<K>;
-  constexpr int NP = Z::ns + Z::nw, NC = Z::nloc;
-  using P = Pad<NP, NC, W>;
-  using G = v3::Geo<P::NB, P::NPB, W>;
-  extern __shared__ __align__(128) double smem[];
-  __shared__ int bad;
-  __shared__ signed char expect[P::NPP];
-  init_expect(expect, P::NPP, Z::ns, NP);
-  const v3::Smem<G> sm{smem};
-  const int warp = threadIdx.x >> 5;
-  for (int64_t e = blockIdx.x; e < nt; e += gridDim.x) {
-    if (threadIdx.x == 0) bad = 0;
-    __syncthreads();
-    const double* rec = recs + e * R::len;
-    double* Se = ST + e * R::st_len;
-    auto load = [&](int i, int j) {
-      return v3::padded_entry<NP, NC, P::NPP>(i, j, [&](int ri, int rj) {
-        return mcs_entry<K>(rec, ri, rj);
-      });
-    };
-    auto store = [&](int i, int j, double v) {
-      i -= P::NPP;
-      j -= P::NPP;
-      if (j <= i && i < NC) Se[pk(i, j)] = -v;
-    };
-    v3::dispatch<G>(warp, load, store, sm, expect, &bad);
-    __syncthreads();
-    if (threadIdx.x == 0 && info) info[e] = bad;
-  }
-}
-
-template <class Kern>
-static int persistent_grid(Kern k, int threads, size_t smem, int64_t n);
 
 template <int NS, int NC, int W, int MINB>
-static int launch_spd_schur_v3(const double* A, const double* B, double* S, int* info,
+static int launch_spd_schur_v5(const double* A, const double* B, double* S, int* info,
                                int64_t batch, cudaStream_t st) {
-  using P = Pad<NS, NC, W>;
-  using G = v3::Geo<P::NB, P::NPB, W>;
-  auto kern = spd_schur_v3<NS, NC, W, MINB>;
+  using G = MicroGeo5<NS, NC, W>;
+  auto kern = spd_schur_v5<NS, NC, W, MINB>;
   const size_t smem = G::SMEM * sizeof(double);
   cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   const int grid = persistent_grid(kern, 32 * W, smem, batch);
@@ -316,13 +222,59 @@ static int launch_spd_schur_v3(const double* A, const double* B, double* S, int*
   return launch_status();
 }
 
+template <int K, int W>
+using McsGeo5 = v5::Geo<((Sizes<K>::ns + Sizes<K>::nw + 7) / 8 * 8 + (Sizes<K>::nloc + 7) / 8 * 8) / 8,
+                        (Sizes<K>::ns + Sizes<K>::nw + 7) / 8, W, Sizes<K>::ns + Sizes<K>::nw,
+                        Sizes<K>::ns>;
+
 template <int K, int W, int MINB>
-static int launch_condense_v3(const double* recs, double* ST, int* info, int64_t nt,
-                              cudaStream_t st) {
+__global__ void __launch_bounds__(32 * W, MINB)
+    condense_v5(const double* __restrict__ recs, double* __restrict__ ST, int* __restrict__ info,
+                int64_t nt) {
   using Z = Sizes<K>;
-  using P = Pad<Z::ns + Z::nw, Z::nloc, W>;
-  using G = v3::Geo<P::NB, P::NPB, W>;
-  auto kern = condense_v3<K, W, MINB>;
+  using R = Record<K>;
+  using G = McsGeo5<K, W>;
+  constexpr int ns = Z::ns, nu = Z::nu, NP = Z::ns + Z::nw, NPP = 8 * G::NPB;
+  extern __shared__ __align__(128) double smem[];
+  __shared__ int bad;
+  __shared__ signed char expect[NPP];
+  for (int i = threadIdx.x; i < NPP; i += blockDim.x) expect[i] = i < ns ? 1 : -1;
+  for (int64_t e = blockIdx.x; e < nt; e += gridDim.x) {
+    if (threadIdx.x == 0) bad = 0;
+    __syncthreads();
+    const double* rec = recs + e * R::len;
+    double* Se = ST + e * R::st_len;
+    auto entry = [&](int i, int j) -> const double* {  // padded (i, j), j < NPP
+      if (i < ns) return j <= i ? rec + R::o_msig + i * ns + j : v5::zero_src();
+      if (i < NP) return j < ns ? rec + R::o_bws + (i - ns) * ns + j : v5::zero_src();
+      if (i < NPP) return i == j ? v5::minus_one_src() : v5::zero_src();  // padding: -1 pivots
+      const int l = i - NPP;
+      if (l >= Z::nloc || j >= ns) return v5::zero_src();
+      return l < nu ? rec + R::o_bus + l * ns + j : rec + R::o_bhs + (l - nu) * ns + j;
+    };
+    auto fetch = [&](int bi, int bj) {
+      const int lane = threadIdx.x & 31, i = 8 * bi + (lane >> 2), j = 8 * bj + 2 * (lane & 3);
+      return make_double2(__ldg(entry(i, j)), __ldg(entry(i, j + 1)));
+    };
+    auto trail = [&](int i, int j) {
+      const int l = i - NPP, m = j - NPP;
+      return (l < nu && m < nu) ? __ldg(rec + R::o_adiv + l * nu + m) : 0.0;
+    };
+    auto store = [&](int i, int j, double v) {
+      i -= NPP;
+      if (i < Z::nloc) Se[pk(i, j - NPP)] = v;
+    };
+    v5::eliminate<G>(fetch, trail, store, smem, expect, &bad);
+    __syncthreads();
+    if (threadIdx.x == 0 && info) info[e] = bad;
+  }
+}
+
+template <int K, int W, int MINB>
+static int launch_condense_v5(const double* recs, double* ST, int* info, int64_t nt,
+                              cudaStream_t st) {
+  using G = McsGeo5<K, W>;
+  auto kern = condense_v5<K, W, MINB>;
   const size_t smem = G::SMEM * sizeof(double);
   cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   const int grid = persistent_grid(kern, 32 * W, smem, nt);
@@ -399,18 +351,6 @@ static int launch_spd_schur(const double* A, const double* B, double* S, int* in
   return launch_status();
 }
 
-template <int K, int W, int MINB = 1>
-static int launch_condense(const double* recs, double* ST, int* info, int64_t nt, cudaStream_t st) {
-  using Z = Sizes<K>;
-  using P = Pad<Z::ns + Z::nw, Z::nloc, W>;
-  auto kern = condense_kernel<K, W, MINB>;
-  const size_t smem = (Record<K>::len + P::E::SMEM_WORK) * sizeof(double);
-  cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-  const int grid = persistent_grid(kern, 32 * W, smem, nt);
-  kern<<<grid, 32 * W, smem, st>>>(recs, ST, info, nt);
-  return launch_status();
-}
-
 }  // namespace mcs
 
 using namespace mcs;
@@ -419,7 +359,7 @@ MCS_API int mcs_spd_schur_batched(int n, int m, int64_t batch, const double* A_p
                                   const double* B, double* S_packed, int* info, void* stream) {
   if (batch <= 0) return 0;
   auto st = static_cast<cudaStream_t>(stream);
-  if (n == 60 && m == 36) return launch_spd_schur_v3<60, 36, 2, 4>(A_packed_lower, B, S_packed, info, batch, st);
+  if (n == 60 && m == 36) return launch_spd_schur_v5<60, 36, 4, 5>(A_packed_lower, B, S_packed, info, batch, st);
   if (n == 8 && m == 4) return launch_spd_schur<8, 4, 2>(A_packed_lower, B, S_packed, info, batch, st);
   return -1000;  // unsupported shape (compiled instantiations only)
 }
@@ -451,11 +391,12 @@ MCS_API int mcs_condense(int k, int64_t nt, const double* records, double* S_pac
   if (nt <= 0) return 0;
   auto st = static_cast<cudaStream_t>(stream);
   switch (k) {
-    case 2: return launch_condense_v3<2, 2, 6>(records, S_packed, info, nt, st);
-    case 3: return launch_condense_v3<3, 2, 4>(records, S_packed, info, nt, st);
-    case 4: return launch_condense_v3<4, 2, 4>(records, S_packed, info, nt, st);
-    case 5: return launch_condense<5, 12>(records, S_packed, info, nt, st);
-    case 6: return launch_condense<6, 16>(records, S_packed, info, nt, st);
+    // v5 engine (elim_v5.cuh); warps / CTAs per SM from tools/condense_v5_sweep.cu
+    case 2: return launch_condense_v5<2, 2, 8>(records, S_packed, info, nt, st);
+    case 3: return launch_condense_v5<3, 2, 8>(records, S_packed, info, nt, st);
+    case 4: return launch_condense_v5<4, 4, 4>(records, S_packed, info, nt, st);
+    case 5: return launch_condense_v5<5, 8, 2>(records, S_packed, info, nt, st);
+    case 6: return launch_condense_v5<6, 8, 2>(records, S_packed, info, nt, st);
   }
   return -1000;
 }

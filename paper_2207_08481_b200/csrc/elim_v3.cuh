@@ -221,17 +221,17 @@ __device__ __forceinline__ void run_role(double (&acc)[Role<G, ROLE>::T][2], LOA
   for (int pb = 0; pb < G::NPB; ++pb) {
     const int nx = pb + 1;
     const bool look = nx < G::NPB;
-    // C1: column nx
+    // C1: column nx (its diagonal tile is first in column-major order, so
+    // the owner starts the inversion before updating the rest)
 #pragma unroll
     for (int t = 0; t < T; ++t) {
-      // tiles of column nx: the column-major order makes them contiguous
-      const bool in_col = RL::bj(t) == nx;
-      if (in_col) {
+      if (RL::bj(t) == nx) {
         upd(true, acc[t][0], acc[t][1], sm.Z(pb, RL::bi(t)), sm.R(pb, RL::bj(t)));
         if (look) {
           if (RL::bi(t) == nx) {
             dv0 = acc[t][0];
             dv1 = acc[t][1];
+            diag_inverse(nx);
           } else {
             put(sm.R(nx, RL::bi(t)), acc[t][0], acc[t][1]);
           }
@@ -239,12 +239,20 @@ __device__ __forceinline__ void run_role(double (&acc)[Role<G, ROLE>::T][2], LOA
       }
     }
     V3T(2);
-    if (look && ROLE == (nx * G::NB - nx * (nx - 1) / 2) % G::W) diag_inverse(nx);
     V3T(3);
-    // C2: the rest of the trailing matrix
+    // C2: the rest of the trailing matrix, k-split outer so the two DMMAs of
+    // a tile are far apart (no accumulator dependency stalls)
 #pragma unroll
-    for (int t = 0; t < T; ++t)
-      if (RL::bj(t) > nx) upd(true, acc[t][0], acc[t][1], sm.Z(pb, RL::bi(t)), sm.R(pb, RL::bj(t)));
+    for (int kk = 0; kk < 8; kk += 4) {
+#pragma unroll
+      for (int t = 0; t < T; ++t) {
+        if (RL::bj(t) > nx) {
+          const double* Z = sm.Z(pb, RL::bi(t));
+          const double* R = sm.R(pb, RL::bj(t));
+          dmma(acc[t][0], acc[t][1], -Z[sw(gr, kk + tg)], R[sw(gr, kk + tg)]);
+        }
+      }
+    }
     V3T(4);
     if (look) {
       __syncwarp();
