@@ -10,8 +10,10 @@
 //             out_B = W y_S + (child updates passing through)
 //   backward  s = y_S - W^T x_B,  x_S = Linv^T s
 // Child contributions are gathered through precomputed source indices in a
-// fixed order (deterministic, no atomics); every GEMV is warp-per-row over
-// contiguous rows (coalesced).
+// fixed order (deterministic, no atomics).  Every GEMV is warp-per-row over
+// contiguous rows (coalesced), RPW rows per warp walked together so that
+// several independent loads per lane are in flight (one row at a time
+// serialises a memory latency plus a shuffle tree per row: ~20 us levels).
 //
 // node table (int64 x 10): s0, ns, nb, off_Linv, off_LinvT, off_W, off_WT, off_out, off_B, 0
 #include "common.cuh"
@@ -24,10 +26,69 @@ struct NodeRec {
   int64_t s0, ns, nb, oL, oLT, oW, oWT, oo, ob, pad;
 };
 
+// start of row j of a packed-upper row-major n x n matrix, minus j (so that
+// element (j, c), c >= j, sits at upk_row(j, n) + c)
+__device__ __forceinline__ int64_t upk_row(int j, int n) {
+  return (int64_t)j * n - (int64_t)j * (j - 1) / 2 - j;
+}
+
 __device__ __forceinline__ double warp_sum(double v) {
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
   return v;
+}
+
+// Warp-cooperative GEMV rows: for r in [0, nrows), v_r = sum_{j in [lo, hi)}
+// row_r[j] x[j] with (row_r, lo, hi) = ROW(r); each warp takes RPW rows at a
+// time and walks them together 32 columns per step, so RPW coalesced loads
+// per lane are in flight instead of one; then EMIT(r, v_r) on lane 0.
+constexpr int RPW = 4;
+template <class ROW, class EMIT>
+__device__ __forceinline__ void warp_rows(int nrows, const double* __restrict__ x, ROW row,
+                                          EMIT emit) {
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  constexpr int NW = MF_THREADS / 32;
+  for (int r0 = warp * RPW; r0 < nrows; r0 += NW * RPW) {
+    const double* p[RPW];
+    int lo[RPW], hi[RPW];
+    int jmin = 1 << 30, jmax = 0;
+#pragma unroll
+    for (int u = 0; u < RPW; ++u) {
+      lo[u] = 0;
+      hi[u] = 0;
+      p[u] = x;
+      if (r0 + u < nrows) row(r0 + u, p[u], lo[u], hi[u]);
+      jmin = min(jmin, lo[u]);
+      jmax = max(jmax, hi[u]);
+    }
+    double acc[RPW];
+#pragma unroll
+    for (int u = 0; u < RPW; ++u) acc[u] = 0.0;
+    // JU column steps per batch, all RPW x JU loads issued before the first FMA
+    // (issue is in order: a consumer waiting on a load blocks the next loads)
+    constexpr int JU = 4;
+    for (int j0 = jmin + lane; j0 < jmax; j0 += 32 * JU) {
+      double v[RPW][JU], xv[JU];
+#pragma unroll
+      for (int c = 0; c < JU; ++c) {
+        const int j = j0 + 32 * c;
+        xv[c] = j < jmax ? x[j] : 0.0;
+#pragma unroll
+        for (int u = 0; u < RPW; ++u) v[u][c] = (j >= lo[u] && j < hi[u]) ? __ldg(p[u] + j) : 0.0;
+      }
+#pragma unroll
+      for (int c = 0; c < JU; ++c)
+#pragma unroll
+        for (int u = 0; u < RPW; ++u) acc[u] = fma(v[u][c], xv[c], acc[u]);
+    }
+#pragma unroll
+    for (int u = 0; u < RPW; ++u) acc[u] = warp_sum(acc[u]);
+    if (lane == 0) {
+#pragma unroll
+      for (int u = 0; u < RPW; ++u)
+        if (r0 + u < nrows) emit(r0 + u, acc[u]);
+    }
+  }
 }
 
 // shared layout per node: [t or s : ns][ys : ns][pass or xb : nb]
@@ -43,7 +104,6 @@ __global__ void __launch_bounds__(MF_THREADS)
   double* t = sm;
   double* ys = sm + max_ns;
   double* pass = sm + 2 * max_ns;
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   // all gathers up front, in parallel: own right-hand side and the child
   // updates that pass through to the boundary
   for (int j = threadIdx.x; j < ns + nb; j += MF_THREADS) {
@@ -64,26 +124,29 @@ __global__ void __launch_bounds__(MF_THREADS)
     }
   }
   __syncthreads();
+  // y_S = Linv t (packed lower, row-major), then out_B = W y_S + pass
   const double* L = mats + nd.oL;
-  for (int r = warp; r < ns; r += MF_THREADS / 32) {
-    const double* row = L + (int64_t)r * (r + 1) / 2;
-    double s = 0.0;
-    for (int j = lane; j <= r; j += 32) s = fma(__ldg(row + j), t[j], s);
-    s = warp_sum(s);
-    if (lane == 0) {
-      y[nd.s0 + r] = s;
-      ys[r] = s;
-    }
-  }
+  warp_rows(
+      ns, t,
+      [&](int r, const double*& p, int& lo, int& hi) {
+        p = L + (int64_t)r * (r + 1) / 2;
+        lo = 0;
+        hi = r + 1;
+      },
+      [&](int r, double v) {
+        y[nd.s0 + r] = v;
+        ys[r] = v;
+      });
   __syncthreads();
   const double* W = mats + nd.oW;
-  for (int r = warp; r < nb; r += MF_THREADS / 32) {
-    const double* row = W + (int64_t)r * ns;
-    double s = 0.0;
-    for (int j = lane; j < ns; j += 32) s = fma(__ldg(row + j), ys[j], s);
-    s = warp_sum(s);
-    if (lane == 0) out[nd.oo + r] = s + pass[r];
-  }
+  warp_rows(
+      nb, ys,
+      [&](int r, const double*& p, int& lo, int& hi) {
+        p = W + (int64_t)r * ns;
+        lo = 0;
+        hi = ns;
+      },
+      [&](int r, double v) { out[nd.oo + r] = v + pass[r]; });
 }
 
 __global__ void __launch_bounds__(MF_THREADS)
@@ -96,30 +159,32 @@ __global__ void __launch_bounds__(MF_THREADS)
   const int ns = (int)nd.ns, nb = (int)nd.nb;
   double* s = sm;
   double* xb = sm + 2 * max_ns;
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int* Bp = B + nd.ob;
   for (int j = threadIdx.x; j < nb; j += MF_THREADS) xb[j] = xp[__ldg(Bp + j)];
   __syncthreads();
+  // s = y_S - W^T x_B (W^T row-major ns x nb), then x_S = Linv^T s (packed upper)
   const double* WT = mats + nd.oWT;
-  for (int r = warp; r < ns; r += MF_THREADS / 32) {
-    const double* row = WT + (int64_t)r * nb;
-    double a = 0.0;
-    for (int j = lane; j < nb; j += 32) a = fma(__ldg(row + j), xb[j], a);
-    a = warp_sum(a);
-    if (lane == 0) s[r] = __ldg(y + nd.s0 + r) - a;
-  }
+  warp_rows(
+      ns, xb,
+      [&](int r, const double*& p, int& lo, int& hi) {
+        p = WT + (int64_t)r * nb;
+        lo = 0;
+        hi = nb;
+      },
+      [&](int r, double v) { s[r] = __ldg(y + nd.s0 + r) - v; });
   __syncthreads();
-  const double* LT = mats + nd.oLT;     // packed upper, row r holds columns r..ns-1
-  for (int r = warp; r < ns; r += MF_THREADS / 32) {
-    const double* row = LT + (int64_t)r * ns - (int64_t)r * (r - 1) / 2 - r;
-    double a = 0.0;
-    for (int j = r + lane; j < ns; j += 32) a = fma(__ldg(row + j), s[j], a);
-    a = warp_sum(a);
-    if (lane == 0) {
-      xp[nd.s0 + r] = a;
-      x[perm[nd.s0 + r]] = a;
-    }
-  }
+  const double* LT = mats + nd.oLT;  // packed upper, row r holds columns r..ns-1
+  warp_rows(
+      ns, s,
+      [&](int r, const double*& p, int& lo, int& hi) {
+        p = LT + upk_row(r, ns);
+        lo = r;
+        hi = ns;
+      },
+      [&](int r, double v) {
+        xp[nd.s0 + r] = v;
+        x[perm[nd.s0 + r]] = v;
+      });
 }
 
 }  // namespace mcs
