@@ -165,8 +165,8 @@ def run_ours(args, rank, world):
     refs = refblocks.build_refs(fes)
     W_h = refblocks.element_weights(fes, prob.nu)
     W = engine.to_dev(W_h)
-    prog = [engine.to_dev(a) for a in engine.block_program(refs)]
-    L = engine.record_layout(k)
+    prog = [engine.to_dev(a) for a in engine.sblock_program(refs)]
+    L = engine.srecord_layout(k)
     rec = torch.empty((nt, L["len"]), dtype=torch.float64, device=dev)
     ST = torch.empty((nt, engine.st_stride(k)), dtype=torch.float64, device=dev)
     ext = torch.empty((nt, _abi.call("mcs_ext_stride", k)), dtype=torch.float64, device=dev)
@@ -176,13 +176,26 @@ def run_ours(args, rank, world):
     stream = torch.cuda.current_stream()
     st = _abi.stream(stream)
 
+    fused = k in engine.FUSED_DEGREES and not args.unfused
+    if fused:
+        tab, woff = (engine.to_dev(a) for a in engine.fused_tables(refs))
+
     def step(ev=None):
         if ev:
             ev[0].record(stream)
-        engine.element_records(nt, W, prog, k, out=rec, stream=stream)
+        if fused:   # A1 + A3 + A4 in one warp-per-element kernel
+            _abi.call("mcs_condense_fused", k, nt, _abi.ptr(W), W.shape[1], _abi.ptr(tab),
+                      _abi.ptr(woff), _abi.ptr(ST), _abi.ptr(ext), _abi.ptr(Sd),
+                      _abi.ptr(info), st)
+            if ev:
+                ev[1].record(stream)
+                ev[2].record(stream)
+                ev[3].record(stream)
+            return
+        engine.element_srecords(nt, W, prog, k, out=rec, stream=stream)
         if ev:
             ev[1].record(stream)
-        _abi.call("mcs_condense", k, nt, _abi.ptr(rec), _abi.ptr(ST), _abi.ptr(info), st)
+        _abi.call("mcs_condense_struct", k, nt, _abi.ptr(rec), _abi.ptr(ST), _abi.ptr(info), st)
         if ev:
             ev[2].record(stream)
         _abi.call("mcs_double_schur", k, nt, _abi.ptr(ST), _abi.ptr(ext), _abi.ptr(Sd),
@@ -316,7 +329,7 @@ def run_ours(args, rank, world):
         "e2e": {"value": world * nt / (e2e_ms * 1e-3), "unit": "elements/s",
                 "h2d_bytes_per_step": W_h.nbytes, "d2h_bytes_per_step": out_bytes,
                 "ms_per_step": e2e_ms},
-        "gpu_launches": 3 * args.steps,
+        "gpu_launches": (1 if fused else 3) * args.steps,
         "clocks": clk,
     }
     if micro:
@@ -476,6 +489,8 @@ def main():
     ap.add_argument("--cfg", type=int, default=2, choices=[1, 2, 3],
                     help="BASELINE config of the bench workload (default 2 = configs[1])")
     ap.add_argument("--no-micro", dest="micro", action="store_false")
+    ap.add_argument("--unfused", action="store_true",
+                    help="k <= 4: time the three-kernel path instead of the fused kernel")
     ap.add_argument("--micro-count", type=int, default=1 << 20)
     ap.add_argument("--cpu-sample", type=int, default=3072)
     ap.add_argument("--ref-sample-per-core", type=int, default=32)

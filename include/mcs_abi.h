@@ -43,6 +43,26 @@ int mcs_sd_stride(int k);
 int mcs_condense(int k, int64_t nt, const double* records, double* S_packed, int* info,
                  void* stream);
 
+/* ---- structured sigma/omega condensation (same result as mcs_condense,
+ *      exploiting the block structure of the MCS element spaces, DESIGN.md
+ *      §3.2): S_T = adiv + Y Y^T, Y = [B_m F_m | B_b L_b^-T].  srecords:
+ *      [nt][mcs_srec_len(k)] = [s | A_m 3x3 blocks | Mb | Bsig | adiv]. */
+int mcs_srec_len(int k);
+int mcs_condense_struct(int k, int64_t nt, const double* srecords, double* S_packed, int* info,
+                        void* stream);
+
+/* ---- fused element pipeline for k <= 4 (replaces assembly.py:49-91 +
+ *      condensation.py:159-177 + condensation.py:207-226 per element): one
+ *      warp per element generates Bsig from the reference-cell tables and the
+ *      element's geometry weights W [nt][nwgt >= 30], forms S_T = adiv + Y Y^T
+ *      and the double Schur outputs (ext, Sd_packed as mcs_double_schur).
+ *      tables: [mcs_fused_table_len(k)]; row_woff: [ceil8(nloc)] weight slot of
+ *      each Bsig row.  info bit 0: singular stress block, bit 1: S_oo not SPD. */
+int mcs_fused_table_len(int k);
+int mcs_condense_fused(int k, int64_t nt, const double* W, int nwgt, const double* tables,
+                       const int* row_woff, double* S_packed, double* ext, double* Sd_packed,
+                       int* info, void* stream);
+
 /* ---- double Schur (replaces condensation.py:207-226 double_schur per
  *      element): ext = [X = S_oo^-1 S_oc (n_int x ncpl) | S_oo^-1 packed],
  *      Sd_packed = S_cc - S_co X. */

@@ -25,6 +25,12 @@ SIGNATURES = {
     "mcs_st_stride": [_i],
     "mcs_condense": [_i, _l, _p, _p, _p, _p],
     "mcs_element_blocks": [_l, _i, _p, _i, _p, _p, _p, _p, _p],
+    # condense_struct.cu
+    "mcs_srec_len": [_i],
+    "mcs_condense_struct": [_i, _l, _p, _p, _p, _p],
+    # condense_fused.cu
+    "mcs_fused_table_len": [_i],
+    "mcs_condense_fused": [_i, _l, _p, _i, _p, _p, _p, _p, _p, _p, _p],
     # double_schur.cu
     "mcs_ext_stride": [_i],
     "mcs_sd_stride": [_i],

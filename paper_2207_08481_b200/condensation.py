@@ -61,6 +61,9 @@ class CondensedSystem:
         self.vv_of_cpl = None
         self._S = self._Sd = self._B = None
         self._dev_maps = None
+        # double Schur outputs produced together with S_T by the fused
+        # kernel (k <= 4); double_schur() publishes them
+        self._pending_ds = None
 
     # -------------------------------------------------------------- indexing
     @property
@@ -162,20 +165,31 @@ class CondensedSystem:
     def s_energy(self, x_full):
         return float(x_full @ (self.S @ x_full))
 
-    def check_info(self, info, what):
-        bad = np.flatnonzero(info.cpu().numpy())
+    def check_info(self, info, what, mask=None):
+        v = info.cpu().numpy()
+        bad = np.flatnonzero(v if mask is None else (v & mask))
         if len(bad):
             raise RuntimeError(f"{what} on element {int(bad[0])}")
 
 
 _PROGRAMS = {}
+_FUSED = {}
+
+
+def _fused_tables(k, refs):
+    """Reference-cell tables of the fused kernel on the device (per k)."""
+    if k not in _FUSED:
+        tab, woff = engine.fused_tables(refs)
+        _FUSED[k] = (engine.to_dev(tab), engine.to_dev(woff))
+    return _FUSED[k]
+STRUCT_TOL = 1e-10
 
 
 def _device_program(k, refs):
-    """Block-generation program of degree k on the device (the reference
-    matrices depend on k only; built once per process)."""
+    """Compact-record generation program of degree k on the device (the
+    reference matrices depend on k only; built once per process)."""
     if k not in _PROGRAMS:
-        _PROGRAMS[k] = [engine.to_dev(a) for a in engine.block_program(refs)]
+        _PROGRAMS[k] = [engine.to_dev(a) for a in engine.sblock_program(refs)]
     return _PROGRAMS[k]
 
 
@@ -184,32 +198,49 @@ def condense_sigma_omega(fes, nu: float, body_force=None, blocks=None,
     """Eliminate (sigma, omega) element-wise on the GPU (reference
     `condensation.py:136-188`).  `blocks` (a list of ElementBlocks, as the
     reference accepts) is packed and uploaded; otherwise the blocks are
-    generated on the GPU from the element geometry (refblocks.py)."""
+    generated on the GPU from the element geometry (refblocks.py).
+
+    Element blocks of the MCS spaces have the block structure of DESIGN.md
+    §3.2 and go through the structured kernel (S_T = adiv + Y Y^T);
+    user-supplied blocks without that structure take the general dense
+    signed-Cholesky kernel.  Both are GPU paths."""
     torch = _torch()
     _abi.lib()
     k = fes.k
     refs = build_refs(fes)
     nt = fes.mesh.num_triangles
+    pending = None
     if blocks is not None:
         arr = lambda name: np.array([getattr(b, name) for b in blocks])
-        rec_h = engine.pack_records(k, arr("msig"), arr("bws"), arr("bus"),
-                                    arr("bhs"), arr("adiv"))
-        records = engine.to_dev(rec_h)
+        msig, bws = arr("msig"), arr("bws")
+        if engine.structure_error(msig, bws, k) <= STRUCT_TOL:
+            rec_h = engine.pack_srecords(k, msig, bws, arr("bus"), arr("bhs"), arr("adiv"))
+            S_dev, info = engine.condense_struct(k, engine.to_dev(rec_h), stream=stream)
+        else:
+            rec_h = engine.pack_records(k, msig, bws, arr("bus"), arr("bhs"), arr("adiv"))
+            S_dev, info = engine.condense(k, engine.to_dev(rec_h), stream=stream)
         loads = np.array([b.load for b in blocks])
+    elif k in engine.FUSED_DEGREES:
+        W = engine.to_dev(element_weights(fes, nu))
+        tab, woff = _fused_tables(k, refs)
+        S_dev, ext, Sd, info = engine.condense_fused(k, nt, W, tab, woff, stream=stream)
+        pending = (ext, Sd, info)
+        loads = load_vectors(fes, refs, body_force)
     else:
         W = engine.to_dev(element_weights(fes, nu))
         prog = _device_program(k, refs)
-        records = engine.element_records(nt, W, prog, k, stream=stream)
+        records = engine.element_srecords(nt, W, prog, k, stream=stream)
+        S_dev, info = engine.condense_struct(k, records, stream=stream)
+        del records                               # blocks are not kept
         loads = load_vectors(fes, refs, body_force)
-    S_dev, info = engine.condense(k, records, stream=stream)
     maps = element_maps(fes)
     load = np.zeros(fes.n_vv)
     nu_l = refs.bus_vol.shape[0]
     np.add.at(load, maps.vv_l2g[:, :nu_l].ravel(),
               (loads * maps.vv_signs[:, :nu_l]).ravel())
     sys_ = CondensedSystem(fes, nu, S_dev, load, maps, refs, None)
-    del records                                   # blocks are not kept (1.3 GB at cfg2)
-    sys_.check_info(info, "singular local stress block")
+    sys_.check_info(info, "singular local stress block", mask=1 if pending else None)
+    sys_._pending_ds = pending
     return sys_
 
 
@@ -219,6 +250,13 @@ def double_schur(sys_: CondensedSystem, stream=None) -> CondensedSystem:
     torch = _torch()
     k = sys_.k
     nt = sys_.S_dev.shape[0]
+    if sys_._pending_ds is not None:             # computed with S_T (fused kernel)
+        ext, Sd, info = sys_._pending_ds
+        sys_._pending_ds = None
+        sys_.ext_dev, sys_.Sd_dev = ext, Sd
+        sys_.vv_of_cpl, sys_.cpl_of_vv = sys_.maps.vv_of_cpl, sys_.maps.cpl_of_vv
+        sys_.check_info(info, "interior velocity block not SPD", mask=2)
+        return sys_
     ext = torch.empty((nt, _abi.call("mcs_ext_stride", k)), dtype=torch.float64, device="cuda")
     Sd = torch.empty((nt, _abi.call("mcs_sd_stride", k)), dtype=torch.float64, device="cuda")
     info = torch.empty(nt, dtype=torch.int32, device="cuda")

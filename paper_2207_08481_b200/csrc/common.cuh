@@ -38,6 +38,43 @@ inline int err_code(cudaError_t e) { return e == cudaSuccess ? 0 : -static_cast<
 // Return the pending launch error (if any) as a negative code.
 inline int launch_status() { return err_code(cudaGetLastError()); }
 
+// per-element outputs of the double Schur (condensation.py:207-226):
+//   ext record  [X (n_int x ncpl, row-major) | S_oo^-1 (lower packed)]  (even stride)
+//   Sd_T        lower packed (even stride)
+template <int K>
+struct ExtLayout {
+  using Z = Sizes<K>;
+  static constexpr int x_len = Z::n_int * Z::ncpl;
+  static constexpr int len = even(x_len + npk(Z::n_int));
+  static constexpr int sd_len = even(npk(Z::ncpl));
+  static constexpr int st_len = even(npk(Z::nloc));
+};
+
+// local index of coupling dof c (facet BDM dofs, then Vhat)
+template <int K>
+__device__ __forceinline__ int cpl_local(int c) {
+  using Z = Sizes<K>;
+  return c < Z::n_em ? c : c + Z::n_int;
+}
+
+// FP64 tensor-core MMA, m8n8k4: lane (g, t) supplies A[g][t], B[t][g] and
+// owns C[g][2t], C[g][2t+1]
+__device__ __forceinline__ void dmma884(double& c0, double& c1, double a, double b) {
+  asm("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+      : "+d"(c0), "+d"(c1)
+      : "d"(a), "d"(b));
+}
+
+// 1/sqrt(x) to full double precision: hardware approximation + 2 Newton steps
+__device__ __forceinline__ double rsqrt_nr(double x) {
+  double y;
+  asm("rsqrt.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(x));
+  double r = fma(-x * y, y, 1.0);
+  y = fma(0.5 * y, r, y);
+  r = fma(-x * y, y, 1.0);
+  return fma(0.5 * y, r, y);
+}
+
 // dof code: 2*index + (sign < 0), or -1 for a constrained dof (reads 0, no write)
 __device__ __forceinline__ double code_sign(int c) { return (c & 1) ? -1.0 : 1.0; }
 __device__ __forceinline__ int code_index(int c) { return c >> 1; }

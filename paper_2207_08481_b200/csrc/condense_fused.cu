@@ -1,0 +1,503 @@
+// Fused element pipeline for degrees k <= 4: geometry weights -> element
+// blocks -> sigma/omega condensation -> double Schur, ONE WARP PER ELEMENT
+// (SURVEY §8a rows A1 + A3 + A4, §8f-1).
+//
+// Algebra (csrc/condense_struct.cu): with the block
+// structure of the MCS element spaces
+//     S_T = adiv + Y Y^T,   Y = [B_m F_m (m < ml) | B_b L_b^-T],
+// B = Bsig = [bus; bhs] generated on the fly from the reference-cell tables
+// (refblocks.py; B[i] = base[i] + sum_a w[i][a] T_a[i], w = the element's
+// bus-edge / bhs weights of the edge row i belongs to), then the reference's
+// double_schur (condensation.py:207-226) on the element-local S_T:
+//     S_oo = L L^T, X = S_oo^-1 S_oc, Sd_T = S_cc - (L^-1 S_oc)^T (L^-1 S_oc),
+//     S_oo^-1 = L^-T L^-1.
+//
+// Why a warp per element: every step is a short dependency chain (12- and
+// 15-pivot Cholesky factorisations, triangular solves) that a CTA-wide
+// pipeline would serialise behind barriers.  A warp needs no barrier, and
+// 12 resident warps per SM keep 12 elements in flight.  Y lives in REGISTERS
+// in the DMMA operand layout: lane (g, t) holds rows 8I + g, columns
+// (8 kc + 2t, 8 kc + 2t + 1) of every 8x8 chunk, so S_T = Y Y^T (m8n8k4
+// FP64 MMA) takes A = Y_I and B = Y_J straight from the same lane's
+// registers (no shared-memory operand traffic).  Columns of Y are ordered
+// so that each 8-column chunk is uniform across lanes except one "mixed"
+// chunk: low blocks m = 4 kc + t (2 columns per lane), then the bubble
+// columns, produced by a DMMA of the bubble part of B with L_b^-T whose
+// accumulator layout IS the operand layout.
+#include "common.cuh"
+
+namespace mcs {
+
+// reference-cell tables of the fused kernel (doubles):
+//   G4 [NR][ns][4] = (base, T_0, T_1, T_2) per Bsig entry | Adiv [nu][nu] |
+//   MbRef [6][nb][nb] | ARef [6][ml][9]      (rows >= nloc zero; segments even)
+template <int K>
+struct FTab {
+  using Z = Sizes<K>;
+  static constexpr int ml = K * (K + 1) / 2, nl = 3 * ml, nb = 3 * K;
+  static constexpr int NR = (Z::nloc + 7) / 8 * 8;
+  static constexpr int o_G4 = 0;
+  static constexpr int o_adiv = o_G4 + 4 * NR * Z::ns;
+  static constexpr int o_Mb = o_adiv + even(Z::nu * Z::nu);
+  static constexpr int o_A = o_Mb + even(6 * nb * nb);
+  static constexpr int len = o_A + even(6 * 9 * ml);
+};
+
+namespace fz {
+
+constexpr int W_MSIG = 0, W_ADIV = 27, NWS = 36;   // weight slots (refblocks.py), 30.. = 0
+
+template <int K>
+struct Geo {
+  using Z = Sizes<K>;
+  using T = FTab<K>;
+  static constexpr int ml = T::ml, nb = T::nb, nl = T::nl, ns = Z::ns, nu = Z::nu;
+  static constexpr int nloc = Z::nloc, NI = Z::n_int, NC = Z::ncpl, NEM = Z::n_em;
+  static constexpr int r = ml % 4;                    // low blocks in the mixed chunk
+  static constexpr int NLF = ml / 4;                  // full low chunks
+  static constexpr int MIX = r > 0 ? 1 : 0;
+  static constexpr int NLOW = NLF + MIX;
+  static constexpr int BMIX = MIX ? 8 - 2 * r : 0;    // bubble columns in the mixed chunk
+  static constexpr int BREST = nb > BMIX ? nb - BMIX : 0;
+  static constexpr int NBP = (BREST + 7) / 8;         // pure bubble chunks
+  static constexpr int NBT = MIX + NBP;               // bubble DMMA n-tiles
+  static constexpr int NKC = NLF + MIX + NBP;         // 8-column chunks of Y
+  static constexpr int NKS = (nb + 3) / 4;            // k-steps of the bubble DMMA
+  static constexpr int NR = T::NR, NRB = NR / 8;
+  static constexpr int NIK = (NI + 3) / 4;            // k-steps of Sd = S_cc - W^T W
+  static constexpr int NCB = (NC + 7) / 8;            // Sd tile rows
+  static constexpr int WST = 36;                      // W row stride (== 4 mod 16: conflict-free)
+  static constexpr int st_len = ExtLayout<K>::st_len;
+  // per-warp shared memory (doubles)
+  static constexpr int o_w = 0;
+  static constexpr int o_F = NWS;                     // F_m, 6 per block
+  static constexpr int o_S = o_F + even(6 * ml);      // packed S_T
+  static constexpr int o_U = o_S + st_len;            // phase-dependent union
+  static constexpr int UA = 2 * nb * nb + even(nb);   // Ls | Li | 1/diag
+  static constexpr int UB = 8 * ns;                   // one 8-row tile of B
+  static constexpr int NIT = (NI + 7) / 8;            // 8-row tiles of L^-1 / X
+  static constexpr int LST = 20;                      // L^-1 row stride (== 4 mod 16)
+  static constexpr int NIR = 8 * NIT > 4 * NIK ? 8 * NIT : 4 * NIK;   // padded rows
+  static constexpr int o_Da = 0;                     // Loo, then S_oc, then W (in place)
+  static constexpr int o_LI = (NI * NI > NIR * WST ? NI * NI : NIR * WST);
+  static constexpr int o_Rd = o_LI + NIR * LST;
+  static constexpr int UD = o_Rd + even(NI);
+  static constexpr int UMAX = UA > UB ? (UA > UD ? UA : UD) : (UB > UD ? UB : UD);
+  static constexpr int PER_WARP = o_U + even(UMAX);
+  static_assert(nb <= 32 && ml <= 32 && NI <= 32 && NC <= 32, "lane-per-row factorisations");
+  static_assert(8 * NCB <= WST, "W columns");
+  static_assert(8 * NIT <= LST && 4 * NIK <= LST, "L^-1 columns");
+  // bubble column of DMMA n-tile bt, output column n (-1: none)
+  __host__ __device__ static constexpr int jmap(int bt, int n) {
+    if (MIX && bt == 0) return (n >= 2 * r && n - 2 * r < nb) ? n - 2 * r : -1;
+    const int j = BMIX + 8 * (bt - MIX) + n;
+    return j < nb ? j : -1;
+  }
+};
+
+// signed-free Cholesky of an n x n SPD matrix held one row per lane
+// (a[c] = row lane, c < n; lanes >= n carry a copy of row 0).  On return
+// l[c] = L[lane][c] (c <= lane significant) and rd[j] = 1 / L[j][j] (same on
+// every lane, written to rd_out by lane 0).  ok = false if a pivot is not
+// positive.
+template <int N>
+__device__ __forceinline__ bool chol_rows(double (&a)[N], double (&l)[N], double* rd_out) {
+  const int lane = threadIdx.x & 31;
+  bool ok = true;
+#pragma unroll
+  for (int j = 0; j < N; ++j) {
+    const double d = __shfl_sync(0xffffffffu, a[j], j);
+    ok &= d > 0.0;
+    const double r = rsqrt_nr(d);
+    if (lane == 0) rd_out[j] = r;
+    l[j] = a[j] * r;
+#pragma unroll
+    for (int c = j + 1; c < N; ++c) a[c] = fma(-l[j], __shfl_sync(0xffffffffu, l[j], c), a[c]);
+  }
+  return ok;
+}
+
+}  // namespace fz
+
+template <int K, int WPB, int MINB>
+__global__ void __launch_bounds__(32 * WPB, MINB)
+    condense_fused_kernel(const double* __restrict__ Wg, int nwgt, const double* __restrict__ tab,
+                          const int* __restrict__ woff, double* __restrict__ ST,
+                          double* __restrict__ ext, double* __restrict__ Sd,
+                          int* __restrict__ info, int64_t nt) {
+  using G = fz::Geo<K>;
+  using T = FTab<K>;
+  using L = ExtLayout<K>;
+  constexpr int ml = G::ml, nb = G::nb, nl = G::nl, ns = G::ns, nu = G::nu, nloc = G::nloc;
+  constexpr int NI = G::NI, NC = G::NC, NEM = G::NEM, NRB = G::NRB, NKC = G::NKC;
+  constexpr int WST = G::WST;
+  extern __shared__ __align__(16) double smem[];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, g = lane >> 2, t = lane & 3;
+  double* sw = smem + warp * G::PER_WARP;
+  double* wts = sw + G::o_w;
+  double* Fs = sw + G::o_F;
+  double* Spk = sw + G::o_S;
+  double* U = sw + G::o_U;
+
+  if (lane < fz::NWS - 30) wts[30 + lane] = 0.0;        // zero weight slots
+  if (lane == 0) Spk[G::st_len - 1] = 0.0;              // packed padding (never written)
+  const int64_t nw = static_cast<int64_t>(gridDim.x) * WPB;
+  int64_t e = static_cast<int64_t>(blockIdx.x) * WPB + warp;
+  const int nwl = nwgt < 30 ? nwgt : 30;
+  double wnext = (e < nt && lane < nwl) ? __ldg(Wg + e * nwgt + lane) : 0.0;
+
+#pragma unroll 1
+  for (; e < nt; e += nw) {
+    if (lane < nwl) wts[lane] = wnext;
+    if (e + nw < nt && lane < nwl) wnext = __ldg(Wg + (e + nw) * nwgt + lane);   // prefetch
+    __syncwarp();
+    int bad = 0;
+
+    // ---------------- A: bubble block factor and the 3x3 block factors
+    double* Ls = U;
+    double* Li = U + nb * nb;
+    double* Rd = U + 2 * nb * nb;
+    {
+      const int i = lane < nb ? lane : 0;
+      double a[nb], l[nb];
+#pragma unroll
+      for (int c = 0; c < nb; ++c) a[c] = 0.0;
+#pragma unroll
+      for (int r = 0; r < 6; ++r) {
+        const double w = wts[fz::W_MSIG + r];
+        const double* mr = tab + T::o_Mb + (r * nb + i) * nb;
+#pragma unroll
+        for (int c = 0; c < nb; ++c) a[c] = fma(w, __ldg(mr + c), a[c]);
+      }
+      if (!fz::chol_rows<nb>(a, l, Rd)) bad |= 1;
+      if (lane < nb) {
+#pragma unroll
+        for (int c = 0; c < nb; ++c) Ls[lane * nb + c] = l[c];
+      }
+    }
+    if (lane < ml) {
+      double A[9];
+#pragma unroll
+      for (int q = 0; q < 9; ++q) A[q] = 0.0;
+#pragma unroll
+      for (int r = 0; r < 6; ++r) {
+        const double w = wts[fz::W_MSIG + r];
+        const double* ar = tab + T::o_A + (r * ml + lane) * 9;
+#pragma unroll
+        for (int q = 0; q < 9; ++q) A[q] = fma(w, __ldg(ar + q), A[q]);
+      }
+      // s = detJ skew(T_a): the bws weights (refblocks.py W_BWS)
+      const double s0 = wts[6], s1 = wts[7], s2 = wts[8];
+      const double a00 = A[0], a10 = A[3], a11 = A[4], a20 = A[6], a21 = A[7], a22 = A[8];
+      const double d11p = a11 - (a10 * a10) / a00;
+      const bool okA = a00 > 0.0 && d11p > 0.0;
+      const double i00 = rsqrt_nr(a00), l00 = a00 * i00;
+      const double l10 = a10 * i00, l20 = a20 * i00;
+      const double d11 = a11 - l10 * l10;
+      const double i11 = rsqrt_nr(d11), l11 = d11 * i11;
+      const double l21 = (a21 - l20 * l10) * i11;
+      const double d22 = a22 - l20 * l20 - l21 * l21;
+      const double i22 = rsqrt_nr(d22);
+      if (!(okA && d22 > 0.0)) bad |= 1;
+      (void)l00;
+      (void)l11;
+      const double v0 = s0 * i00;
+      const double v1 = (s1 - l10 * v0) * i11;
+      const double v2 = (s2 - l20 * v0 - l21 * v1) * i22;
+      const double vn = rsqrt_nr(v0 * v0 + v1 * v1 + v2 * v2);
+      const double u0 = v0 * vn, u1 = v1 * vn, u2 = v2 * vn;
+      const double au0 = fabs(u0), au1 = fabs(u1), au2 = fabs(u2);
+      const int ax = (au0 <= au1 && au0 <= au2) ? 0 : (au1 <= au2 ? 1 : 2);
+      const double ua = ax == 0 ? u0 : (ax == 1 ? u1 : u2);
+      double q10 = -ua * u0, q11 = -ua * u1, q12 = -ua * u2;
+      if (ax == 0) q10 += 1.0;
+      else if (ax == 1) q11 += 1.0;
+      else q12 += 1.0;
+      const double qn = rsqrt_nr(q10 * q10 + q11 * q11 + q12 * q12);
+      q10 *= qn;
+      q11 *= qn;
+      q12 *= qn;
+      const double q20 = u1 * q12 - u2 * q11, q21 = u2 * q10 - u0 * q12, q22 = u0 * q11 - u1 * q10;
+      const double f20 = q12 * i22, f21 = q22 * i22;
+      const double f10 = (q11 - l21 * f20) * i11, f11 = (q21 - l21 * f21) * i11;
+      const double f00 = (q10 - l10 * f10 - l20 * f20) * i00;
+      const double f01 = (q20 - l10 * f11 - l20 * f21) * i00;
+      double* Fm = Fs + 6 * lane;
+      Fm[0] = f00;
+      Fm[1] = f01;
+      Fm[2] = f10;
+      Fm[3] = f11;
+      Fm[4] = f20;
+      Fm[5] = f21;
+    }
+    __syncwarp();
+    if (lane < nb) {   // column `lane` of L_b^-1 (forward substitution)
+      double x[nb];
+#pragma unroll
+      for (int j = 0; j < nb; ++j) {
+        double acc = (j == lane) ? 1.0 : 0.0;
+#pragma unroll
+        for (int q = 0; q < j; ++q) acc = fma(-Ls[j * nb + q], x[q], acc);
+        x[j] = acc * Rd[j];
+      }
+#pragma unroll
+      for (int j = 0; j < nb; ++j) Li[j * nb + lane] = x[j];
+    }
+    __syncwarp();
+    // B operands of the bubble DMMA: (L_b^-T)[q][j] = Li[j][q], q = 4 ks + t, j = jmap(bt, g)
+    double LiR[G::NBT][G::NKS];
+#pragma unroll
+    for (int bt = 0; bt < G::NBT; ++bt) {
+      const int j = G::jmap(bt, g);
+#pragma unroll
+      for (int ks = 0; ks < G::NKS; ++ks) {
+        const int q = 4 * ks + t;
+        LiR[bt][ks] = (j >= 0 && q < nb) ? Li[j * nb + q] : 0.0;
+      }
+    }
+    __syncwarp();
+
+    // ---------------- B: Y in registers, one 8-row tile of B at a time
+    double2 Yf[NRB][NKC];
+    double* Bt = U;
+#pragma unroll
+    for (int I = 0; I < NRB; ++I) {
+      for (int q = lane; q < 8 * ns; q += 32) {
+        const int wo = __ldg(woff + 8 * I + q / ns);
+        const double2* p = reinterpret_cast<const double2*>(tab + T::o_G4) + 2 * (8 * I * ns + q);
+        const double2 v01 = __ldg(p), v23 = __ldg(p + 1);
+        double v = fma(wts[wo], v01.y, v01.x);
+        v = fma(wts[wo + 1], v23.x, v);
+        v = fma(wts[wo + 2], v23.y, v);
+        Bt[q] = v;
+      }
+      __syncwarp();
+      const double* brow = Bt + g * ns;
+#pragma unroll
+      for (int kc = 0; kc < G::NLOW; ++kc) {
+        const int m = 4 * kc + t;
+        const int mm = m < ml ? m : ml - 1;
+        const double b0 = brow[3 * mm], b1 = brow[3 * mm + 1], b2 = brow[3 * mm + 2];
+        const double* Fm = Fs + 6 * mm;
+        double y0 = fma(b0, Fm[0], fma(b1, Fm[2], b2 * Fm[4]));
+        double y1 = fma(b0, Fm[1], fma(b1, Fm[3], b2 * Fm[5]));
+        if (m >= ml) y0 = y1 = 0.0;
+        Yf[I][kc] = make_double2(y0, y1);
+      }
+#pragma unroll
+      for (int kc = G::NLOW; kc < NKC; ++kc) Yf[I][kc] = make_double2(0.0, 0.0);
+#pragma unroll
+      for (int bt = 0; bt < G::NBT; ++bt) {
+        double c0 = 0.0, c1 = 0.0;
+#pragma unroll
+        for (int ks = 0; ks < G::NKS; ++ks) {
+          const int q = 4 * ks + t;
+          const double a = q < nb ? brow[nl + q] : 0.0;
+          dmma884(c0, c1, a, LiR[bt][ks]);
+        }
+        const int kc = G::NLF + bt;
+        Yf[I][kc].x += c0;
+        Yf[I][kc].y += c1;
+      }
+      __syncwarp();
+    }
+
+    // ---------------- C: S_T = adiv + Y Y^T (DMMA), packed into shared memory
+    const double wad = wts[fz::W_ADIV];
+#pragma unroll
+    for (int I = 0; I < NRB; ++I) {
+#pragma unroll
+      for (int J = 0; J <= I; ++J) {
+        double c0 = 0.0, c1 = 0.0;
+#pragma unroll
+        for (int kc = 0; kc < NKC; ++kc) {
+          dmma884(c0, c1, Yf[I][kc].x, Yf[J][kc].x);
+          dmma884(c0, c1, Yf[I][kc].y, Yf[J][kc].y);
+        }
+        const int i = 8 * I + g, j = 8 * J + 2 * t;
+        if (i < nu && j < nu) c0 = fma(wad, __ldg(tab + T::o_adiv + i * nu + j), c0);
+        if (i < nu && j + 1 < nu) c1 = fma(wad, __ldg(tab + T::o_adiv + i * nu + j + 1), c1);
+        if (i < nloc) {
+          if (j <= i) Spk[pk(i, j)] = c0;
+          if (j + 1 <= i) Spk[pk(i, j + 1)] = c1;
+        }
+        asm volatile("" ::: "memory");   // keep the epilogue loads tile by tile (registers)
+      }
+    }
+    __syncwarp();
+    {
+      const double2* src = reinterpret_cast<const double2*>(Spk);
+      double2* dst = reinterpret_cast<double2*>(ST + e * G::st_len);
+      for (int q = lane; q < G::st_len / 2; q += 32) dst[q] = src[q];
+    }
+
+    // ---------------- D: double Schur on the element-local S_T
+    //   S_oo = L L^T (lane-per-row Cholesky), L^-1 (lane-per-column forward
+    //   substitution), then four small GEMMs on the tensor cores:
+    //   W = L^-1 S_oc, X = L^-T W, S_oo^-1 = L^-T L^-1, Sd_T = S_cc - W^T W.
+    auto S = [&](int a, int b) { return a >= b ? Spk[pk(a, b)] : Spk[pk(b, a)]; };
+    constexpr int LST = G::LST, NIR = G::NIR;
+    double* Loo = U + G::o_Da;
+    double* Soc = U + G::o_Da;            // after L^-1 is formed
+    double* LIs = U + G::o_LI;
+    double* Wd = U + G::o_Da;             // W overwrites S_oc column block by column block
+    double* Rdo = U + G::o_Rd;
+    {
+      const int i = lane < NI ? lane : 0;
+      double a[NI], l[NI];
+#pragma unroll
+      for (int c = 0; c < NI; ++c) a[c] = S(NEM + i, NEM + c);
+      if (!fz::chol_rows<NI>(a, l, Rdo)) bad |= 2;
+      if (lane < NI) {
+#pragma unroll
+        for (int c = 0; c < NI; ++c) Loo[lane * NI + c] = l[c];
+      }
+    }
+    for (int q = lane; q < NIR * LST; q += 32) {   // zero padding of L^-1
+      const int j = q / LST, c = q % LST;
+      if (j >= NI || c >= NI) LIs[q] = 0.0;
+    }
+    __syncwarp();
+    if (lane < NI) {   // column `lane` of L^-1
+      double x[NI];
+#pragma unroll
+      for (int j = 0; j < NI; ++j) {
+        double acc = (j == lane) ? 1.0 : 0.0;
+#pragma unroll
+        for (int q = 0; q < j; ++q) acc = fma(-Loo[j * NI + q], x[q], acc);
+        x[j] = acc * Rdo[j];
+        LIs[j * LST + lane] = x[j];
+      }
+    }
+    __syncwarp();
+    for (int q = lane; q < NIR * WST; q += 32) {   // S_oc, zero padded (over Loo)
+      const int j = q / WST, c = q % WST;
+      Soc[q] = (j < NI && c < NC) ? S(NEM + j, cpl_local<K>(c)) : 0.0;
+    }
+    __syncwarp();
+    // W = L^-1 S_oc  (NIT x NCB tiles); a column block of W replaces the
+    // column block of S_oc it was computed from
+#pragma unroll
+    for (int J = 0; J < G::NCB; ++J) {
+      double c[G::NIT][2];
+#pragma unroll
+      for (int I = 0; I < G::NIT; ++I) {
+        c[I][0] = c[I][1] = 0.0;
+#pragma unroll
+        for (int ks = 0; ks < G::NIK; ++ks)
+          dmma884(c[I][0], c[I][1], LIs[(8 * I + g) * LST + 4 * ks + t],
+                  Soc[(4 * ks + t) * WST + 8 * J + g]);
+      }
+      __syncwarp();
+#pragma unroll
+      for (int I = 0; I < G::NIT; ++I)
+        if (8 * I + g < NIR)
+          *reinterpret_cast<double2*>(Wd + (8 * I + g) * WST + 8 * J + 2 * t) =
+              make_double2(c[I][0], c[I][1]);
+      __syncwarp();
+    }
+    __syncwarp();
+    double* xo = ext + e * L::len;
+    // X = L^-T W
+#pragma unroll
+    for (int I = 0; I < G::NIT; ++I) {
+#pragma unroll
+      for (int J = 0; J < G::NCB; ++J) {
+        double c0 = 0.0, c1 = 0.0;
+#pragma unroll
+        for (int ks = 0; ks < G::NIK; ++ks)
+          dmma884(c0, c1, LIs[(4 * ks + t) * LST + 8 * I + g], Wd[(4 * ks + t) * WST + 8 * J + g]);
+        const int i = 8 * I + g, c = 8 * J + 2 * t;
+        if (i < NI) {
+          if (c < NC) xo[i * NC + c] = c0;
+          if (c + 1 < NC) xo[i * NC + c + 1] = c1;
+        }
+      }
+    }
+    // S_oo^-1 = L^-T L^-1 (lower packed)
+#pragma unroll
+    for (int I = 0; I < G::NIT; ++I) {
+#pragma unroll
+      for (int J = 0; J <= I; ++J) {
+        double c0 = 0.0, c1 = 0.0;
+#pragma unroll
+        for (int ks = 0; ks < G::NIK; ++ks)
+          dmma884(c0, c1, LIs[(4 * ks + t) * LST + 8 * I + g], LIs[(4 * ks + t) * LST + 8 * J + g]);
+        const int i = 8 * I + g, j = 8 * J + 2 * t;
+        if (i < NI) {
+          if (j <= i) xo[L::x_len + pk(i, j)] = c0;
+          if (j + 1 <= i) xo[L::x_len + pk(i, j + 1)] = c1;
+        }
+      }
+    }
+    // Sd_T = S_cc - W^T W on the tensor cores (lower 8x8 tiles)
+    double* so = Sd + e * L::sd_len;
+#pragma unroll
+    for (int I = 0; I < G::NCB; ++I) {
+#pragma unroll
+      for (int J = 0; J <= I; ++J) {
+        double c0 = 0.0, c1 = 0.0;
+#pragma unroll
+        for (int ks = 0; ks < G::NIK; ++ks) {
+          const double* wr = Wd + (4 * ks + t) * WST;
+          dmma884(c0, c1, wr[8 * I + g], wr[8 * J + g]);
+        }
+        const int a = 8 * I + g, b = 8 * J + 2 * t;
+        if (a < NC) {
+          const int la = cpl_local<K>(a);
+          if (b <= a) so[pk(a, b)] = S(la, cpl_local<K>(b)) - c0;
+          if (b + 1 <= a) so[pk(a, b + 1)] = S(la, cpl_local<K>(b + 1)) - c1;
+        }
+      }
+    }
+    if (lane == 0 && info) info[e] = bad;
+    __syncwarp();
+  }
+}
+
+template <int K, int WPB, int MINB>
+static int launch_condense_fused(int64_t nt, const double* W, int nwgt, const double* tab,
+                                 const int* woff, double* ST, double* ext, double* Sd, int* info,
+                                 cudaStream_t st) {
+  using G = fz::Geo<K>;
+  auto kern = condense_fused_kernel<K, WPB, MINB>;
+  const size_t smem = static_cast<size_t>(WPB) * G::PER_WARP * sizeof(double);
+  cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  int per_sm = 0, dev = 0, nsm = 148;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, 32 * WPB, smem) != cudaSuccess ||
+      per_sm < 1)
+    per_sm = 1;
+  const int64_t want = (nt + WPB - 1) / WPB, cap = static_cast<int64_t>(per_sm) * nsm;
+  const int grid = static_cast<int>(want < cap ? want : cap);
+  kern<<<grid, 32 * WPB, smem, st>>>(W, nwgt, tab, woff, ST, ext, Sd, info, nt);
+  return launch_status();
+}
+
+}  // namespace mcs
+
+using namespace mcs;
+
+MCS_API int mcs_fused_table_len(int k) {
+  switch (k) {
+    case 2: return FTab<2>::len;
+    case 3: return FTab<3>::len;
+    case 4: return FTab<4>::len;
+  }
+  return -1;
+}
+
+MCS_API int mcs_condense_fused(int k, int64_t nt, const double* W, int nwgt, const double* tables,
+                               const int* row_woff, double* S_packed, double* ext,
+                               double* Sd_packed, int* info, void* stream) {
+  if (nt <= 0) return 0;
+  if (nwgt < 30) return -1000;
+  auto st = static_cast<cudaStream_t>(stream);
+  switch (k) {
+    case 2: return launch_condense_fused<2, 4, 4>(nt, W, nwgt, tables, row_woff, S_packed, ext, Sd_packed, info, st);
+    case 3: return launch_condense_fused<3, 4, 3>(nt, W, nwgt, tables, row_woff, S_packed, ext, Sd_packed, info, st);
+    case 4: return launch_condense_fused<4, 4, 3>(nt, W, nwgt, tables, row_woff, S_packed, ext, Sd_packed, info, st);
+  }
+  return -1000;
+}

@@ -16,22 +16,6 @@
 namespace mcs {
 
 template <int K>
-struct ExtLayout {
-  using Z = Sizes<K>;
-  static constexpr int x_len = Z::n_int * Z::ncpl;
-  static constexpr int len = even(x_len + npk(Z::n_int));
-  static constexpr int sd_len = even(npk(Z::ncpl));
-  static constexpr int st_len = even(npk(Z::nloc));
-};
-
-// local index of coupling dof c (facet BDM dofs, then Vhat)
-template <int K>
-__device__ __forceinline__ int cpl_local(int c) {
-  using Z = Sizes<K>;
-  return c < Z::n_em ? c : c + Z::n_int;
-}
-
-template <int K>
 __device__ __forceinline__ double sym_at(const double* P, int a, int b) {
   return a >= b ? P[pk(a, b)] : P[pk(b, a)];
 }

@@ -44,6 +44,7 @@ def test_binding_matches_header():
 def test_layout_queries(k):
     lib = ctypes.CDLL(_abi.LIB_PATH)
     assert lib.mcs_record_len(k) == engine.record_layout(k)["len"]
+    assert lib.mcs_srec_len(k) == engine.srecord_layout(k)["len"]
     assert lib.mcs_st_stride(k) == engine.st_stride(k)
     z = local_sizes(k)
     ni, nc = z["n_int"], z["ncpl"]
