@@ -87,6 +87,23 @@ struct Geo {
   static_assert(nb <= 32 && ml <= 32 && NI <= 32 && NC <= 32, "lane-per-row factorisations");
   static_assert(8 * NCB <= WST, "W columns");
   static_assert(8 * NIT <= LST && 4 * NIK <= LST, "L^-1 columns");
+  // Bsig row i: 0 facet (bus volume + edge term of edge i/(k+1)), 1 interior
+  // bubble (volume only), 2 Vhat (bhs of edge (i-nu)/k), 3 padding
+  __host__ __device__ static constexpr int row_type(int i) {
+    return i < NEM ? 0 : (i < nu ? 1 : (i < nloc ? 2 : 3));
+  }
+  // weight slot of row i's three edge weights (refblocks.py W_BUSE / W_BHS)
+  __host__ __device__ static constexpr int row_woff(int i) {
+    return i < NEM ? 9 + 3 * (i / (K + 1)) : ((i >= nu && i < nloc) ? 18 + 3 * ((i - nu) / K) : 30);
+  }
+  // compact shared-memory copy of the Bsig tables: facet rows (base, T0, T1,
+  // T2) per entry, interior rows base only, Vhat rows (T0, T1, T2)
+  __host__ __device__ static constexpr int row_off(int i) {
+    return i < NEM ? 4 * ns * i
+                   : (i < nu ? 4 * ns * NEM + ns * (i - NEM)
+                             : 4 * ns * NEM + ns * (nu - NEM) + 3 * ns * (i - nu));
+  }
+  static constexpr int TAB_SMEM = even(4 * ns * NEM + ns * (nu - NEM) + 3 * ns * (nloc - nu));
   // bubble column of DMMA n-tile bt, output column n (-1: none)
   __host__ __device__ static constexpr int jmap(int bt, int n) {
     if (MIX && bt == 0) return (n >= 2 * r && n - 2 * r < nb) ? n - 2 * r : -1;
@@ -133,7 +150,26 @@ __global__ void __launch_bounds__(32 * WPB, MINB)
   constexpr int WST = G::WST;
   extern __shared__ __align__(16) double smem[];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, g = lane >> 2, t = lane & 3;
-  double* sw = smem + warp * G::PER_WARP;
+  double* stab = smem;                                   // compact Bsig tables (per CTA)
+  double* sw = smem + G::TAB_SMEM + warp * G::PER_WARP;
+  for (int q = threadIdx.x; q < nloc * ns; q += 32 * WPB) {
+    const int i = q / ns, c = q % ns, ty = G::row_type(i);
+    const double* src = tab + T::o_G4 + 4 * q;
+    double* dst = stab + G::row_off(i);
+    if (ty == 0) {
+      dst[4 * c] = src[0];
+      dst[4 * c + 1] = src[1];
+      dst[4 * c + 2] = src[2];
+      dst[4 * c + 3] = src[3];
+    } else if (ty == 1) {
+      dst[c] = src[0];
+    } else {
+      dst[3 * c] = src[1];
+      dst[3 * c + 1] = src[2];
+      dst[3 * c + 2] = src[3];
+    }
+  }
+  __syncthreads();
   double* wts = sw + G::o_w;
   double* Fs = sw + G::o_F;
   double* Spk = sw + G::o_S;
@@ -262,14 +298,34 @@ __global__ void __launch_bounds__(32 * WPB, MINB)
     double* Bt = U;
 #pragma unroll
     for (int I = 0; I < NRB; ++I) {
-      for (int q = lane; q < 8 * ns; q += 32) {
-        const int wo = __ldg(woff + 8 * I + q / ns);
-        const double2* p = reinterpret_cast<const double2*>(tab + T::o_G4) + 2 * (8 * I * ns + q);
-        const double2 v01 = __ldg(p), v23 = __ldg(p + 1);
-        double v = fma(wts[wo], v01.y, v01.x);
-        v = fma(wts[wo + 1], v23.x, v);
-        v = fma(wts[wo + 2], v23.y, v);
-        Bt[q] = v;
+      // rows of one type per instruction (compile-time after unrolling),
+      // lanes along the row: coalesced table reads, warp-uniform weights
+#pragma unroll
+      for (int rr = 0; rr < 8; ++rr) {
+        const int i = 8 * I + rr;
+        const int ty = G::row_type(i);
+        const int wo = G::row_woff(i);
+        const double w0 = wts[wo], w1 = wts[wo + 1], w2 = wts[wo + 2];
+        const double* p = stab + G::row_off(i);
+#pragma unroll
+        for (int c0 = 0; c0 < ns; c0 += 32) {
+          const int c = c0 + lane;
+          if (c0 + 32 <= ns || c < ns) {
+            double v = 0.0;
+            if (ty == 0) {            // facet row: base + edge term
+              const double2 v01 = *reinterpret_cast<const double2*>(p + 4 * c);
+              const double2 v23 = *reinterpret_cast<const double2*>(p + 4 * c + 2);
+              v = fma(w0, v01.y, v01.x);
+              v = fma(w1, v23.x, v);
+              v = fma(w2, v23.y, v);
+            } else if (ty == 1) {     // interior bubble row: J-invariant volume part
+              v = p[c];
+            } else if (ty == 2) {     // Vhat row: bhs of its edge
+              v = fma(w2, p[3 * c + 2], fma(w1, p[3 * c + 1], w0 * p[3 * c]));
+            }
+            Bt[rr * ns + c] = v;
+          }
+        }
       }
       __syncwarp();
       const double* brow = Bt + g * ns;
@@ -370,9 +426,16 @@ __global__ void __launch_bounds__(32 * WPB, MINB)
       }
     }
     __syncwarp();
-    for (int q = lane; q < NIR * WST; q += 32) {   // S_oc, zero padded (over Loo)
-      const int j = q / WST, c = q % WST;
-      Soc[q] = (j < NI && c < NC) ? S(NEM + j, cpl_local<K>(c)) : 0.0;
+    {   // S_oc (row j = interior dof NEM + j, column c = coupling dof), zero padded, over Loo
+      const int lc = cpl_local<K>(lane);
+#pragma unroll
+      for (int j = 0; j < NIR; ++j) {
+        const int a = NEM + j;
+        double v = 0.0;
+        if (j < NI && lane < NC) v = Spk[lc < a ? pk(a, lc) : pk(lc, a)];
+        Soc[j * WST + lane] = v;
+        if (lane < WST - 32) Soc[j * WST + 32 + lane] = 0.0;
+      }
     }
     __syncwarp();
     // W = L^-1 S_oc  (NIT x NCB tiles); a column block of W replaces the
@@ -461,7 +524,7 @@ static int launch_condense_fused(int64_t nt, const double* W, int nwgt, const do
                                  cudaStream_t st) {
   using G = fz::Geo<K>;
   auto kern = condense_fused_kernel<K, WPB, MINB>;
-  const size_t smem = static_cast<size_t>(WPB) * G::PER_WARP * sizeof(double);
+  const size_t smem = (G::TAB_SMEM + static_cast<size_t>(WPB) * G::PER_WARP) * sizeof(double);
   cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   int per_sm = 0, dev = 0, nsm = 148;
   cudaGetDevice(&dev);
@@ -495,9 +558,10 @@ MCS_API int mcs_condense_fused(int k, int64_t nt, const double* W, int nwgt, con
   if (nwgt < 30) return -1000;
   auto st = static_cast<cudaStream_t>(stream);
   switch (k) {
-    case 2: return launch_condense_fused<2, 4, 4>(nt, W, nwgt, tables, row_woff, S_packed, ext, Sd_packed, info, st);
-    case 3: return launch_condense_fused<3, 4, 3>(nt, W, nwgt, tables, row_woff, S_packed, ext, Sd_packed, info, st);
-    case 4: return launch_condense_fused<4, 4, 3>(nt, W, nwgt, tables, row_woff, S_packed, ext, Sd_packed, info, st);
+    // one CTA per SM: the compact tables once per CTA, one element per warp
+    case 2: return launch_condense_fused<2, 16, 1>(nt, W, nwgt, tables, row_woff, S_packed, ext, Sd_packed, info, st);
+    case 3: return launch_condense_fused<3, 12, 1>(nt, W, nwgt, tables, row_woff, S_packed, ext, Sd_packed, info, st);
+    case 4: return launch_condense_fused<4, 12, 1>(nt, W, nwgt, tables, row_woff, S_packed, ext, Sd_packed, info, st);
   }
   return -1000;
 }
