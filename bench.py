@@ -133,16 +133,39 @@ def load_peaks():
 
 def ncu_traffic(prefix):
     """DRAM bytes (read + write) per launch of the kernel whose name starts
-    with `prefix`, from the committed `ncu --set full` summary, if any."""
-    try:
-        with open(os.path.join(ROOT, "profiles", "ncu_kernels_r01.json")) as fh:
-            d = json.load(fh)
-    except OSError:
-        return None
-    for name, rec in d.items():
-        if name.startswith(prefix):
-            return rec.get("dram_bytes")
+    with `prefix`, from the newest committed `ncu --set full` summary
+    (profiles/ncu_kernels_*.json) that has it."""
+    import glob
+    for path in sorted(glob.glob(os.path.join(ROOT, "profiles", "ncu_kernels_*.json")),
+                       key=os.path.getmtime, reverse=True):
+        try:
+            with open(path) as fh:
+                d = json.load(fh)
+        except (OSError, ValueError):
+            continue
+        for name, rec in d.items():
+            if name.startswith(prefix):
+                return rec.get("dram_bytes")
     return None
+
+
+def flops_structured(k):
+    """FP64 flops per element of the structured path actually executed
+    (DESIGN.md §5): Bsig generation, block factors, Y, S_T = adiv + Y Y^T,
+    and the double Schur (Cholesky, L^-1, W = L^-1 S_oc, X = L^-T W,
+    S_oo^-1 = L^-T L^-1, Sd = S_cc - W^T W).  2 flops per FMA."""
+    ns = 3 * (k + 1) * (k + 2) // 2 - 3
+    nu, nh = (k + 1) * (k + 2), 3 * k
+    nl_, ni = nu + nh, (k + 1) * (k - 1)
+    nc, nem = nl_ - ni, 3 * (k + 1)
+    ml, nb = k * (k + 1) // 2, 3 * k
+    ny = 2 * ml + nb
+    gen = 2 * 3 * ns * (nem + nh)
+    fac = 2 * 6 * nb * nb + 2 * nb ** 3 / 3 + ml * (2 * 6 * 9 + 60)
+    y = nl_ * (2 * 6 * ml + nb * (nb + 1))
+    syrk = nl_ * (nl_ + 1) * ny + nu * (nu + 1)
+    ds = ni ** 3 + 2 * ni * ni * nc + nc * (nc + 1) * ni
+    return gen + fac + y + syrk + ds
 
 
 def run_ours(args, rank, world):
@@ -178,15 +201,14 @@ def run_ours(args, rank, world):
 
     fused = k in engine.FUSED_DEGREES and not args.unfused
     if fused:
-        tab, woff = (engine.to_dev(a) for a in engine.fused_tables(refs))
+        tab = engine.to_dev(engine.fused_tables(refs)[0])
 
     def step(ev=None):
         if ev:
             ev[0].record(stream)
         if fused:   # A1 + A3 + A4 in one warp-per-element kernel
             _abi.call("mcs_condense_fused", k, nt, _abi.ptr(W), W.shape[1], _abi.ptr(tab),
-                      _abi.ptr(woff), _abi.ptr(ST), _abi.ptr(ext), _abi.ptr(Sd),
-                      _abi.ptr(info), st)
+                      _abi.ptr(ST), _abi.ptr(ext), _abi.ptr(Sd), _abi.ptr(info), st)
             if ev:
                 ev[1].record(stream)
                 ev[2].record(stream)
@@ -272,7 +294,7 @@ def run_ours(args, rank, world):
                      "ms_per_iteration": float(np.median(solves)) / rep.iterations,
                      "precond_setup_s": round(t_sup, 3),
                      "jacobi_scale": M.inner.jacobi_scale,
-                     "reference_iterations": {"additive": 44}.get(comp)}
+                     "reference_iterations": ({"additive": 44} if args.cfg == 2 and not args.n else {}).get(comp)}
     clk = clocks.stop()
 
     # ---- e2e through the C ABI with host buffers: H2D weights, D2H results
@@ -302,7 +324,28 @@ def run_ours(args, rank, world):
 
     peaks = load_peaks()
     f_cond, f_ds = flops_per_element(k)
-    achieved = f_cond * nt / (t_a3.mean() * 1e-3) / 1e12
+    if fused:
+        # the fused kernel is the whole step: A1 + A3 + A4
+        f_kern = flops_structured(k)
+        t_kern = t_step.mean()
+        kname, kpref = f"condense_fused (A1+A3+A4), k={k}", f"condense_fused_kernel<{k},"
+    else:
+        t_kern = t_a3.mean()
+        kname, kpref = f"condense_struct (A3), k={k}", f"condense_struct_kernel<{k},"
+        z_ = refblocks.local_sizes(k)
+        ny_ = k * (k + 1) + 3 * k
+        f_kern = (z_["nloc"] * (z_["nloc"] + 1) * ny_ + z_["nloc"] * (12 * (k * (k + 1) // 2)
+                  + 3 * k * (3 * k + 1)))
+    achieved = f_kern * nt / (t_kern * 1e-3) / 1e12
+    roofline = {"bound": "fp64", "kernel": kname, "achieved": achieved,
+                "peak": peaks["fp64_tflops"], "unit": "TFLOP/s",
+                "frac": achieved / peaks["fp64_tflops"] if peaks["fp64_tflops"] else None,
+                "flops_per_element": f_kern,
+                "dense_equivalent_flops_per_element": f_cond + (f_ds if fused else 0),
+                "dense_equivalent_tflops": (f_cond + (f_ds if fused else 0)) * nt
+                / (t_kern * 1e-3) / 1e12,
+                "traffic": ncu_traffic(kpref),
+                "peak_source": "profiles/fp64_peak_r01.json (measured DMMA/DFMA max)"}
     out = {
         "metric": METRIC, "value": value, "unit": "elements/s", "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_per_step,
@@ -320,12 +363,7 @@ def run_ours(args, rank, world):
                            "frac": apply_bytes / (t_apply * 1e-3) / 1e9 / peaks["hbm_gbs"],
                            "traffic": ncu_traffic(f"elem_apply_kernel<{z['nloc']},")},
         "pcg": pcg,
-        "roofline": {"bound": "fp64", "kernel": f"condense (A3), k={k}",
-                     "achieved": achieved, "peak": peaks["fp64_tflops"], "unit": "TFLOP/s",
-                     "frac": achieved / peaks["fp64_tflops"] if peaks["fp64_tflops"] else None,
-                     "flops_per_element": f_cond,
-                     "traffic": ncu_traffic(f"condense_v3<{k},") or ncu_traffic(f"condense_kernel<{k},"),
-                     "peak_source": "profiles/fp64_peak_r01.json (measured DMMA/DFMA max)"},
+        "roofline": roofline,
         "e2e": {"value": world * nt / (e2e_ms * 1e-3), "unit": "elements/s",
                 "h2d_bytes_per_step": W_h.nbytes, "d2h_bytes_per_step": out_bytes,
                 "ms_per_step": e2e_ms},

@@ -56,12 +56,11 @@ int mcs_condense_struct(int k, int64_t nt, const double* srecords, double* S_pac
  *      warp per element generates Bsig from the reference-cell tables and the
  *      element's geometry weights W [nt][nwgt >= 30], forms S_T = adiv + Y Y^T
  *      and the double Schur outputs (ext, Sd_packed as mcs_double_schur).
- *      tables: [mcs_fused_table_len(k)]; row_woff: [ceil8(nloc)] weight slot of
- *      each Bsig row.  info bit 0: singular stress block, bit 1: S_oo not SPD. */
+ *      tables: [mcs_fused_table_len(k)] (engine.fused_tables).  info bit 0:
+ *      singular stress block, bit 1: S_oo not SPD. */
 int mcs_fused_table_len(int k);
 int mcs_condense_fused(int k, int64_t nt, const double* W, int nwgt, const double* tables,
-                       const int* row_woff, double* S_packed, double* ext, double* Sd_packed,
-                       int* info, void* stream);
+                       double* S_packed, double* ext, double* Sd_packed, int* info, void* stream);
 
 /* ---- double Schur (replaces condensation.py:207-226 double_schur per
  *      element): ext = [X = S_oo^-1 S_oc (n_int x ncpl) | S_oo^-1 packed],

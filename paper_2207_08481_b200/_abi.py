@@ -30,7 +30,7 @@ SIGNATURES = {
     "mcs_condense_struct": [_i, _l, _p, _p, _p, _p],
     # condense_fused.cu
     "mcs_fused_table_len": [_i],
-    "mcs_condense_fused": [_i, _l, _p, _i, _p, _p, _p, _p, _p, _p, _p],
+    "mcs_condense_fused": [_i, _l, _p, _i, _p, _p, _p, _p, _p, _p],
     # double_schur.cu
     "mcs_ext_stride": [_i],
     "mcs_sd_stride": [_i],

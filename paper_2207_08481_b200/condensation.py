@@ -179,8 +179,7 @@ _FUSED = {}
 def _fused_tables(k, refs):
     """Reference-cell tables of the fused kernel on the device (per k)."""
     if k not in _FUSED:
-        tab, woff = engine.fused_tables(refs)
-        _FUSED[k] = (engine.to_dev(tab), engine.to_dev(woff))
+        _FUSED[k] = engine.to_dev(engine.fused_tables(refs)[0])
     return _FUSED[k]
 STRUCT_TOL = 1e-10
 
@@ -222,8 +221,8 @@ def condense_sigma_omega(fes, nu: float, body_force=None, blocks=None,
         loads = np.array([b.load for b in blocks])
     elif k in engine.FUSED_DEGREES:
         W = engine.to_dev(element_weights(fes, nu))
-        tab, woff = _fused_tables(k, refs)
-        S_dev, ext, Sd, info = engine.condense_fused(k, nt, W, tab, woff, stream=stream)
+        S_dev, ext, Sd, info = engine.condense_fused(k, nt, W, _fused_tables(k, refs),
+                                                     stream=stream)
         pending = (ext, Sd, info)
         loads = load_vectors(fes, refs, body_force)
     else:

@@ -139,7 +139,7 @@ __device__ __forceinline__ bool chol_rows(double (&a)[N], double (&l)[N], double
 template <int K, int WPB, int MINB>
 __global__ void __launch_bounds__(32 * WPB, MINB)
     condense_fused_kernel(const double* __restrict__ Wg, int nwgt, const double* __restrict__ tab,
-                          const int* __restrict__ woff, double* __restrict__ ST,
+                          double* __restrict__ ST,
                           double* __restrict__ ext, double* __restrict__ Sd,
                           int* __restrict__ info, int64_t nt) {
   using G = fz::Geo<K>;
@@ -520,7 +520,7 @@ __global__ void __launch_bounds__(32 * WPB, MINB)
 
 template <int K, int WPB, int MINB>
 static int launch_condense_fused(int64_t nt, const double* W, int nwgt, const double* tab,
-                                 const int* woff, double* ST, double* ext, double* Sd, int* info,
+                                 double* ST, double* ext, double* Sd, int* info,
                                  cudaStream_t st) {
   using G = fz::Geo<K>;
   auto kern = condense_fused_kernel<K, WPB, MINB>;
@@ -534,7 +534,7 @@ static int launch_condense_fused(int64_t nt, const double* W, int nwgt, const do
     per_sm = 1;
   const int64_t want = (nt + WPB - 1) / WPB, cap = static_cast<int64_t>(per_sm) * nsm;
   const int grid = static_cast<int>(want < cap ? want : cap);
-  kern<<<grid, 32 * WPB, smem, st>>>(W, nwgt, tab, woff, ST, ext, Sd, info, nt);
+  kern<<<grid, 32 * WPB, smem, st>>>(W, nwgt, tab, ST, ext, Sd, info, nt);
   return launch_status();
 }
 
@@ -552,16 +552,16 @@ MCS_API int mcs_fused_table_len(int k) {
 }
 
 MCS_API int mcs_condense_fused(int k, int64_t nt, const double* W, int nwgt, const double* tables,
-                               const int* row_woff, double* S_packed, double* ext,
+                               double* S_packed, double* ext,
                                double* Sd_packed, int* info, void* stream) {
   if (nt <= 0) return 0;
   if (nwgt < 30) return -1000;
   auto st = static_cast<cudaStream_t>(stream);
   switch (k) {
     // one CTA per SM: the compact tables once per CTA, one element per warp
-    case 2: return launch_condense_fused<2, 16, 1>(nt, W, nwgt, tables, row_woff, S_packed, ext, Sd_packed, info, st);
-    case 3: return launch_condense_fused<3, 12, 1>(nt, W, nwgt, tables, row_woff, S_packed, ext, Sd_packed, info, st);
-    case 4: return launch_condense_fused<4, 12, 1>(nt, W, nwgt, tables, row_woff, S_packed, ext, Sd_packed, info, st);
+    case 2: return launch_condense_fused<2, 16, 1>(nt, W, nwgt, tables, S_packed, ext, Sd_packed, info, st);
+    case 3: return launch_condense_fused<3, 12, 1>(nt, W, nwgt, tables, S_packed, ext, Sd_packed, info, st);
+    case 4: return launch_condense_fused<4, 12, 1>(nt, W, nwgt, tables, S_packed, ext, Sd_packed, info, st);
   }
   return -1000;
 }

@@ -127,7 +127,8 @@ FUSED_ZERO_SLOT = 30          # weight slots 30..35 read as zero in the fused ke
 
 
 def fused_tables(refs: BlockRefs):
-    """(tables float64 [len], row_woff int32 [NR]) for the fused kernel.
+    """(tables float64 [len], row_woff int32 [NR]) for the fused kernel
+    (row_woff documents the weight slots; the kernel derives them from k).
 
     Bsig row i = base[i] + sum_a W[row_woff[i] + a] * T_a[i]: the volume part
     of bus (J-invariant) plus the edge term -<s_nn, u_n> of the edge the
@@ -168,7 +169,7 @@ def fused_tables(refs: BlockRefs):
 FUSED_DEGREES = (2, 3, 4)
 
 
-def condense_fused(k: int, nt: int, W_dev, tables_dev, woff_dev, ST=None, ext=None, Sd=None,
+def condense_fused(k: int, nt: int, W_dev, tables_dev, ST=None, ext=None, Sd=None,
                    info=None, stream=None):
     """Weights -> S_T, ext = [X | S_oo^-1], Sd_T in one warp-per-element
     kernel (csrc/condense_fused.cu).  info bit 0: singular stress block,
@@ -186,7 +187,7 @@ def condense_fused(k: int, nt: int, W_dev, tables_dev, woff_dev, ST=None, ext=No
     if info is None:
         info = torch.empty(nt, dtype=torch.int32, device=dev)
     _abi.call("mcs_condense_fused", k, nt, _abi.ptr(W_dev), W_dev.shape[1], _abi.ptr(tables_dev),
-              _abi.ptr(woff_dev), _abi.ptr(ST), _abi.ptr(ext), _abi.ptr(Sd), _abi.ptr(info),
+              _abi.ptr(ST), _abi.ptr(ext), _abi.ptr(Sd), _abi.ptr(info),
               _abi.stream(stream))
     return ST, ext, Sd, info
 

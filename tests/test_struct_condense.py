@@ -198,9 +198,9 @@ def test_gpu_fused_matches_oracle(cuda, cfg, n, k):
     fes = FeSystem(prob.mesh, prob.regions, k)
     refs = refblocks.build_refs(fes)
     W = engine.to_dev(refblocks.element_weights(fes, prob.nu))
-    tab, woff = engine.fused_tables(refs)
+    tab, _ = engine.fused_tables(refs)
     nt = fes.mesh.num_triangles
-    ST, ext, Sd, info = engine.condense_fused(k, nt, W, engine.to_dev(tab), engine.to_dev(woff))
+    ST, ext, Sd, info = engine.condense_fused(k, nt, W, engine.to_dev(tab))
     assert (info.cpu().numpy() == 0).all()
     z = refblocks.local_sizes(k)
     ni, nc = z["n_int"], z["ncpl"]
@@ -227,10 +227,9 @@ def test_gpu_fused_reports_failures(cuda):
     refs = refblocks.build_refs(fes)
     W = refblocks.element_weights(fes, prob.nu)
     W[1, refblocks.W_MSIG:refblocks.W_MSIG + 6] *= -1.0
-    tab, woff = engine.fused_tables(refs)
+    tab, _ = engine.fused_tables(refs)
     nt = fes.mesh.num_triangles
-    _, _, _, info = engine.condense_fused(prob.k, nt, engine.to_dev(W), engine.to_dev(tab),
-                                          engine.to_dev(woff))
+    _, _, _, info = engine.condense_fused(prob.k, nt, engine.to_dev(W), engine.to_dev(tab))
     info = info.cpu().numpy()
     assert info[1] & 1
     assert (np.delete(info, [1]) == 0).all()
