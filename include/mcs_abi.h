@@ -62,6 +62,19 @@ int mcs_fused_table_len(int k);
 int mcs_condense_fused(int k, int64_t nt, const double* W, int nwgt, const double* tables,
                        double* S_packed, double* ext, double* Sd_packed, int* info, void* stream);
 
+/* ---- stress recovery (replaces CondensedSystem.recover_stress,
+ *      condensation.py:64-74: (sigma, omega)_T = -M^-1 [Bsig^T; 0] u_T): one
+ *      warp per element regenerates Bsig from the weights W [nt][nwgt >= 30]
+ *      and the tables [mcs_recover_table_len(k)], solves with the block
+ *      structure of msig / bws.  vv_codes: [nt][nloc] codes over ALL (V, Vhat)
+ *      dofs (2*global + (sign < 0)); x_full: all (V, Vhat) dofs; sigma:
+ *      [nt][ns], omega: [nt][nw] (element-major, the reference numbering).
+ *      info[e] != 0: singular local stress block. */
+int mcs_recover_table_len(int k);
+int mcs_recover_stress(int k, int64_t nt, const double* W, int nwgt, const double* tables,
+                       const int* vv_codes, const double* x_full, double* sigma, double* omega,
+                       int* info, void* stream);
+
 /* ---- double Schur (replaces condensation.py:207-226 double_schur per
  *      element): ext = [X = S_oo^-1 S_oc (n_int x ncpl) | S_oo^-1 packed],
  *      Sd_packed = S_cc - S_co X. */

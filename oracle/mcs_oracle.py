@@ -120,6 +120,20 @@ def double_schur_element(S_T, k):
     return Soo, X, Sd
 
 
+def recover_stress(fes, R_list, x_full):
+    """Element-wise (sigma, omega) = -R_T u_T; follows `condensation.py:64-74`
+    (sigma / omega dofs are element-local, numbered element-major)."""
+    l2g, sg = vv_maps(fes)
+    ns, nw = R_list[0].shape[0] - fes.k * (fes.k + 1) // 2, fes.k * (fes.k + 1) // 2
+    sig = np.empty(len(R_list) * ns)
+    wv = np.empty(len(R_list) * nw)
+    for t, R in enumerate(R_list):
+        so = -R @ (x_full[l2g[t]] * sg[t])
+        sig[t * ns:(t + 1) * ns] = so[:ns]
+        wv[t * nw:(t + 1) * nw] = so[ns:]
+    return sig, wv
+
+
 def vv_maps(fes):
     """Per-element combined (V, Vhat) local->global map and signs;
     `condensation.py:147-153`."""

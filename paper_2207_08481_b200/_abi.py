@@ -28,6 +28,9 @@ SIGNATURES = {
     # condense_struct.cu
     "mcs_srec_len": [_i],
     "mcs_condense_struct": [_i, _l, _p, _p, _p, _p],
+    # recover.cu
+    "mcs_recover_table_len": [_i],
+    "mcs_recover_stress": [_i, _l, _p, _i, _p, _p, _p, _p, _p, _p, _p],
     # condense_fused.cu
     "mcs_fused_table_len": [_i],
     "mcs_condense_fused": [_i, _l, _p, _i, _p, _p, _p, _p, _p, _p],

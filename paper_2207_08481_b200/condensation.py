@@ -159,8 +159,31 @@ class CondensedSystem:
     @property
     def recovery(self):
         raise NotImplementedError(
-            "stress recovery (condensation.py:64-74) is SURVEY §8f row 3, not on "
-            "the GPU path yet")
+            "the per-element recovery matrices R_T are not stored on the GPU path "
+            "(572 MB at cfg2); recover_stress() regenerates them on the fly")
+
+    def recover_stress(self, x_full, stream=None):
+        """Element-wise (sigma, omega) from a velocity vector over all (V, Vhat)
+        dofs (reference `condensation.py:64-74`), on the GPU
+        (csrc/recover.cu).  NumPy in -> NumPy out; CUDA tensor in -> tensors."""
+        torch = _torch()
+        k, nt = self.k, self.fes.mesh.num_triangles
+        if k not in _RECOVERY:
+            _RECOVERY[k] = engine.to_dev(engine.recovery_tables(self.refs))
+        if getattr(self, "_rec_inputs", None) is None:
+            m = self.maps
+            codes = (2 * m.vv_l2g + (m.vv_signs < 0)).astype(np.int32)
+            self._rec_inputs = (engine.to_dev(element_weights(self.fes, self.nu)),
+                                engine.to_dev(np.ascontiguousarray(codes)))
+        W, codes = self._rec_inputs
+        on_host = not (hasattr(x_full, "is_cuda") and x_full.is_cuda)
+        x = torch.from_numpy(np.ascontiguousarray(x_full, dtype=np.float64)).cuda() \
+            if on_host else x_full.contiguous()
+        sig, om, info = engine.recover_stress(k, nt, W, _RECOVERY[k], codes, x, stream=stream)
+        self.check_info(info, "singular local stress block")
+        if on_host:
+            return sig.cpu().numpy(), om.cpu().numpy()
+        return sig, om
 
     def s_energy(self, x_full):
         return float(x_full @ (self.S @ x_full))
@@ -174,6 +197,7 @@ class CondensedSystem:
 
 _PROGRAMS = {}
 _FUSED = {}
+_RECOVERY = {}
 
 
 def _fused_tables(k, refs):

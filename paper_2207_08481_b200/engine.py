@@ -169,6 +169,40 @@ def fused_tables(refs: BlockRefs):
 FUSED_DEGREES = (2, 3, 4)
 
 
+def recovery_tables(refs: BlockRefs) -> np.ndarray:
+    """Tables of the stress-recovery kernel (csrc/recover.cu RTab): the fused
+    tables followed by Phi^-T (nw x ml), where bws = [Phi (x) s | 0]."""
+    k = refs.k
+    ml = k * (k + 1) // 2
+    Phi = refs.bws[0][:, 0:3 * ml:3]                  # (nw, ml)
+    PhiT = np.linalg.inv(Phi).T
+    tab = fused_tables(refs)[0]
+    out = np.zeros(len(tab) + _even(ml * ml))
+    out[:len(tab)] = tab
+    out[len(tab):len(tab) + ml * ml] = PhiT.ravel()
+    return out
+
+
+def recover_stress(k: int, nt: int, W_dev, tables_dev, codes_dev, x_dev, sig=None, om=None,
+                   info=None, stream=None):
+    """(sigma, omega) per element from a full velocity vector (csrc/recover.cu)."""
+    torch = _t()
+    if _abi.call("mcs_recover_table_len", k) != tables_dev.numel():
+        raise _abi.McsError("recovery table layout mismatch between Python and libmcsgpu")
+    z = local_sizes(k)
+    dev = W_dev.device
+    if sig is None:
+        sig = torch.empty(nt * z["ns"], dtype=torch.float64, device=dev)
+    if om is None:
+        om = torch.empty(nt * z["nw"], dtype=torch.float64, device=dev)
+    if info is None:
+        info = torch.empty(nt, dtype=torch.int32, device=dev)
+    _abi.call("mcs_recover_stress", k, nt, _abi.ptr(W_dev), W_dev.shape[1], _abi.ptr(tables_dev),
+              _abi.ptr(codes_dev), _abi.ptr(x_dev), _abi.ptr(sig), _abi.ptr(om), _abi.ptr(info),
+              _abi.stream(stream))
+    return sig, om, info
+
+
 def condense_fused(k: int, nt: int, W_dev, tables_dev, ST=None, ext=None, Sd=None,
                    info=None, stream=None):
     """Weights -> S_T, ext = [X | S_oo^-1], Sd_T in one warp-per-element
