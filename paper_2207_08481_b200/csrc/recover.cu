@@ -46,7 +46,7 @@ __global__ void __launch_bounds__(32 * RC_WARPS)
   using Z = Sizes<K>;
   using T = RTab<K>;
   constexpr int ns = Z::ns, nloc = Z::nloc, ml = T::ml, nl = T::nl, nb = T::nb, nw = Z::nw;
-  constexpr int PER = 36 + even(nloc) + even(ns) + 2 * nb * nb + even(nb) + 2 * even(ml);
+  constexpr int PER = 36 + even(nloc) + even(ns) + 2 * nb * nb + 2 * even(nb) + even(ml);
   extern __shared__ __align__(16) double smem[];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   double* w = smem + warp * PER;         // weights, slots 30.. = 0
@@ -56,7 +56,7 @@ __global__ void __launch_bounds__(32 * RC_WARPS)
   double* Li = Ls + nb * nb;             // L_b^-1
   double* Rd = Li + nb * nb;             // 1 / diag(L_b)
   double* dc = Rd + even(nb);            // d_m / c_m
-  double* yb = dc + even(ml);            // L_b^-1 f_b
+  double* yb = dc + even(ml);            // L_b^-1 f_b (nb)
   if (lane < 6) w[30 + lane] = 0.0;
   for (int64_t e = (int64_t)blockIdx.x * RC_WARPS + warp; e < nt;
        e += (int64_t)gridDim.x * RC_WARPS) {
@@ -206,8 +206,8 @@ static int launch_recover(int64_t nt, const double* W, int nwgt, const double* t
                           cudaStream_t st) {
   using Z = Sizes<K>;
   using T = RTab<K>;
-  constexpr int PER = 36 + even(Z::nloc) + even(Z::ns) + 2 * T::nb * T::nb + even(T::nb) +
-                      2 * even(T::ml);
+  constexpr int PER = 36 + even(Z::nloc) + even(Z::ns) + 2 * T::nb * T::nb + 2 * even(T::nb) +
+                      even(T::ml);
   const size_t smem = (size_t)RC_WARPS * PER * sizeof(double);
   auto kern = recover_kernel<K>;
   cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
