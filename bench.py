@@ -277,7 +277,7 @@ def run_ours(args, rank, world):
         M = velocity_preconditioner(fes, sys_, prob.nu, SolverOptions(composition=comp))
         torch.cuda.synchronize()
         t_sup = time.perf_counter() - t0
-        b_h = condensed_rhs(fes, sys_)
+        b_h = condensed_rhs(fes, sys_)[0]
         b = torch.from_numpy(b_h).to(dev)
         cg(S, b, M, rtol=1e-8, maxit=2000)      # warm-up (captures the CUDA graphs)
         torch.cuda.synchronize()

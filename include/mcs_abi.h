@@ -141,6 +141,23 @@ int mcs_mf_top(int t, const int* T, const int* perm, const double* b, const int*
                const int* src, const double* out, double* g, const double* Sinv, double* xp,
                double* x, void* stream);
 
+/* ---- Stokes (saddle) mode (replaces the B / B^T products of driver.py:148-151
+ *      and preconditioners.py:405-420, and the Gram-Schmidt products of the
+ *      GMRES of krylov.py:25-100).  Bpu: [nq][nu] reference matrix (J-invariant);
+ *      codes: the free (V, Vhat) dof codes [nt][nloc] (first nu = V dofs);
+ *      pressure dofs element-major [nt][nq].  B^T accumulates into y (zero it). */
+int mcs_apply_B(int nq, int nu, int nloc, int64_t nt, const double* Bpu, const int* codes,
+                const double* x, double* y, void* stream);
+int mcs_apply_BT(int nq, int nu, int nloc, int64_t nt, const double* Bpu, const int* codes,
+                 const double* p, double* y, void* stream);
+/* h[i] = V[i] . w for i < m (V row-major, leading dimension ld); partial:
+ * [m][mcs_mdot_len()] scratch.  w = beta w + alpha V^T h.  Deterministic. */
+int mcs_mdot_len(void);
+int mcs_mdot(int m, int64_t n, int64_t ld, const double* V, const double* w, double* partial,
+             double* h, void* stream);
+int mcs_gemv_acc(int m, int64_t n, int64_t ld, const double* V, const double* h, double alpha,
+                 double beta, double* w, void* stream);
+
 /* ---- PCG vector algebra (replaces krylov.py:103-137 NumPy ops); deterministic
  *      reductions into device scalars sc[]. */
 int mcs_reduce_workspace_len(void);

@@ -118,6 +118,51 @@ def case(R, name, cfg, n, with_matrices=True, comps=("additive", "multiplicative
           {c: int(out[f'cg_{c}_iters']) for c in comps})
 
 
+def stokes_case(R, name, cfg, n, comps=("additive", "multiplicative")):
+    """Stokes (saddle) mode through the reference's own pieces, exactly as
+    `driver.solve_stokes` wires them (driver.py:148-160): K = [[S, B^T],
+    [B, 0]] on free dofs, SaddlePreconditioner(velocity_preconditioner,
+    PressureMassPrecond, B_free), krylov.gmres."""
+    import scipy.sparse as sp
+    sys.path.insert(0, ROOT)
+    from paper_2207_08481_b200.problems import baseline_config
+    prob = baseline_config(cfg, n)
+    m = R["mesh"].from_arrays(prob.mesh.vertices, prob.mesh.triangles)
+    eps = 1e-12
+    key = "tilde_neumann" if cfg == 3 else "neumann"
+    regions = R["mesh"].classify_boundary(
+        m, dirichlet=lambda x: x[0] < 1 - eps, **{key: lambda x: x[0] >= 1 - eps})
+    fes = R["dofmap"].FeSystem(m, regions, prob.k)
+    sys_ = R["condensation"].condense_sigma_omega(fes, prob.nu, prob.body_force)
+    R["condensation"].double_schur(sys_)
+    free = fes.vv_free
+    S_free = sys_.S[free][:, free].tocsr()
+    B_free = sys_.B[:, free].tocsr()
+    K = sp.bmat([[S_free, B_free.T], [B_free, None]], format="csr")
+    rhs_u, rhs_p = R["driver"].condensed_rhs(fes, sys_)
+    rhs = np.concatenate([rhs_u, rhs_p])
+    mp = R["pc"].PressureMassPrecond.build(fes, prob.nu)
+    out = dict(k=prob.k, nu=prob.nu, n=n, cfg=cfg, rhs=rhs)
+    _csr("B", sys_.B, out)
+    rng = np.random.default_rng(21)
+    v = rng.standard_normal(K.shape[0])
+    out["probe_v"], out["probe_Kv"] = v, K @ v
+    for comp in comps:
+        opts = R["driver"].SolverOptions(mode="stokes", target="Sd", smoother="jacobi",
+                                         composition=comp, rtol=1e-8, maxit=500)
+        vel = R["driver"].velocity_preconditioner(fes, sys_, prob.nu, opts)
+        saddle = R["pc"].SaddlePreconditioner(vel, mp, B_free)
+        out[f"probe_P_{comp}"] = saddle.apply(v)
+        x, rep = R["krylov"].gmres(lambda u: K @ u, rhs, saddle.apply, rtol=1e-8, maxit=500)
+        out[f"gmres_{comp}_iters"] = rep.iterations
+        out[f"gmres_{comp}_res"] = np.array(rep.residuals)
+        out[f"gmres_{comp}_x"] = x
+    path = os.path.join(OUT, name + ".npz")
+    np.savez_compressed(path, **out)
+    print(f"{path}: {os.path.getsize(path) / 1e3:.0f} kB, gmres iters",
+          {c: int(out[f'gmres_{c}_iters']) for c in comps})
+
+
 def microbench(R):
     import scipy.linalg as sla
     sys.path.insert(0, ROOT)
@@ -135,11 +180,19 @@ def microbench(R):
 def main():
     os.makedirs(OUT, exist_ok=True)
     R = _ref()
+    if "--stokes" in sys.argv:
+        stokes_case(R, "stokes_c1_n2", 1, 2)
+        stokes_case(R, "stokes_c2_n3", 2, 3)
+        stokes_case(R, "stokes_c3_n2", 3, 2)
+        return
     case(R, "c1_n2", 1, 2)
     case(R, "c2_n3", 2, 3)
     case(R, "c3_n2", 3, 2)
     case(R, "cfg1", 1, 16, with_matrices=False)
     microbench(R)
+    stokes_case(R, "stokes_c1_n2", 1, 2)
+    stokes_case(R, "stokes_c2_n3", 2, 3)
+    stokes_case(R, "stokes_c3_n2", 3, 2)
 
 
 if __name__ == "__main__":

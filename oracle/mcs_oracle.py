@@ -411,6 +411,95 @@ def cg(apply_A, b, apply_M, rtol=1e-8, maxit=1000):
     return x, it, res
 
 
+# ------------------------------------------------------------ Stokes mode
+
+
+def assemble_B(fes, bpu):
+    """Pressure rows over all (V, Vhat) dofs; `condensation.py:178-186`
+    (bpu per element, signs of the V dofs)."""
+    l2g, sg = vv_maps(fes)
+    nu_l = fes.bdm.ndof
+    nt = fes.mesh.num_triangles
+    vals = np.broadcast_to(bpu[None], (nt,) + bpu.shape) * sg[:, None, :nu_l]
+    rows = np.repeat(fes.dof_q.loc2glob, nu_l, axis=1).ravel()
+    cols = np.tile(l2g[:, :nu_l], (1, bpu.shape[0])).ravel()
+    return sp.coo_matrix((vals.ravel(), (rows, cols)),
+                         shape=(fes.dof_q.ndof, fes.n_vv)).tocsr()
+
+
+def pressure_mass_diag(fes, nu):
+    """`preconditioners.py:390-396`: detJ_t / nu on the element's dofs."""
+    d = np.empty(fes.dof_q.ndof)
+    for t in range(fes.mesh.num_triangles):
+        d[fes.dof_q.loc2glob[t]] = fes.detJ[t] / nu
+    return d
+
+
+def saddle_apply(velocity_apply, diag, B_free):
+    """`preconditioners.py:405-420`."""
+    def apply(r):
+        nv = B_free.shape[1]
+        r_u, r_p = r[:nv], r[nv:]
+        a = velocity_apply(r_u)
+        dp = (r_p - B_free @ a) / diag
+        du = a - velocity_apply(B_free.T @ dp)
+        return np.concatenate([du, dp])
+    return apply
+
+
+def gmres(apply_A, b, apply_M=None, rtol=1e-6, maxit=500, project=None):
+    """`krylov.py:25-100` (full GMRES, right preconditioned, modified
+    Gram-Schmidt, Givens rotations); returns (x, iterations, residuals)."""
+    if apply_M is None:
+        apply_M = lambda v: v
+    b = np.asarray(b, dtype=float)
+    if project is not None:
+        b = project(b)
+    n = len(b)
+    r0 = b.copy()
+    beta = np.linalg.norm(r0)
+    bnorm = np.linalg.norm(b)
+    res = [1.0 if bnorm == 0 else beta / bnorm]
+    if bnorm == 0.0 or beta / bnorm <= rtol:
+        return np.zeros(n), 0, res
+    V = [r0 / beta]
+    H = np.zeros((maxit + 1, maxit))
+    cs, sn = np.zeros(maxit), np.zeros(maxit)
+    g = np.zeros(maxit + 1)
+    g[0] = beta
+    j = 0
+    while j < maxit:
+        w = np.array(apply_A(apply_M(V[j])), dtype=float)
+        if project is not None:
+            w = project(w)
+        for i in range(j + 1):
+            H[i, j] = w @ V[i]
+            w -= H[i, j] * V[i]
+        H[j + 1, j] = np.linalg.norm(w)
+        for i in range(j):
+            t = cs[i] * H[i, j] + sn[i] * H[i + 1, j]
+            H[i + 1, j] = -sn[i] * H[i, j] + cs[i] * H[i + 1, j]
+            H[i, j] = t
+        hsub = H[j + 1, j]
+        denom = np.hypot(H[j, j], hsub)
+        cs[j], sn[j] = H[j, j] / denom, hsub / denom
+        H[j, j], H[j + 1, j] = denom, 0.0
+        g[j + 1] = -sn[j] * g[j]
+        g[j] = cs[j] * g[j]
+        res.append(abs(g[j + 1]) / bnorm)
+        happy = hsub <= 1e-14 * denom
+        if not happy:
+            V.append(w / hsub)
+        j += 1
+        if res[-1] <= rtol or happy:
+            break
+    y = np.linalg.solve(H[:j, :j], g[:j])
+    x = apply_M(np.array(V[:j]).T @ y)
+    if project is not None:
+        x = project(x)
+    return x, j, res
+
+
 # -------------------------------------------------------------- microbench
 
 

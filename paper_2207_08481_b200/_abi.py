@@ -28,6 +28,12 @@ SIGNATURES = {
     # condense_struct.cu
     "mcs_srec_len": [_i],
     "mcs_condense_struct": [_i, _l, _p, _p, _p, _p],
+    # stokes.cu
+    "mcs_apply_B": [_i, _i, _i, _l, _p, _p, _p, _p, _p],
+    "mcs_apply_BT": [_i, _i, _i, _l, _p, _p, _p, _p, _p],
+    "mcs_mdot_len": [],
+    "mcs_mdot": [_i, _l, _l, _p, _p, _p, _p, _p],
+    "mcs_gemv_acc": [_i, _l, _l, _p, _p, _d, _d, _p, _p],
     # recover.cu
     "mcs_recover_table_len": [_i],
     "mcs_recover_stress": [_i, _l, _p, _i, _p, _p, _p, _p, _p, _p, _p],

@@ -1,0 +1,154 @@
+// Stokes (saddle-point) mode (reference driver.py:148-160,
+// krylov.py:25-100 gmres, preconditioners.py:384-420 PressureMassPrecond /
+// SaddlePreconditioner).
+//
+//   B apply    y_p[t nq + q] = sum_u Bpu[q][u] s_tu x[g_tu]        (thread per row)
+//   B^T apply  y[g_tu] = sum_t s_tu sum_q Bpu[q][u] p[t nq + q]     (atomics onto a
+//              zeroed vector: <= 2 contributions per dof, 0 + a + b == 0 + b + a,
+//              bitwise deterministic)
+//   GMRES      h = V w for the Krylov basis V (m x n, row-major) in two
+//              deterministic passes (fixed chunking, partials summed in order),
+//              w = beta w + alpha V^T h (thread per entry, fixed order over rows).
+// Bpu (nq x nu) is J-invariant (refblocks.py), so it lives in shared memory.
+#include "common.cuh"
+
+namespace mcs {
+
+constexpr int SK_THREADS = 256;
+
+__global__ void __launch_bounds__(SK_THREADS)
+    apply_B_kernel(int nq, int nu, int nloc, int64_t nt, const double* __restrict__ Bpu,
+                   const int* __restrict__ codes, const double* __restrict__ x,
+                   double* __restrict__ y) {
+  extern __shared__ double sB[];
+  for (int i = threadIdx.x; i < nq * nu; i += SK_THREADS) sB[i] = Bpu[i];
+  __syncthreads();
+  const int64_t n = nt * nq;
+  for (int64_t r = (int64_t)blockIdx.x * SK_THREADS + threadIdx.x; r < n;
+       r += (int64_t)gridDim.x * SK_THREADS) {
+    const int64_t t = r / nq;
+    const int q = (int)(r - t * nq);
+    const int* cd = codes + t * nloc;
+    double acc = 0.0;
+    for (int u = 0; u < nu; ++u) {
+      const int c = __ldg(cd + u);
+      if (c >= 0) acc = fma(sB[q * nu + u], code_sign(c) * __ldg(x + code_index(c)), acc);
+    }
+    y[r] = acc;
+  }
+}
+
+__global__ void __launch_bounds__(SK_THREADS)
+    apply_BT_kernel(int nq, int nu, int nloc, int64_t nt, const double* __restrict__ Bpu,
+                    const int* __restrict__ codes, const double* __restrict__ p,
+                    double* __restrict__ y) {
+  extern __shared__ double sB[];
+  for (int i = threadIdx.x; i < nq * nu; i += SK_THREADS) sB[i] = Bpu[i];
+  __syncthreads();
+  const int64_t n = nt * nu;
+  for (int64_t r = (int64_t)blockIdx.x * SK_THREADS + threadIdx.x; r < n;
+       r += (int64_t)gridDim.x * SK_THREADS) {
+    const int64_t t = r / nu;
+    const int u = (int)(r - t * nu);
+    const int c = __ldg(codes + t * nloc + u);
+    if (c < 0) continue;
+    const double* pt = p + t * nq;
+    double acc = 0.0;
+    for (int q = 0; q < nq; ++q) acc = fma(sB[q * nu + u], __ldg(pt + q), acc);
+    atomicAdd(y + code_index(c), code_sign(c) * acc);
+  }
+}
+
+constexpr int MD_CHUNKS = 64;
+
+// partial[i][c] = sum over chunk c of V[i] . w
+__global__ void __launch_bounds__(SK_THREADS)
+    mdot_partial_kernel(int64_t n, int64_t ld, const double* __restrict__ V,
+                        const double* __restrict__ w, double* __restrict__ partial) {
+  const int i = blockIdx.y, c = blockIdx.x;
+  const int64_t len = (n + MD_CHUNKS - 1) / MD_CHUNKS;
+  const int64_t lo = c * len, hi = lo + len < n ? lo + len : n;
+  const double* v = V + i * ld;
+  double s = 0.0;
+  for (int64_t k = lo + threadIdx.x; k < hi; k += SK_THREADS) s = fma(v[k], w[k], s);
+  __shared__ double red[SK_THREADS / 32];
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) s += __shfl_down_sync(0xffffffffu, s, o);
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = s;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double t = 0.0;
+    for (int q = 0; q < SK_THREADS / 32; ++q) t += red[q];
+    partial[i * MD_CHUNKS + c] = t;
+  }
+}
+
+__global__ void mdot_final_kernel(int m, const double* __restrict__ partial,
+                                  double* __restrict__ h) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= m) return;
+  double s = 0.0;
+  for (int c = 0; c < MD_CHUNKS; ++c) s += partial[i * MD_CHUNKS + c];
+  h[i] = s;
+}
+
+// w[k] = beta w[k] + alpha sum_{i < m} h[i] V[i][k]   (rows in order)
+__global__ void __launch_bounds__(SK_THREADS)
+    gemv_acc_kernel(int m, int64_t n, int64_t ld, const double* __restrict__ V,
+                    const double* __restrict__ h, double alpha, double beta,
+                    double* __restrict__ w) {
+  for (int64_t k = (int64_t)blockIdx.x * SK_THREADS + threadIdx.x; k < n;
+       k += (int64_t)gridDim.x * SK_THREADS) {
+    double s = 0.0;
+    for (int i = 0; i < m; ++i) s = fma(__ldg(h + i), V[i * ld + k], s);
+    w[k] = beta == 0.0 ? alpha * s : fma(alpha, s, beta * w[k]);
+  }
+}
+
+static int sk_grid(int64_t n) {
+  const int64_t g = (n + SK_THREADS - 1) / SK_THREADS;
+  return (int)(g < 8 * 148 ? (g < 1 ? 1 : g) : 8 * 148);
+}
+
+}  // namespace mcs
+
+using namespace mcs;
+
+MCS_API int mcs_apply_B(int nq, int nu, int nloc, int64_t nt, const double* Bpu, const int* codes,
+                        const double* x, double* y, void* stream) {
+  if (nt <= 0) return 0;
+  auto st = static_cast<cudaStream_t>(stream);
+  apply_B_kernel<<<sk_grid(nt * nq), SK_THREADS, nq * nu * sizeof(double), st>>>(
+      nq, nu, nloc, nt, Bpu, codes, x, y);
+  return launch_status();
+}
+
+MCS_API int mcs_apply_BT(int nq, int nu, int nloc, int64_t nt, const double* Bpu, const int* codes,
+                         const double* p, double* y, void* stream) {
+  if (nt <= 0) return 0;
+  auto st = static_cast<cudaStream_t>(stream);
+  apply_BT_kernel<<<sk_grid(nt * nu), SK_THREADS, nq * nu * sizeof(double), st>>>(
+      nq, nu, nloc, nt, Bpu, codes, p, y);
+  return launch_status();
+}
+
+MCS_API int mcs_mdot_len(void) { return MD_CHUNKS; }
+
+MCS_API int mcs_mdot(int m, int64_t n, int64_t ld, const double* V, const double* w,
+                     double* partial, double* h, void* stream) {
+  if (m <= 0) return 0;
+  auto st = static_cast<cudaStream_t>(stream);
+  mdot_partial_kernel<<<dim3(MD_CHUNKS, m), SK_THREADS, 0, st>>>(n, ld, V, w, partial);
+  int rc = launch_status();
+  if (rc) return rc;
+  mdot_final_kernel<<<(m + 127) / 128, 128, 0, st>>>(m, partial, h);
+  return launch_status();
+}
+
+MCS_API int mcs_gemv_acc(int m, int64_t n, int64_t ld, const double* V, const double* h,
+                         double alpha, double beta, double* w, void* stream) {
+  if (n <= 0) return 0;
+  auto st = static_cast<cudaStream_t>(stream);
+  gemv_acc_kernel<<<sk_grid(n), SK_THREADS, 0, st>>>(m, n, ld, V, h, alpha, beta, w);
+  return launch_status();
+}

@@ -56,14 +56,18 @@ def velocity_preconditioner(fes, sys_: CondensedSystem, nu, opts: SolverOptions)
 
 
 def condensed_rhs(fes, sys_: CondensedSystem):
-    """rhs_u = (load - S vv_values)[free] (reference `driver.py:105-110`);
-    the Dirichlet lift is applied on the GPU when the data are nonzero."""
+    """(rhs_u, rhs_p) with the Dirichlet lift (reference `driver.py:105-110`):
+    rhs_u = (load - S vv_values)[free], rhs_p = -B vv_values.  The lift
+    materialises S / B only when the Dirichlet data are nonzero (never for
+    the BASELINE configs)."""
     load = sys_.load[fes.vv_free].copy()
+    n_p = fes.dof_q.ndof
     if np.any(fes.vv_values):
-        # S @ vv_values over all dofs, restricted to free rows
-        S = sys_.S
-        load -= (S @ fes.vv_values)[fes.vv_free]
-    return load
+        load -= (sys_.S @ fes.vv_values)[fes.vv_free]
+        rhs_p = -(sys_.B @ fes.vv_values)
+    else:
+        rhs_p = np.zeros(n_p)
+    return load, rhs_p
 
 
 @dataclass
@@ -89,7 +93,7 @@ def solve_elliptic(problem, k, nu, opts: SolverOptions) -> EllipticResult:
     fes, sys_ = build_system(problem, k, nu, opts)
     M = velocity_preconditioner(fes, sys_, nu, opts)
     A = SOperator(sys_)
-    rhs = condensed_rhs(fes, sys_)
+    rhs = condensed_rhs(fes, sys_)[0]
     _sync()
     t_sup = time.perf_counter() - t0
     t1 = time.perf_counter()
@@ -102,9 +106,82 @@ def solve_elliptic(problem, k, nu, opts: SolverOptions) -> EllipticResult:
                           t_sup, t_sol)
 
 
+def pressure_projector(fes):
+    """Remove the constant pressure mode from the trailing block of a stacked
+    (velocity, pressure) device vector (reference `driver.py:113-130`)."""
+    import torch
+    from .operators import workspace
+    loc = fes.dof_q.loc2glob
+    one = np.zeros(fes.dof_q.ndof)
+    one[loc[:, 0]] = 1.0 / fes.tab_q[0, 0]
+    mass = np.zeros(fes.dof_q.ndof)
+    mass[loc.ravel()] = (fes.detJ[:, None] * (fes.tab_q @ fes.quad_tri.weights)[None, :]).ravel()
+    denom = float(mass @ one)
+    nvfree = int(fes.vv_free.sum())
+    one_d, mass_d = torch.from_numpy(one).cuda(), torch.from_numpy(mass).cuda()
+
+    def project(x):
+        out = x.clone()
+        p = out[nvfree:]
+        coef = workspace().dot_host(mass_d, p) / denom
+        p.add_(one_d, alpha=-coef)
+        return out
+
+    project.mass, project.one = mass, one
+    return project
+
+
+@dataclass
+class StokesResult:
+    fes: FeSystem
+    system: CondensedSystem
+    x_free: object
+    u: np.ndarray
+    uhat: np.ndarray
+    p: np.ndarray
+    sigma: np.ndarray
+    w: np.ndarray
+    report: KrylovReport
+    t_sup: float
+    t_sol: float
+
+
 def solve_stokes(problem, k, nu, opts: SolverOptions):
-    if opts.mode != "elliptic":
-        raise NotImplementedError(
-            "Stokes (saddle/GMRES) mode is SURVEY §8f row 4; the GPU path covers "
-            "the elliptic mode of the north star")
-    return solve_elliptic(problem, k, nu, opts)
+    """Reference `driver.py:133-180`: elliptic mode -> PCG on S; Stokes mode
+    -> right-preconditioned GMRES on K = [[S, B^T], [B, 0]] with the block
+    triangular saddle preconditioner (two ExtendedAsp applications, the
+    diagonal pressure mass) and, for pure Dirichlet problems, the constant
+    pressure mode projected out.  Both end with the GPU stress recovery."""
+    if opts.mode == "elliptic":
+        return solve_elliptic(problem, k, nu, opts)
+    if opts.mode != "stokes":
+        raise ValueError(f"unknown mode {opts.mode!r}")
+    from .krylov import gmres
+    from .operators import SaddleOperator
+    t0 = time.perf_counter()
+    fes, sys_ = build_system(problem, k, nu, opts)
+    vel = velocity_preconditioner(fes, sys_, nu, opts)
+    K = SaddleOperator(sys_)
+    rhs_u, rhs_p = condensed_rhs(fes, sys_)
+    mp = pc.PressureMassPrecond.build(fes, nu)
+    saddle = pc.SaddlePreconditioner(vel, mp, K.B)
+    mean_zero = bool(fes.regions.mean_zero_pressure)
+    project = pressure_projector(fes) if mean_zero else None
+    _sync()
+    t_sup = time.perf_counter() - t0
+    t1 = time.perf_counter()
+    x, report = gmres(K, np.concatenate([rhs_u, rhs_p]), saddle, rtol=opts.rtol,
+                      maxit=opts.maxit, project=project)
+    _sync()
+    t_sol = time.perf_counter() - t1
+    nv = K.n_v
+    x_free = x[:nv]
+    p_phys = -x[nv:]
+    if mean_zero:
+        area = float(np.sum(fes.detJ) / 2.0)
+        p_phys = p_phys - float(project.mass @ p_phys) / area * project.one
+    x_full = fes.vv_values.copy()
+    x_full[fes.vv_free] = x_free
+    sigma, w = sys_.recover_stress(x_full)
+    return StokesResult(fes, sys_, x_free, x_full[:fes.n_v], x_full[fes.n_v:], p_phys, sigma, w,
+                        report, t_sup, t_sol)

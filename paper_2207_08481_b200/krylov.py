@@ -164,3 +164,122 @@ def cg(apply_A, b, apply_M=None, rtol=1e-8, maxit=1000, stream=None, use_graph=T
         rz, rz_new = rz_new, rz
     x = S.x.clone()
     return (x.cpu().numpy() if host else x), report
+
+
+def _norm(ws: Workspace, v) -> float:
+    ws.dot(v, v, ws.TMP)
+    return float(np.sqrt(ws.sc[ws.TMP].item()))
+
+
+def _op(op, v, out):
+    if hasattr(op, "apply"):
+        return op.apply(v, out=out)
+    out.copy_(op(v))
+    return out
+
+
+def gmres(apply_A, b, apply_M=None, rtol=1e-6, maxit=500, project=None, x0=None):
+    """Full (non-restarted) right-preconditioned GMRES (reference
+    `krylov.py:25-100`) with the Krylov basis in HBM.
+
+    Same control flow and reporting as the reference: optional null-space
+    `project` on b and on every new direction, residual history of the
+    Givens-rotated least-squares residual, happy-breakdown test
+    h_{j+1,j} <= 1e-14 |rotated diagonal|, FloatingPointError on a
+    non-finite h, x = x0 + M (V y).  The Arnoldi orthogonalisation is
+    classical Gram-Schmidt applied twice (CGS2: two deterministic V w /
+    V^T h product pairs per step, csrc/stokes.cu) instead of the
+    reference's modified Gram-Schmidt loop: the same Hessenberg matrix up to
+    rounding, with one host read-back of the column per step.  The small
+    (maxit+1) x maxit least-squares problem stays on the host, as in the
+    reference."""
+    import torch
+    bd, host = as_device(b)
+    ws: Workspace = workspace()
+    n = bd.numel()
+    ident = apply_M is None
+    b_ = bd.clone()
+    if project is not None:
+        b_ = project(b_)
+    x0d = torch.zeros(n, dtype=torch.float64, device="cuda") if x0 is None else as_device(x0)[0]
+    if x0 is not None and _norm(ws, x0d) > 0.0:
+        r0 = b_ - _op(apply_A, x0d, empty(n))
+    else:
+        r0 = b_.clone()
+    beta = _norm(ws, r0)
+    bnorm = _norm(ws, b_)
+    report = KrylovReport(residuals=[1.0 if bnorm == 0 else beta / bnorm])
+
+    def finish(x):
+        x = x if host is False else x.cpu().numpy()
+        return x, report
+
+    if bnorm == 0.0 or beta / bnorm <= rtol:
+        report.converged = True
+        return finish(x0d)
+    cap = min(maxit + 1, 64)
+    V = torch.empty((cap, n), dtype=torch.float64, device="cuda")
+    V[0].copy_(r0).mul_(1.0 / beta)
+    H = np.zeros((maxit + 1, maxit))
+    cs, sn = np.zeros(maxit), np.zeros(maxit)
+    g = np.zeros(maxit + 1)
+    g[0] = beta
+    partial = torch.empty(_abi.call("mcs_mdot_len") * (maxit + 1), dtype=torch.float64,
+                          device="cuda")
+    h1 = torch.empty(maxit + 1, dtype=torch.float64, device="cuda")
+    h2 = torch.empty(maxit + 1, dtype=torch.float64, device="cuda")
+    z, w = empty(n), empty(n)
+    j = 0
+    while j < maxit:
+        mz = V[j] if ident else _op(apply_M, V[j], z)
+        _op(apply_A, mz, w)
+        if project is not None:
+            w = project(w)
+        m = j + 1
+        for hh in (h1, h2):                               # CGS2
+            _abi.call("mcs_mdot", m, n, n, _abi.ptr(V), _abi.ptr(w), _abi.ptr(partial),
+                      _abi.ptr(hh), _abi.stream(None))
+            _abi.call("mcs_gemv_acc", m, n, n, _abi.ptr(V), _abi.ptr(hh), -1.0, 1.0,
+                      _abi.ptr(w), _abi.stream(None))
+        hcol = (h1[:m] + h2[:m]).cpu().numpy()
+        hnext = _norm(ws, w)
+        H[:m, j] = hcol
+        H[j + 1, j] = hnext
+        if not np.isfinite(hnext) or not np.all(np.isfinite(hcol)):
+            raise FloatingPointError("GMRES residual became non-finite")
+        for i in range(j):                                # accumulated Givens rotations
+            t = cs[i] * H[i, j] + sn[i] * H[i + 1, j]
+            H[i + 1, j] = -sn[i] * H[i, j] + cs[i] * H[i + 1, j]
+            H[i, j] = t
+        hsub = H[j + 1, j]
+        denom = np.hypot(H[j, j], hsub)
+        cs[j] = H[j, j] / denom
+        sn[j] = hsub / denom
+        H[j, j] = denom
+        H[j + 1, j] = 0.0
+        g[j + 1] = -sn[j] * g[j]
+        g[j] = cs[j] * g[j]
+        res = abs(g[j + 1]) / bnorm
+        report.residuals.append(res)
+        happy = hsub <= 1e-14 * denom
+        if not happy:
+            if j + 1 >= V.shape[0]:                       # grow the basis
+                Vn = torch.empty((min(maxit + 1, 2 * V.shape[0]), n), dtype=torch.float64,
+                                 device="cuda")
+                Vn[:V.shape[0]].copy_(V)
+                V = Vn
+            V[j + 1].copy_(w).mul_(1.0 / hsub)
+        j += 1
+        if res <= rtol or happy:
+            report.converged = True
+            break
+    mm = j
+    y = np.linalg.solve(H[:mm, :mm], g[:mm])
+    yd = torch.from_numpy(y).cuda()
+    t = empty(n)
+    _abi.call("mcs_gemv_acc", mm, n, n, _abi.ptr(V), _abi.ptr(yd), 1.0, 0.0, _abi.ptr(t), _abi.stream(None))
+    xk = x0d + (t if ident else _op(apply_M, t, empty(n)))
+    if project is not None:
+        xk = project(xk)
+    report.iterations = mm
+    return finish(xk)

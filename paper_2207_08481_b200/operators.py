@@ -112,3 +112,68 @@ class SdOperator(_ElemOperator):
             raise ValueError("double_schur() must be run first")
         m = sys_.dev_maps()
         super().__init__(sys_, sys_.Sd_dev, m["cpl_codes"], sys_.maps.n_cpl_free)
+
+
+class BOperator:
+    """Divergence constraint B_free: free (V, Vhat) dofs -> pressure dofs
+    (reference `sys_.B[:, vv_free]`, condensation.py:178-186; element-batched
+    from the J-invariant Bpu, csrc/stokes.cu)."""
+
+    def __init__(self, sys_):
+        torch = torch_mod()
+        self.sys, self.k = sys_, sys_.k
+        z = sys_.z
+        self.nq, self.nu, self.nloc = z["nq"], z["nu"], z["nloc"]
+        self.nt = sys_.S_dev.shape[0]
+        self.Bpu = torch.from_numpy(np.ascontiguousarray(sys_.refs.bpu)).cuda()
+        self.codes = sys_.dev_maps()["vv_codes"]
+        self.n_p = self.nt * self.nq
+        self.n_v = sys_.maps.n_vv_free
+        self.shape = (self.n_p, self.n_v)
+
+    def apply(self, x, out=None, stream=None):
+        xd, host = as_device(x)
+        y = out if out is not None else empty(self.n_p)
+        _abi.call("mcs_apply_B", self.nq, self.nu, self.nloc, self.nt, _abi.ptr(self.Bpu),
+                  _abi.ptr(self.codes), _abi.ptr(xd), _abi.ptr(y), _abi.stream(stream))
+        return y.cpu().numpy() if host else y
+
+    def apply_T(self, p, out=None, stream=None):
+        pd, host = as_device(p)
+        y = out if out is not None else empty(self.n_v)
+        y.zero_()
+        _abi.call("mcs_apply_BT", self.nq, self.nu, self.nloc, self.nt, _abi.ptr(self.Bpu),
+                  _abi.ptr(self.codes), _abi.ptr(pd), _abi.ptr(y), _abi.stream(stream))
+        return y.cpu().numpy() if host else y
+
+    __call__ = apply
+
+    def __matmul__(self, x):
+        return self.apply(x)
+
+
+class SaddleOperator:
+    """K = [[S_free, B_free^T], [B_free, 0]] on stacked (velocity, pressure)
+    vectors (reference driver.py:150)."""
+
+    def __init__(self, sys_):
+        self.S = SOperator(sys_)
+        self.B = BOperator(sys_)
+        self.n_v, self.n_p = self.B.n_v, self.B.n_p
+        self.n = self.n_v + self.n_p
+        self.shape = (self.n, self.n)
+        self._bt = empty(self.n_v)
+
+    def apply(self, x, out=None, stream=None):
+        xd, host = as_device(x)
+        y = out if out is not None else empty(self.n)
+        self.S.apply(xd[:self.n_v], out=y[:self.n_v], stream=stream)
+        self.B.apply_T(xd[self.n_v:], out=self._bt, stream=stream)
+        axpby(1.0, self._bt, 1.0, y[:self.n_v], stream)     # S x_u + (B^T x_p): fixed order
+        self.B.apply(xd[:self.n_v], out=y[self.n_v:], stream=stream)
+        return y.cpu().numpy() if host else y
+
+    __call__ = apply
+
+    def __matmul__(self, x):
+        return self.apply(x)

@@ -371,3 +371,65 @@ class ExtendedAsp:
         return out.cpu().numpy() if host else out
 
     __call__ = apply
+
+
+# ------------------------------------------------------ Stokes (saddle) mode
+
+class PressureMassPrecond:
+    """Exact inverse of the nu^-1-scaled pressure mass matrix (reference
+    `preconditioners.py:384-402`): diagonal detJ_t / nu on the element-major
+    pressure dofs (orthonormal element bases)."""
+
+    def __init__(self, diag):
+        torch = __import__("torch")
+        self.diag = np.asarray(diag, dtype=float)
+        self.diag_dev = torch.from_numpy(self.diag).cuda()
+
+    @classmethod
+    def build(cls, fes, nu: float):
+        nq = fes.dof_q.loc2glob.shape[1]
+        d = np.empty(fes.dof_q.ndof)
+        d[fes.dof_q.loc2glob.ravel()] = np.repeat(fes.detJ / nu, nq)
+        return cls(d)
+
+    def apply(self, r, out=None, stream=None):
+        rd, host = as_device(r)
+        out = out if out is not None else empty(len(self.diag))
+        __import__("torch").div(rd, self.diag_dev, out=out)
+        return out.cpu().numpy() if host else out
+
+    def mass_matrix(self):
+        return sp.diags(self.diag).tocsr()
+
+
+class SaddlePreconditioner:
+    """Block triangular preconditioner, two velocity solves per application
+    (reference `preconditioners.py:405-420`):
+        a = V r_u;  dp = P (r_p - B a);  du = a - V (B^T dp)."""
+
+    def __init__(self, velocity_apply, pressure: PressureMassPrecond, B):
+        self.velocity_apply, self.pressure, self.B = velocity_apply, pressure, B
+        self.n_v, self.n_p = B.n_v, B.n_p
+        self._a, self._bt, self._v2 = empty(self.n_v), empty(self.n_v), empty(self.n_v)
+        self._bp = empty(self.n_p)
+
+    def _vel(self, r, out):
+        if hasattr(self.velocity_apply, "apply"):
+            return self.velocity_apply.apply(r, out=out)
+        out.copy_(self.velocity_apply(r))
+        return out
+
+    def apply(self, r, out=None, stream=None):
+        rd, host = as_device(r)
+        out = out if out is not None else empty(self.n_v + self.n_p)
+        a = self._vel(rd[:self.n_v], self._a)
+        self.B.apply(a, out=self._bp, stream=stream)
+        axpby(1.0, rd[self.n_v:], -1.0, self._bp, stream)          # r_p - B a
+        dp = self.pressure.apply(self._bp, out=out[self.n_v:], stream=stream)
+        self.B.apply_T(dp, out=self._bt, stream=stream)
+        v2 = self._vel(self._bt, self._v2)
+        out[:self.n_v].copy_(a)
+        axpby(-1.0, v2, 1.0, out[:self.n_v], stream)              # a - V(B^T dp)
+        return out.cpu().numpy() if host else out
+
+    __call__ = apply

@@ -88,3 +88,20 @@ def test_gpu_recover_stress_device_tensors(cuda):
     s_h, w_h = sys_.recover_stress(x)
     s_d, w_d = sys_.recover_stress(torch.from_numpy(x).cuda())
     assert np.array_equal(s_d.cpu().numpy(), s_h) and np.array_equal(w_d.cpu().numpy(), w_h)
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("name,cfg,n", [("c1_n2", 1, 2), ("c2_n3", 2, 3), ("c3_n2", 3, 2)])
+def test_gpu_recover_stress_matches_reference_fixture(cuda, name, cfg, n):
+    """Against the recovery matrices R_T the reference itself produced
+    (tests/golden, condensation.py:159-177)."""
+    from conftest import golden
+    from paper_2207_08481_b200.condensation import condense_sigma_omega
+    g = golden(name)
+    prob, fes = _setup(cfg, n)
+    sys_ = condense_sigma_omega(fes, prob.nu, prob.body_force)
+    x = np.random.default_rng(14).standard_normal(fes.n_vv)
+    sig, om = sys_.recover_stress(x)
+    s_ref, w_ref = O.recover_stress(fes, list(g["recovery"]), x)
+    assert rel(sig, s_ref) <= 1e-10
+    assert rel(om, w_ref) <= 1e-10

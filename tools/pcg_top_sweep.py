@@ -19,7 +19,7 @@ prob = baseline_config(cfg)
 fes = FeSystem(prob.mesh, prob.regions, prob.k)
 sys_ = double_schur(condense_sigma_omega(fes, prob.nu, prob.body_force))
 S = SOperator(sys_)
-b = torch.from_numpy(condensed_rhs(fes, sys_)).cuda()
+b = torch.from_numpy(condensed_rhs(fes, sys_)[0]).cuda()
 for top in [int(v) for v in sys.argv[1:]] or [4096]:
     coarse.TOP_MAX = top
     t0 = time.perf_counter()

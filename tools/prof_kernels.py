@@ -35,6 +35,6 @@ if what in ("all", "cfg"):
     fes = FeSystem(prob.mesh, prob.regions, prob.k)
     sys_ = double_schur(condense_sigma_omega(fes, prob.nu, prob.body_force))
     M = velocity_preconditioner(fes, sys_, prob.nu, SolverOptions(composition="multiplicative"))
-    x, rep = cg(SOperator(sys_), condensed_rhs(fes, sys_), M, rtol=1e-8, maxit=3)
+    x, rep = cg(SOperator(sys_), condensed_rhs(fes, sys_)[0], M, rtol=1e-8, maxit=3)
     torch.cuda.synchronize()
     print("iters", rep.iterations)

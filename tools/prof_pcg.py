@@ -19,7 +19,7 @@ fes = FeSystem(prob.mesh, prob.regions, prob.k)
 sys_ = double_schur(condense_sigma_omega(fes, prob.nu, prob.body_force))
 M = velocity_preconditioner(fes, sys_, prob.nu, SolverOptions(composition=comp))
 S = SOperator(sys_)
-b = torch.from_numpy(condensed_rhs(fes, sys_)).cuda()
+b = torch.from_numpy(condensed_rhs(fes, sys_)[0]).cuda()
 torch.cuda.synchronize()
 torch.cuda.cudart().cudaProfilerStart()
 x, rep = cg(S, b, M, rtol=1e-8, maxit=int(os.environ.get("PROF_IT", "4")), use_graph=False)

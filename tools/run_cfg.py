@@ -30,7 +30,7 @@ out["condense_total_s"] = time.perf_counter() - t0
 out["elements"] = prob.mesh.num_triangles
 out["n_vv_free"] = sys_.maps.n_vv_free
 S = SOperator(sys_)
-b = torch.from_numpy(condensed_rhs(fes, sys_)).cuda()
+b = torch.from_numpy(condensed_rhs(fes, sys_)[0]).cuda()
 for comp in ("additive", "multiplicative"):
     t0 = time.perf_counter()
     M = velocity_preconditioner(fes, sys_, prob.nu, SolverOptions(composition=comp))
