@@ -75,33 +75,29 @@ __global__ void jacobi_setup_kernel(const double* __restrict__ Sd, int sd_stride
   if (info) info[b] = bad;
 }
 
-// Row-parallel variant: thread (b, i) = output row i of facet block b, so
-// B x more independent loads are in flight than with one thread per block
-// (the 2.2k-facet / 148-SM grid of the thread-per-block kernel cannot hide
-// HBM latency).  r is gathered B times (L1/L2 hits), binv / bidx / x stay
-// coalesced along b.
+// Thread per facet block, all loads issued before the first FMA.
 template <int B>
-__global__ void __launch_bounds__(128)
-    jacobi_apply_rows_kernel(const double* __restrict__ binv, const int* __restrict__ bidx,
-                             int nblk, const double* __restrict__ r, double* __restrict__ x,
-                             double scale_inv) {
+__global__ void __launch_bounds__(64)
+    jacobi_apply_kernel(const double* __restrict__ binv, const int* __restrict__ bidx, int nblk,
+                        const double* __restrict__ r, double* __restrict__ x, double scale_inv) {
   const int b = blockIdx.x * blockDim.x + threadIdx.x;
-  const int i = blockIdx.y;
   if (b >= nblk) return;
+  constexpr int NP = B * (B + 1) / 2;
   int id[B];
-  double rl[B], a[B];
+  double rl[B], a[NP];
 #pragma unroll
-  for (int j = 0; j < B; ++j) {
-    id[j] = __ldg(bidx + (int64_t)j * nblk + b);
-    const int p = i >= j ? pk(i, j) : pk(j, i);
-    a[j] = __ldg(binv + (int64_t)p * nblk + b);
-  }
+  for (int j = 0; j < B; ++j) id[j] = __ldg(bidx + (int64_t)j * nblk + b);
+#pragma unroll
+  for (int p = 0; p < NP; ++p) a[p] = __ldg(binv + (int64_t)p * nblk + b);
 #pragma unroll
   for (int j = 0; j < B; ++j) rl[j] = id[j] >= 0 ? __ldg(r + id[j]) : 0.0;
-  double s = 0.0;
 #pragma unroll
-  for (int j = 0; j < B; ++j) s = fma(a[j], rl[j], s);
-  if (id[i] >= 0) x[id[i]] = s * scale_inv;
+  for (int i = 0; i < B; ++i) {
+    double s = 0.0;
+#pragma unroll
+    for (int j = 0; j < B; ++j) s = fma(a[i >= j ? pk(i, j) : pk(j, i)], rl[j], s);
+    if (id[i] >= 0) x[id[i]] = s * scale_inv;
+  }
 }
 
 template <int LANES>
@@ -144,13 +140,13 @@ MCS_API int mcs_jacobi_apply(int k, int nblk, const double* binv, const int* bid
                              const double* r, double* x, double scale_inv, void* stream) {
   if (nblk <= 0) return 0;
   auto st = static_cast<cudaStream_t>(stream);
-  const dim3 grid((nblk + 127) / 128, 2 * k + 1);
+  const int grid = (nblk + 63) / 64;
   switch (k) {
-    case 2: jacobi_apply_rows_kernel<5><<<grid, 128, 0, st>>>(binv, bidx, nblk, r, x, scale_inv); break;
-    case 3: jacobi_apply_rows_kernel<7><<<grid, 128, 0, st>>>(binv, bidx, nblk, r, x, scale_inv); break;
-    case 4: jacobi_apply_rows_kernel<9><<<grid, 128, 0, st>>>(binv, bidx, nblk, r, x, scale_inv); break;
-    case 5: jacobi_apply_rows_kernel<11><<<grid, 128, 0, st>>>(binv, bidx, nblk, r, x, scale_inv); break;
-    case 6: jacobi_apply_rows_kernel<13><<<grid, 128, 0, st>>>(binv, bidx, nblk, r, x, scale_inv); break;
+    case 2: jacobi_apply_kernel<5><<<grid, 64, 0, st>>>(binv, bidx, nblk, r, x, scale_inv); break;
+    case 3: jacobi_apply_kernel<7><<<grid, 64, 0, st>>>(binv, bidx, nblk, r, x, scale_inv); break;
+    case 4: jacobi_apply_kernel<9><<<grid, 64, 0, st>>>(binv, bidx, nblk, r, x, scale_inv); break;
+    case 5: jacobi_apply_kernel<11><<<grid, 64, 0, st>>>(binv, bidx, nblk, r, x, scale_inv); break;
+    case 6: jacobi_apply_kernel<13><<<grid, 64, 0, st>>>(binv, bidx, nblk, r, x, scale_inv); break;
     default: return -1000;
   }
   return launch_status();
