@@ -43,6 +43,25 @@ struct FTab {
   static constexpr int len = o_A + even(6 * 9 * ml);
 };
 
+// optional per-phase clock accounting (tools/fused_prof.py builds a copy of
+// this file with MCS_FUSED_PROF defined; the library never does)
+#ifdef MCS_FUSED_PROF
+__device__ unsigned long long g_fz_prof[8];
+#define FZ_T0() long long _fz_t = clock64()
+#define FZ_T(i)                                                              \
+  do {                                                                       \
+    __syncwarp();                                                            \
+    if ((threadIdx.x & 31) == 0) {                                           \
+      const long long _n = clock64();                                        \
+      atomicAdd(&g_fz_prof[i], (unsigned long long)(_n - _fz_t));            \
+      _fz_t = _n;                                                            \
+    }                                                                        \
+  } while (0)
+#else
+#define FZ_T0()
+#define FZ_T(i)
+#endif
+
 namespace fz {
 
 constexpr int W_MSIG = 0, W_ADIV = 27, NWS = 36;   // weight slots (refblocks.py), 30.. = 0
@@ -189,6 +208,7 @@ __global__ void __launch_bounds__(32 * WPB, MINB)
     __syncwarp();
     int bad = 0;
 
+    FZ_T0();
     // ---------------- A: bubble block factor and the 3x3 block factors
     double* Ls = U;
     double* Li = U + nb * nb;
@@ -293,6 +313,7 @@ __global__ void __launch_bounds__(32 * WPB, MINB)
     }
     __syncwarp();
 
+    FZ_T(0);
     // ---------------- B: Y in registers, one 8-row tile of B at a time
     double2 Yf[NRB][NKC];
     double* Bt = U;
@@ -358,6 +379,7 @@ __global__ void __launch_bounds__(32 * WPB, MINB)
       __syncwarp();
     }
 
+    FZ_T(1);
     // ---------------- C: S_T = adiv + Y Y^T (DMMA), packed into shared memory
     const double wad = wts[fz::W_ADIV];
 #pragma unroll
@@ -387,6 +409,7 @@ __global__ void __launch_bounds__(32 * WPB, MINB)
       for (int q = lane; q < G::st_len / 2; q += 32) dst[q] = src[q];
     }
 
+    FZ_T(2);
     // ---------------- D: double Schur on the element-local S_T
     //   S_oo = L L^T (lane-per-row Cholesky), L^-1 (lane-per-column forward
     //   substitution), then four small GEMMs on the tensor cores:
@@ -513,6 +536,7 @@ __global__ void __launch_bounds__(32 * WPB, MINB)
         }
       }
     }
+    FZ_T(3);
     if (lane == 0 && info) info[e] = bad;
     __syncwarp();
   }
@@ -565,3 +589,9 @@ MCS_API int mcs_condense_fused(int k, int64_t nt, const double* W, int nwgt, con
   }
   return -1000;
 }
+
+#ifdef MCS_FUSED_PROF
+extern "C" __attribute__((visibility("default"))) void fz_prof_read(unsigned long long* out) {
+  cudaMemcpyFromSymbol(out, mcs::g_fz_prof, 8 * sizeof(unsigned long long));
+}
+#endif
