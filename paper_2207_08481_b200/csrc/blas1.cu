@@ -10,7 +10,7 @@
 
 namespace mcs {
 
-constexpr int RED_BLOCKS = 296;  // 2 x 148 SMs
+constexpr int RED_BLOCKS = 1184;  // 8 x 148 SMs: enough loads in flight for HBM
 constexpr int RED_THREADS = 256;
 
 __device__ __forceinline__ double block_sum(double v) {
@@ -101,7 +101,7 @@ __global__ void axpby_kernel(int64_t n, double a, const double* __restrict__ x, 
 
 static int grid_for(int64_t n) {
   const int64_t g = (n + 255) / 256;
-  return (int)(g < 4 * 148 ? (g < 1 ? 1 : g) : 4 * 148);
+  return (int)(g < 16 * 148 ? (g < 1 ? 1 : g) : 16 * 148);
 }
 
 }  // namespace mcs

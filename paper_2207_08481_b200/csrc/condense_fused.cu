@@ -122,7 +122,10 @@ struct Geo {
                    : (i < nu ? 4 * ns * NEM + ns * (i - NEM)
                              : 4 * ns * NEM + ns * (nu - NEM) + 3 * ns * (i - nu));
   }
-  static constexpr int TAB_SMEM = even(4 * ns * NEM + ns * (nu - NEM) + 3 * ns * (nloc - nu));
+  static constexpr int TAB_B = even(4 * ns * NEM + ns * (nu - NEM) + 3 * ns * (nloc - nu));
+  static constexpr int TAB_MB = TAB_B;                       // MbRef [6][nb][nb]
+  static constexpr int TAB_A = TAB_MB + even(6 * nb * nb);   // ARef [6][ml][9]
+  static constexpr int TAB_SMEM = TAB_A + even(6 * 9 * ml);
   // bubble column of DMMA n-tile bt, output column n (-1: none)
   __host__ __device__ static constexpr int jmap(int bt, int n) {
     if (MIX && bt == 0) return (n >= 2 * r && n - 2 * r < nb) ? n - 2 * r : -1;
@@ -171,6 +174,8 @@ __global__ void __launch_bounds__(32 * WPB, MINB)
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, g = lane >> 2, t = lane & 3;
   double* stab = smem;                                   // compact Bsig tables (per CTA)
   double* sw = smem + G::TAB_SMEM + warp * G::PER_WARP;
+  for (int q = threadIdx.x; q < 6 * nb * nb; q += 32 * WPB) stab[G::TAB_MB + q] = tab[T::o_Mb + q];
+  for (int q = threadIdx.x; q < 6 * 9 * ml; q += 32 * WPB) stab[G::TAB_A + q] = tab[T::o_A + q];
   for (int q = threadIdx.x; q < nloc * ns; q += 32 * WPB) {
     const int i = q / ns, c = q % ns, ty = G::row_type(i);
     const double* src = tab + T::o_G4 + 4 * q;
@@ -221,9 +226,9 @@ __global__ void __launch_bounds__(32 * WPB, MINB)
 #pragma unroll
       for (int r = 0; r < 6; ++r) {
         const double w = wts[fz::W_MSIG + r];
-        const double* mr = tab + T::o_Mb + (r * nb + i) * nb;
+        const double* mr = stab + G::TAB_MB + (r * nb + i) * nb;
 #pragma unroll
-        for (int c = 0; c < nb; ++c) a[c] = fma(w, __ldg(mr + c), a[c]);
+        for (int c = 0; c < nb; ++c) a[c] = fma(w, mr[c], a[c]);
       }
       if (!fz::chol_rows<nb>(a, l, Rd)) bad |= 1;
       if (lane < nb) {
@@ -238,9 +243,9 @@ __global__ void __launch_bounds__(32 * WPB, MINB)
 #pragma unroll
       for (int r = 0; r < 6; ++r) {
         const double w = wts[fz::W_MSIG + r];
-        const double* ar = tab + T::o_A + (r * ml + lane) * 9;
+        const double* ar = stab + G::TAB_A + (r * ml + lane) * 9;
 #pragma unroll
-        for (int q = 0; q < 9; ++q) A[q] = fma(w, __ldg(ar + q), A[q]);
+        for (int q = 0; q < 9; ++q) A[q] = fma(w, ar[q], A[q]);
       }
       // s = detJ skew(T_a): the bws weights (refblocks.py W_BWS)
       const double s0 = wts[6], s1 = wts[7], s2 = wts[8];

@@ -187,10 +187,11 @@ def gmres(apply_A, b, apply_M=None, rtol=1e-6, maxit=500, project=None, x0=None)
     Givens-rotated least-squares residual, happy-breakdown test
     h_{j+1,j} <= 1e-14 |rotated diagonal|, FloatingPointError on a
     non-finite h, x = x0 + M (V y).  The Arnoldi orthogonalisation is
-    classical Gram-Schmidt applied twice (CGS2: two deterministic V w /
-    V^T h product pairs per step, csrc/stokes.cu) instead of the
-    reference's modified Gram-Schmidt loop: the same Hessenberg matrix up to
-    rounding, with one host read-back of the column per step.  The small
+    classical Gram-Schmidt with DGKS re-orthogonalisation (one or two
+    deterministic V w / V^T h product pairs per step, csrc/stokes.cu)
+    instead of the reference's modified Gram-Schmidt loop: the same
+    Hessenberg matrix up to rounding, with one host read-back of the column
+    per step.  The small
     (maxit+1) x maxit least-squares problem stays on the host, as in the
     reference."""
     import torch
@@ -236,13 +237,21 @@ def gmres(apply_A, b, apply_M=None, rtol=1e-6, maxit=500, project=None, x0=None)
         if project is not None:
             w = project(w)
         m = j + 1
-        for hh in (h1, h2):                               # CGS2
+        wnorm = _norm(ws, w)
+        # classical Gram-Schmidt, repeated once when the first pass lost more
+        # than half the norm (DGKS criterion 1/sqrt(2)): MGS-quality
+        # orthogonality at the cost of one or two V w / V^T h pairs per step
+        h2.zero_()
+        for hh in (h1, h2):
             _abi.call("mcs_mdot", m, n, n, _abi.ptr(V), _abi.ptr(w), _abi.ptr(partial),
                       _abi.ptr(hh), _abi.stream(None))
             _abi.call("mcs_gemv_acc", m, n, n, _abi.ptr(V), _abi.ptr(hh), -1.0, 1.0,
                       _abi.ptr(w), _abi.stream(None))
+            hnext = _norm(ws, w)
+            if hnext > 0.7071067811865476 * wnorm:
+                break
+            wnorm = hnext
         hcol = (h1[:m] + h2[:m]).cpu().numpy()
-        hnext = _norm(ws, w)
         H[:m, j] = hcol
         H[j + 1, j] = hnext
         if not np.isfinite(hnext) or not np.all(np.isfinite(hcol)):
