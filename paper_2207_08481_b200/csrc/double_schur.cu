@@ -12,6 +12,7 @@
 //   ext record  [X (n_int x ncpl, row-major) | S_oo^-1 (lower packed)]  (even stride)
 //   Sd_T        lower packed (even stride)
 #include "elim_v3.cuh"
+#include "elim_v5.cuh"
 
 namespace mcs {
 
@@ -182,6 +183,82 @@ static int launch_double_schur_v3(const double* ST, double* ext, double* Sd, int
   return launch_status();
 }
 
+// ---- v5: the left-looking signed-Cholesky engine of elim_v5.cuh on the same
+// K = [[S_oo, S_oc, I], [S_co, S_cc, 0], [I, 0, 0]] (n_int positive pivots).
+// The engine's STORE receives minus the trailing block:
+//   [[-Sd_T, X^T], [X, S_oo^-1]].
+template <int K, int W>
+using DsGeo5 = v5::Geo<((Sizes<K>::n_int + 7) / 8 * 8 + (Sizes<K>::ncpl + Sizes<K>::n_int + 7) / 8 * 8) / 8,
+                       (Sizes<K>::n_int + 7) / 8, W, Sizes<K>::n_int, Sizes<K>::n_int>;
+
+template <int K, int W, int MINB>
+__global__ void __launch_bounds__(32 * W, MINB)
+    double_schur_v5(const double* __restrict__ ST, double* __restrict__ ext,
+                    double* __restrict__ Sd, int* __restrict__ info, int64_t nt) {
+  using Z = Sizes<K>;
+  using L = ExtLayout<K>;
+  using G = DsGeo5<K, W>;
+  constexpr int NI = Z::n_int, NC = Z::ncpl, NEM = Z::n_em, NPP = 8 * G::NPB;
+  extern __shared__ __align__(128) double smem[];
+  __shared__ int bad;
+  __shared__ signed char expect[NPP];
+  for (int i = threadIdx.x; i < NPP; i += blockDim.x) expect[i] = 1;
+  for (int64_t e = blockIdx.x; e < nt; e += gridDim.x) {
+    if (threadIdx.x == 0) bad = 0;
+    __syncthreads();
+    const double* S = ST + e * L::st_len;
+    double* xo = ext + e * L::len;
+    double* so = Sd + e * L::sd_len;
+    auto sym = [&](int a, int b) { return __ldg(S + (a >= b ? pk(a, b) : pk(b, a))); };
+    auto entry = [&](int i, int j) -> double {   // padded (i, j), j < NPP (pivot columns)
+      if (i < NPP) {
+        if (i < NI && j < NI) return sym(NEM + i, NEM + j);
+        return i == j ? 1.0 : 0.0;
+      }
+      if (j >= NI) return 0.0;
+      const int r = i - NPP;
+      if (r < NC) return sym(cpl_local<K>(r), NEM + j);
+      return (r - NC == j) ? 1.0 : 0.0;              // identity rows (r < NC + NI), padding 0
+    };
+    auto fetch = [&](int bi, int bj) {
+      const int lane = threadIdx.x & 31, i = 8 * bi + (lane >> 2), j = 8 * bj + 2 * (lane & 3);
+      return make_double2(entry(i, j), entry(i, j + 1));
+    };
+    auto trail = [&](int i, int j) {                 // -K_tt: -S_cc, zero elsewhere
+      const int r = i - NPP, c = j - NPP;
+      return (r < NC && c < NC) ? -sym(cpl_local<K>(r), cpl_local<K>(c)) : 0.0;
+    };
+    auto store = [&](int i, int j, double v) {
+      const int r = i - NPP, c = j - NPP;
+      if (r < NC) so[pk(r, c)] = -v;
+      else if (r < NC + NI) {
+        if (c < NC) xo[(r - NC) * NC + c] = v;
+        else xo[L::x_len + pk(r - NC, c - NC)] = v;
+      }
+    };
+    v5::eliminate<G>(fetch, trail, store, smem, expect, &bad);
+    __syncthreads();
+    if (threadIdx.x == 0 && info) info[e] = bad;
+  }
+}
+
+template <int K, int W, int MINB>
+static int launch_double_schur_v5(const double* ST, double* ext, double* Sd, int* info, int64_t nt,
+                                  cudaStream_t st) {
+  using G = DsGeo5<K, W>;
+  auto kern = double_schur_v5<K, W, MINB>;
+  const size_t smem = G::SMEM * sizeof(double);
+  cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  int per_sm = 1, dev = 0, nsm = 148;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, 32 * W, smem);
+  if (per_sm < 1) per_sm = 1;
+  const int64_t g = (int64_t)per_sm * nsm;
+  kern<<<(int)(nt < g ? nt : g), 32 * W, smem, st>>>(ST, ext, Sd, info, nt);
+  return launch_status();
+}
+
 template <int K>
 static int launch_double_schur(const double* ST, double* ext, double* Sd, int* info, int64_t nt,
                                cudaStream_t st) {
@@ -237,8 +314,8 @@ MCS_API int mcs_double_schur(int k, int64_t nt, const double* S_packed, double* 
     case 2: return launch_double_schur_v3<2, 2, 6>(S_packed, ext, Sd_packed, info, nt, st);
     case 3: return launch_double_schur_v3<3, 2, 4>(S_packed, ext, Sd_packed, info, nt, st);
     case 4: return launch_double_schur_v3<4, 2, 4>(S_packed, ext, Sd_packed, info, nt, st);
-    case 5: return launch_double_schur_v3<5, 4, 2>(S_packed, ext, Sd_packed, info, nt, st);
-    case 6: return launch_double_schur_v3<6, 4, 2>(S_packed, ext, Sd_packed, info, nt, st);
+    case 5: return launch_double_schur_v5<5, 4, 4>(S_packed, ext, Sd_packed, info, nt, st);
+    case 6: return launch_double_schur_v5<6, 8, 2>(S_packed, ext, Sd_packed, info, nt, st);
   }
   return -1000;
 }

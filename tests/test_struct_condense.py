@@ -233,3 +233,36 @@ def test_gpu_fused_reports_failures(cuda):
     info = info.cpu().numpy()
     assert info[1] & 1
     assert (np.delete(info, [1]) == 0).all()
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("k", [4, 5, 6])
+def test_gpu_double_schur_kernel_matches_oracle(cuda, k):
+    """mcs_double_schur (the k = 5, 6 path; v5 engine) on GPU-condensed S_T:
+    X, S_oo^-1 and Sd_T against condensation.py:207-226."""
+    import torch
+    from paper_2207_08481_b200 import _abi
+    prob = baseline_config(2, 2)
+    fes = FeSystem(prob.mesh, prob.regions, k)
+    refs = refblocks.build_refs(fes)
+    W = refblocks.element_weights(fes, prob.nu)
+    L = engine.srecord_layout(k)
+    recs = _host_program_eval(engine.sblock_program(refs), W, L["len"])
+    ST, info = engine.condense_struct(k, engine.to_dev(recs))
+    nt = len(W)
+    ext = torch.empty((nt, _abi.call("mcs_ext_stride", k)), dtype=torch.float64, device="cuda")
+    Sd = torch.empty((nt, _abi.call("mcs_sd_stride", k)), dtype=torch.float64, device="cuda")
+    _abi.call("mcs_double_schur", k, nt, _abi.ptr(ST), _abi.ptr(ext), _abi.ptr(Sd),
+              _abi.ptr(info), _abi.stream(None))
+    assert (info.cpu().numpy() == 0).all()
+    z = refblocks.local_sizes(k)
+    ni, nc = z["n_int"], z["ncpl"]
+    S_all = engine.unpack_sym(ST.cpu().numpy(), z["nloc"])
+    E = ext.cpu().numpy()
+    Sd_got = engine.unpack_sym(Sd.cpu().numpy(), nc)
+    for t in range(nt):
+        Soo, X, Sd_ref = O.double_schur_element(S_all[t], k)
+        assert rel(E[t, :ni * nc].reshape(ni, nc), X) <= 1e-10
+        Sinv = engine.unpack_sym(E[t, ni * nc:ni * nc + ni * (ni + 1) // 2], ni)
+        assert rel(Sinv, np.linalg.inv(Soo)) <= 1e-10
+        assert rel(Sd_got[t], Sd_ref) <= 1e-10
