@@ -91,6 +91,38 @@ __device__ __forceinline__ void warp_rows(int nrows, const double* __restrict__ 
   }
 }
 
+// Thread-per-row GEMV for narrow rows (width <= THREAD_ROW_MAX): every row of
+// the node is in flight at once (one memory round trip instead of one per
+// 32 rows per warp); each thread reads its row's contiguous span, 4 partial
+// sums in a fixed order (deterministic).
+constexpr int THREAD_ROW_MAX = 48;
+template <class ROW, class EMIT>
+__device__ __forceinline__ void thread_rows(int nrows, const double* __restrict__ x, ROW row,
+                                            EMIT emit) {
+  for (int r = threadIdx.x; r < nrows; r += MF_THREADS) {
+    const double* p;
+    int lo, hi;
+    row(r, p, lo, hi);
+    double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
+    int j = lo;
+    for (; j + 3 < hi; j += 4) {
+      a0 = fma(__ldg(p + j), x[j], a0);
+      a1 = fma(__ldg(p + j + 1), x[j + 1], a1);
+      a2 = fma(__ldg(p + j + 2), x[j + 2], a2);
+      a3 = fma(__ldg(p + j + 3), x[j + 3], a3);
+    }
+    for (; j < hi; ++j) a0 = fma(__ldg(p + j), x[j], a0);
+    emit(r, (a0 + a1) + (a2 + a3));
+  }
+}
+
+template <class ROW, class EMIT>
+__device__ __forceinline__ void node_rows(int nrows, int width, const double* __restrict__ x,
+                                          ROW row, EMIT emit) {
+  if (width <= THREAD_ROW_MAX) thread_rows(nrows, x, row, emit);
+  else warp_rows(nrows, x, row, emit);
+}
+
 // shared layout per node: [t or s : ns][ys : ns][pass or xb : nb]
 __global__ void __launch_bounds__(MF_THREADS)
     mf_forward(const int* __restrict__ level_nodes, const NodeRec* __restrict__ nodes,
@@ -126,8 +158,8 @@ __global__ void __launch_bounds__(MF_THREADS)
   __syncthreads();
   // y_S = Linv t (packed lower, row-major), then out_B = W y_S + pass
   const double* L = mats + nd.oL;
-  warp_rows(
-      ns, t,
+  node_rows(
+      ns, ns, t,
       [&](int r, const double*& p, int& lo, int& hi) {
         p = L + (int64_t)r * (r + 1) / 2;
         lo = 0;
@@ -139,8 +171,8 @@ __global__ void __launch_bounds__(MF_THREADS)
       });
   __syncthreads();
   const double* W = mats + nd.oW;
-  warp_rows(
-      nb, ys,
+  node_rows(
+      nb, ns, ys,
       [&](int r, const double*& p, int& lo, int& hi) {
         p = W + (int64_t)r * ns;
         lo = 0;
@@ -164,8 +196,8 @@ __global__ void __launch_bounds__(MF_THREADS)
   __syncthreads();
   // s = y_S - W^T x_B (W^T row-major ns x nb), then x_S = Linv^T s (packed upper)
   const double* WT = mats + nd.oWT;
-  warp_rows(
-      ns, xb,
+  node_rows(
+      ns, nb, xb,
       [&](int r, const double*& p, int& lo, int& hi) {
         p = WT + (int64_t)r * nb;
         lo = 0;
@@ -174,8 +206,8 @@ __global__ void __launch_bounds__(MF_THREADS)
       [&](int r, double v) { s[r] = __ldg(y + nd.s0 + r) - v; });
   __syncthreads();
   const double* LT = mats + nd.oLT;  // packed upper, row r holds columns r..ns-1
-  warp_rows(
-      ns, s,
+  node_rows(
+      ns, ns, s,
       [&](int r, const double*& p, int& lo, int& hi) {
         p = LT + upk_row(r, ns);
         lo = r;
