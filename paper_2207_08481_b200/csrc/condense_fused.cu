@@ -387,25 +387,33 @@ __global__ void __launch_bounds__(32 * WPB, MINB)
     FZ_T(1);
     // ---------------- C: S_T = adiv + Y Y^T (DMMA), packed into shared memory
     const double wad = wts[fz::W_ADIV];
+    // one tile row I at a time: the I + 1 independent accumulator chains of
+    // the row interleave (k outer, J inner) and share the A operand Y_I
 #pragma unroll
     for (int I = 0; I < NRB; ++I) {
+      double acc[NRB][2];
+#pragma unroll
+      for (int J = 0; J <= I; ++J) acc[J][0] = acc[J][1] = 0.0;
+#pragma unroll
+      for (int kc = 0; kc < NKC; ++kc) {
+#pragma unroll
+        for (int J = 0; J <= I; ++J) dmma884(acc[J][0], acc[J][1], Yf[I][kc].x, Yf[J][kc].x);
+#pragma unroll
+        for (int J = 0; J <= I; ++J) dmma884(acc[J][0], acc[J][1], Yf[I][kc].y, Yf[J][kc].y);
+      }
+      const int i = 8 * I + g;
 #pragma unroll
       for (int J = 0; J <= I; ++J) {
-        double c0 = 0.0, c1 = 0.0;
-#pragma unroll
-        for (int kc = 0; kc < NKC; ++kc) {
-          dmma884(c0, c1, Yf[I][kc].x, Yf[J][kc].x);
-          dmma884(c0, c1, Yf[I][kc].y, Yf[J][kc].y);
-        }
-        const int i = 8 * I + g, j = 8 * J + 2 * t;
+        const int j = 8 * J + 2 * t;
+        double c0 = acc[J][0], c1 = acc[J][1];
         if (i < nu && j < nu) c0 = fma(wad, __ldg(tab + T::o_adiv + i * nu + j), c0);
         if (i < nu && j + 1 < nu) c1 = fma(wad, __ldg(tab + T::o_adiv + i * nu + j + 1), c1);
         if (i < nloc) {
           if (j <= i) Spk[pk(i, j)] = c0;
           if (j + 1 <= i) Spk[pk(i, j + 1)] = c1;
         }
-        asm volatile("" ::: "memory");   // keep the epilogue loads tile by tile (registers)
       }
+      asm volatile("" ::: "memory");   // keep the epilogue loads row by row (registers)
     }
     __syncwarp();
     {
