@@ -29,7 +29,10 @@ __device__ __forceinline__ double block_sum(double v) {
   return s;  // valid in thread 0
 }
 
-// last block: sum partials[0..RED_BLOCKS) in order -> *out
+// last block: sum partials[0..gridDim) -> *out with all its threads (fixed
+// strided assignment + the fixed block_sum tree: deterministic).  Partials
+// are read through L2 (ld.global.cg) after the fence, batched, instead of
+// one volatile round trip at a time.
 __device__ __forceinline__ void finish(double part, double* partials, unsigned* counter,
                                        double* out) {
   __shared__ bool last;
@@ -41,15 +44,12 @@ __device__ __forceinline__ void finish(double part, double* partials, unsigned* 
   __syncthreads();
   if (!last) return;
   __threadfence();
-  if (threadIdx.x < 32) {
-    double s = 0.0;
-    for (int b = threadIdx.x; b < (int)gridDim.x; b += 32) s += ((volatile double*)partials)[b];
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) s += __shfl_down_sync(0xffffffffu, s, o);
-    if (threadIdx.x == 0) {
-      *out = s;
-      *counter = 0u;
-    }
+  double s = 0.0;
+  for (int b = threadIdx.x; b < (int)gridDim.x; b += RED_THREADS) s += __ldcg(partials + b);
+  s = block_sum(s);
+  if (threadIdx.x == 0) {
+    *out = s;
+    *counter = 0u;
   }
 }
 
