@@ -28,7 +28,7 @@ struct WarpRing {
 
 // Signed gather x_loc[j] = sign * x[idx] (0 for constrained dofs).
 __device__ __forceinline__ double gather_signed(const double* x, int c) {
-  return c >= 0 ? code_sign(c) * __ldg(x + code_index(c)) : 0.0;
+  return c >= 0 ? code_sign(c) * x[code_index(c)] : 0.0;   // x: produced upstream (no ld.nc)
 }
 
 // y = sum_T P^T D M_T D P x, warp per element, W warps per CTA, NST bulk-copy
@@ -39,7 +39,7 @@ __device__ __forceinline__ double gather_signed(const double* x, int c) {
 template <int N, int STRIDE, int W, int NST>
 __global__ void __launch_bounds__(W * 32)
     elem_apply_kernel(const double* __restrict__ M, const int* __restrict__ codes,
-                      const double* __restrict__ x, double* __restrict__ y, int64_t nt) {
+                      const double* x, double* __restrict__ y, int64_t nt) {
   constexpr int R = (N + 31) / 32;
   extern __shared__ __align__(128) double sm[];
   __shared__ __align__(8) uint64_t bars[W][NST];
@@ -73,6 +73,8 @@ __global__ void __launch_bounds__(W * 32)
     cd0[r] = (j < N && e0 < nt) ? __ldg(codes + e0 * N + j) : -1;
     cd1[r] = (j < N && e1 < nt) ? __ldg(codes + e1 * N + j) : -1;
   }
+  pdl_wait();   // static data (matrix bulk copies, codes) is in flight; x may now be read
+  pdl_trigger();
 #pragma unroll
   for (int r = 0; r < R; ++r) xv[r] = gather_signed(x, cd0[r]);
   int it = 0;
@@ -136,7 +138,7 @@ __global__ void __launch_bounds__(W * 32)
 template <int K, int LEN, int W, int NST>
 __global__ void __launch_bounds__(W * 32)
     ext_restrict_kernel(const double* __restrict__ ext, const int* __restrict__ bidx,
-                        const int* __restrict__ ccodes, const double* __restrict__ r,
+                        const int* __restrict__ ccodes, const double* r,
                         double* __restrict__ bubble, double* __restrict__ acc, int64_t nt) {
   using Z = Sizes<K>;
   constexpr int NI = Z::n_int, NC = Z::ncpl, XL = NI * NC;
@@ -169,8 +171,15 @@ __global__ void __launch_bounds__(W * 32)
   for (int q = 0; q < RI; ++q) {
     const int j = lane + 32 * q;
     const int b0 = (j < NI && gw < nt) ? __ldg(bidx + gw * NI + j) : -1;
-    rv[q] = b0 >= 0 ? __ldg(r + b0) : 0.0;
+    rv[q] = (double)b0;   // index parked until r may be read
     b1[q] = (j < NI && gw + nw < nt) ? __ldg(bidx + (gw + nw) * NI + j) : -1;
+  }
+  pdl_wait();
+  pdl_trigger();
+#pragma unroll
+  for (int q = 0; q < RI; ++q) {
+    const int b0 = (int)rv[q];
+    rv[q] = b0 >= 0 ? r[b0] : 0.0;
   }
 #pragma unroll
   for (int q = 0; q < RC; ++q) {
@@ -192,7 +201,7 @@ __global__ void __launch_bounds__(W * 32)
 #pragma unroll
     for (int q = 0; q < RI; ++q) {
       const int j = lane + 32 * q;
-      rv[q] = b1[q] >= 0 ? __ldg(r + b1[q]) : 0.0;
+      rv[q] = b1[q] >= 0 ? r[b1[q]] : 0.0;
       b1[q] = (j < NI && e2 < nt) ? __ldg(bidx + e2 * NI + j) : -1;
     }
 #pragma unroll
@@ -248,8 +257,8 @@ __global__ void __launch_bounds__(W * 32)
 template <int K, int LEN, int W, int NST>
 __global__ void __launch_bounds__(W * 32)
     ext_prolong_kernel(const double* __restrict__ ext, const int* __restrict__ bidx,
-                       const int* __restrict__ ccodes, const double* __restrict__ zc,
-                       const double* __restrict__ bubble, double* __restrict__ out, int64_t nt) {
+                       const int* __restrict__ ccodes, const double* zc,
+                       const double* bubble, double* __restrict__ out, int64_t nt) {
   using Z = Sizes<K>;
   constexpr int NI = Z::n_int, NC = Z::ncpl, XL = NI * NC;
   constexpr int XLE = even(XL);
@@ -281,9 +290,15 @@ __global__ void __launch_bounds__(W * 32)
 #pragma unroll
   for (int q = 0; q < RC; ++q) {
     const int c = lane + 32 * q;
-    const int c0 = (c < NC && gw < nt) ? __ldg(ccodes + gw * NC + c) : -1;
-    zv[q] = gather_signed(zc, c0);
+    zv[q] = (double)((c < NC && gw < nt) ? __ldg(ccodes + gw * NC + c) : -1);
     c1[q] = (c < NC && gw + nw < nt) ? __ldg(ccodes + (gw + nw) * NC + c) : -1;
+  }
+  pdl_wait();
+  pdl_trigger();
+#pragma unroll
+  for (int q = 0; q < RC; ++q) {
+    const int c0 = (int)zv[q];
+    zv[q] = gather_signed(zc, c0);
   }
   int it = 0;
   for (int64_t e = gw; e < nt; e += nw, ++it) {
@@ -305,7 +320,7 @@ __global__ void __launch_bounds__(W * 32)
 #pragma unroll
     for (int q = 0; q < RI; ++q) {
       const int i = lane + 32 * q;
-      bub[q] = i < NI ? __ldg(bubble + e * NI + i) : 0.0;
+      bub[q] = i < NI ? bubble[e * NI + i] : 0.0;
       bi[q] = i < NI ? __ldg(bidx + e * NI + i) : 0;
     }
     __syncwarp();
@@ -335,15 +350,19 @@ __global__ void __launch_bounds__(W * 32)
 }
 
 // w_c[j] = r[map[j]] - acc[j]
-__global__ void gather_sub_kernel(const double* __restrict__ r, const int* __restrict__ map,
-                                  const double* __restrict__ acc, double* __restrict__ w, int n) {
+__global__ void gather_sub_kernel(const double* r, const int* __restrict__ map,
+                                  const double* acc, double* __restrict__ w, int n) {
+  pdl_wait();
+  pdl_trigger();
   for (int j = blockIdx.x * blockDim.x + threadIdx.x; j < n; j += gridDim.x * blockDim.x)
     w[j] = r[map[j]] - acc[j];
 }
 
 // out[map[j]] = z[j]
-__global__ void scatter_kernel(const double* __restrict__ z, const int* __restrict__ map,
+__global__ void scatter_kernel(const double* z, const int* __restrict__ map,
                                double* __restrict__ out, int n) {
+  pdl_wait();
+  pdl_trigger();
   for (int j = blockIdx.x * blockDim.x + threadIdx.x; j < n; j += gridDim.x * blockDim.x)
     out[map[j]] = z[j];
 }
@@ -386,8 +405,7 @@ static int launch_apply(const double* M, const int* codes, const double* x, doub
   if (per_sm < 1) per_sm = 1;
   const int64_t want = (nt + W - 1) / W;
   const int64_t g = (int64_t)per_sm * sm_count();
-  kern<<<(int)(want < g ? want : g), W * 32, smem, st>>>(M, codes, x, y, nt);
-  return launch_status();
+  return launch_pdl_g(PDL_ELEM, kern, (int)(want < g ? want : g), W * 32, smem, st, M, codes, x, y, nt);
 }
 
 template <int K>
@@ -408,8 +426,8 @@ static int launch_restrict(const double* ext, const int* bidx, const int* cc, co
   cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, W * 32, smem);
   if (per_sm < 1) per_sm = 1;
   const int64_t want = (nt + W - 1) / W, g = (int64_t)per_sm * sm_count();
-  kern<<<(int)(want < g ? want : g), W * 32, smem, st>>>(ext, bidx, cc, r, bubble, acc, nt);
-  return launch_status();
+  return launch_pdl_g(PDL_ELEM, kern, (int)(want < g ? want : g), W * 32, smem, st, ext, bidx, cc, r, bubble,
+                    acc, nt);
 }
 
 template <int K>
@@ -426,8 +444,8 @@ static int launch_prolong(const double* ext, const int* bidx, const int* cc, con
   cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, W * 32, smem);
   if (per_sm < 1) per_sm = 1;
   const int64_t want = (nt + W - 1) / W, g = (int64_t)per_sm * sm_count();
-  kern<<<(int)(want < g ? want : g), W * 32, smem, st>>>(ext, bidx, cc, zc, bubble, out, nt);
-  return launch_status();
+  return launch_pdl_g(PDL_ELEM, kern, (int)(want < g ? want : g), W * 32, smem, st, ext, bidx, cc, zc, bubble,
+                    out, nt);
 }
 
 }  // namespace mcs
@@ -492,14 +510,12 @@ MCS_API int mcs_gather_sub(int n, const double* r, const int* map, const double*
   if (n <= 0) return 0;
   auto st = static_cast<cudaStream_t>(stream);
   const int grid = (n + 255) / 256 < 4 * sm_count() ? (n + 255) / 256 : 4 * sm_count();
-  gather_sub_kernel<<<grid, 256, 0, st>>>(r, map, acc, w, n);
-  return launch_status();
+  return launch_pdl_g(PDL_ELEM, gather_sub_kernel, grid, 256, 0, st, r, map, acc, w, n);
 }
 
 MCS_API int mcs_scatter(int n, const double* z, const int* map, double* out, void* stream) {
   if (n <= 0) return 0;
   auto st = static_cast<cudaStream_t>(stream);
   const int grid = (n + 255) / 256 < 4 * sm_count() ? (n + 255) / 256 : 4 * sm_count();
-  scatter_kernel<<<grid, 256, 0, st>>>(z, map, out, n);
-  return launch_status();
+  return launch_pdl_g(PDL_ELEM, scatter_kernel, grid, 256, 0, st, z, map, out, n);
 }

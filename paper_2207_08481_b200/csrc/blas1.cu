@@ -6,6 +6,8 @@
 // stopping test and negative-curvature check.  Reductions are deterministic:
 // a fixed grid, fixed per-thread strides, a fixed shuffle tree per block and
 // the last-arriving block summing the block partials in index order.
+#include <cstdlib>
+
 #include "common.cuh"
 
 namespace mcs {
@@ -56,6 +58,8 @@ __device__ __forceinline__ void finish(double part, double* partials, unsigned* 
 __global__ void __launch_bounds__(RED_THREADS)
     dot_kernel(int64_t n, const double* __restrict__ x, const double* __restrict__ y,
                double* partials, unsigned* counter, double* out) {
+  pdl_wait();
+  pdl_trigger();
   double s = 0.0;
   for (int64_t i = (int64_t)blockIdx.x * RED_THREADS + threadIdx.x; i < n;
        i += (int64_t)gridDim.x * RED_THREADS)
@@ -69,6 +73,8 @@ __global__ void __launch_bounds__(RED_THREADS)
     cg_update_kernel(int64_t n, double* __restrict__ x, double* __restrict__ r,
                      const double* __restrict__ p, const double* __restrict__ Ap, double* sc,
                      int rz, int pap, int rr, double* partials, unsigned* counter) {
+  pdl_wait();
+  pdl_trigger();
   const double alpha = sc[rz] / sc[pap];
   double s = 0.0;
   for (int64_t i = (int64_t)blockIdx.x * RED_THREADS + threadIdx.x; i < n;
@@ -85,6 +91,8 @@ __global__ void __launch_bounds__(RED_THREADS)
 // p = z + (sc[num]/sc[den]) p
 __global__ void xpby_kernel(int64_t n, const double* __restrict__ z, double* __restrict__ p,
                             const double* sc, int num, int den) {
+  pdl_wait();
+  pdl_trigger();
   const double beta = sc[num] / sc[den];
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
        i += (int64_t)gridDim.x * blockDim.x)
@@ -94,10 +102,28 @@ __global__ void xpby_kernel(int64_t n, const double* __restrict__ z, double* __r
 // y = a x + b y
 __global__ void axpby_kernel(int64_t n, double a, const double* __restrict__ x, double b,
                              double* __restrict__ y) {
+  pdl_wait();
+  pdl_trigger();
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
        i += (int64_t)gridDim.x * blockDim.x)
     y[i] = b == 0.0 ? a * x[i] : fma(a, x[i], b * y[i]);
 }
+
+static int grid_for(int64_t n);
+
+}  // namespace mcs
+
+bool mcs::pdl_enabled(int group) {
+  static int mask = -1;
+  if (mask < 0) {
+    const char* e = getenv("MCS_NO_PDL");
+    const char* m = getenv("MCS_PDL_MASK");
+    mask = (e && e[0] == '1') ? 0 : (m ? atoi(m) : 15);
+  }
+  return (mask & group) != 0;
+}
+
+namespace mcs {
 
 static int grid_for(int64_t n) {
   const int64_t g = (n + 255) / 256;
@@ -113,28 +139,24 @@ MCS_API int mcs_reduce_workspace_len() { return RED_BLOCKS; }
 MCS_API int mcs_dot(int64_t n, const double* x, const double* y, double* partials, unsigned* counter,
                     double* out, void* stream) {
   auto st = static_cast<cudaStream_t>(stream);
-  dot_kernel<<<RED_BLOCKS, RED_THREADS, 0, st>>>(n, x, y, partials, counter, out);
-  return launch_status();
+  return launch_pdl_g(PDL_BLAS, dot_kernel, RED_BLOCKS, RED_THREADS, 0, st, n, x, y, partials, counter, out);
 }
 
 MCS_API int mcs_cg_update(int64_t n, double* x, double* r, const double* p, const double* Ap, double* sc,
                           int rz, int pap, int rr, double* partials, unsigned* counter, void* stream) {
   auto st = static_cast<cudaStream_t>(stream);
-  cg_update_kernel<<<RED_BLOCKS, RED_THREADS, 0, st>>>(n, x, r, p, Ap, sc, rz, pap, rr, partials,
-                                                      counter);
-  return launch_status();
+  return launch_pdl_g(PDL_BLAS, cg_update_kernel, RED_BLOCKS, RED_THREADS, 0, st, n, x, r, p, Ap, sc, rz, pap,
+                    rr, partials, counter);
 }
 
 MCS_API int mcs_xpby(int64_t n, const double* z, double* p, const double* sc, int num, int den,
                      void* stream) {
   auto st = static_cast<cudaStream_t>(stream);
-  xpby_kernel<<<grid_for(n), 256, 0, st>>>(n, z, p, sc, num, den);
-  return launch_status();
+  return launch_pdl_g(PDL_BLAS, xpby_kernel, grid_for(n), 256, 0, st, n, z, p, sc, num, den);
 }
 
 MCS_API int mcs_axpby(int64_t n, double a, const double* x, double b, double* y, void* stream) {
   if (n <= 0) return 0;
   auto st = static_cast<cudaStream_t>(stream);
-  axpby_kernel<<<grid_for(n), 256, 0, st>>>(n, a, x, b, y);
-  return launch_status();
+  return launch_pdl_g(PDL_BLAS, axpby_kernel, grid_for(n), 256, 0, st, n, a, x, b, y);
 }

@@ -128,10 +128,20 @@ __global__ void __launch_bounds__(MF_THREADS)
     mf_forward(const int* __restrict__ level_nodes, const NodeRec* __restrict__ nodes,
                const double* __restrict__ mats, const int* __restrict__ src_t,
                const int* __restrict__ src_o, const int* __restrict__ perm,
-               const double* __restrict__ b, double* __restrict__ y, double* __restrict__ out,
-               int max_ns) {
+               const double* b, double* __restrict__ y, double* out, int max_ns) {
   extern __shared__ double sm[];
   const NodeRec nd = nodes[level_nodes[blockIdx.x]];
+  {   // static factors -> L2 while the previous level finishes
+    const char* c0 = reinterpret_cast<const char*>(mats + nd.oL);
+    const char* c1 = reinterpret_cast<const char*>(mats + nd.oW);
+    const int64_t n0 = 8 * nd.ns * (nd.ns + 1) / 2, n1 = 8 * nd.nb * nd.ns;
+    for (int64_t o = threadIdx.x * 128; o < n0; o += MF_THREADS * 128)
+      asm volatile("prefetch.global.L2 [%0];" ::"l"(c0 + o));
+    for (int64_t o = threadIdx.x * 128; o < n1; o += MF_THREADS * 128)
+      asm volatile("prefetch.global.L2 [%0];" ::"l"(c1 + o));
+  }
+  pdl_wait();
+  pdl_trigger();
   const int ns = (int)nd.ns, nb = (int)nd.nb;
   double* t = sm;
   double* ys = sm + max_ns;
@@ -141,7 +151,7 @@ __global__ void __launch_bounds__(MF_THREADS)
   for (int j = threadIdx.x; j < ns + nb; j += MF_THREADS) {
     if (j < ns) {
       const int64_t p = nd.s0 + j;
-      double v = __ldg(b + __ldg(perm + p));
+      double v = b[__ldg(perm + p)];
       const int a = __ldg(src_t + 2 * p), c = __ldg(src_t + 2 * p + 1);
       if (a >= 0) v -= out[a];
       if (c >= 0) v -= out[c];
@@ -184,10 +194,21 @@ __global__ void __launch_bounds__(MF_THREADS)
 __global__ void __launch_bounds__(MF_THREADS)
     mf_backward(const int* __restrict__ level_nodes, const NodeRec* __restrict__ nodes,
                 const double* __restrict__ mats, const int* __restrict__ B,
-                const int* __restrict__ perm, const double* __restrict__ y,
-                double* __restrict__ xp, double* __restrict__ x, int max_ns) {
+                const int* __restrict__ perm, const double* y,
+                double* xp, double* __restrict__ x, int max_ns) {
   extern __shared__ double sm[];
   const NodeRec nd = nodes[level_nodes[blockIdx.x]];
+  {   // static factors -> L2 while the previous level finishes
+    const char* c0 = reinterpret_cast<const char*>(mats + nd.oWT);
+    const char* c1 = reinterpret_cast<const char*>(mats + nd.oLT);
+    const int64_t n0 = 8 * nd.nb * nd.ns, n1 = 8 * nd.ns * (nd.ns + 1) / 2;
+    for (int64_t o = threadIdx.x * 128; o < n0; o += MF_THREADS * 128)
+      asm volatile("prefetch.global.L2 [%0];" ::"l"(c0 + o));
+    for (int64_t o = threadIdx.x * 128; o < n1; o += MF_THREADS * 128)
+      asm volatile("prefetch.global.L2 [%0];" ::"l"(c1 + o));
+  }
+  pdl_wait();
+  pdl_trigger();
   const int ns = (int)nd.ns, nb = (int)nd.nb;
   double* s = sm;
   double* xb = sm + 2 * max_ns;
@@ -203,7 +224,7 @@ __global__ void __launch_bounds__(MF_THREADS)
         lo = 0;
         hi = nb;
       },
-      [&](int r, double v) { s[r] = __ldg(y + nd.s0 + r) - v; });
+      [&](int r, double v) { s[r] = y[nd.s0 + r] - v; });
   __syncthreads();
   const double* LT = mats + nd.oLT;  // packed upper, row r holds columns r..ns-1
   node_rows(
@@ -231,9 +252,8 @@ MCS_API int mcs_mf_forward(int nnodes, const int* level_nodes, const void* nodes
   auto st = static_cast<cudaStream_t>(stream);
   const size_t smem = (2 * (size_t)max_ns + max_nb) * sizeof(double);
   cudaFuncSetAttribute(mf_forward, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-  mf_forward<<<nnodes, MF_THREADS, smem, st>>>(level_nodes, static_cast<const NodeRec*>(nodes),
-                                               mats, src_t, src_o, perm, b, y, out, max_ns);
-  return launch_status();
+  return launch_pdl_g(PDL_COARSE, mf_forward, nnodes, MF_THREADS, smem, st, level_nodes,
+                    static_cast<const NodeRec*>(nodes), mats, src_t, src_o, perm, b, y, out, max_ns);
 }
 
 MCS_API int mcs_mf_backward(int nnodes, const int* level_nodes, const void* nodes,
@@ -243,9 +263,8 @@ MCS_API int mcs_mf_backward(int nnodes, const int* level_nodes, const void* node
   auto st = static_cast<cudaStream_t>(stream);
   const size_t smem = (2 * (size_t)max_ns + max_nb) * sizeof(double);
   cudaFuncSetAttribute(mf_backward, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-  mf_backward<<<nnodes, MF_THREADS, smem, st>>>(level_nodes, static_cast<const NodeRec*>(nodes),
-                                                mats, B, perm, y, xp, x, max_ns);
-  return launch_status();
+  return launch_pdl_g(PDL_COARSE, mf_backward, nnodes, MF_THREADS, smem, st, level_nodes,
+                    static_cast<const NodeRec*>(nodes), mats, B, perm, y, xp, x, max_ns);
 }
 
 // ---- top of the separator tree: dense explicit inverse of its Schur complement
@@ -253,9 +272,11 @@ namespace mcs {
 
 // g[q] = b[perm[T[q]]] - sum_{p in src[ptr[q]..ptr[q+1])} out[p]   (fixed order)
 __global__ void mf_top_gather(int t, const int* __restrict__ T, const int* __restrict__ perm,
-                              const double* __restrict__ b, const int* __restrict__ ptr,
-                              const int* __restrict__ src, const double* __restrict__ out,
+                              const double* b, const int* __restrict__ ptr,
+                              const int* __restrict__ src, const double* out,
                               double* __restrict__ g) {
+  pdl_wait();
+  pdl_trigger();
   const int q = blockIdx.x * blockDim.x + threadIdx.x;
   if (q >= t) return;
   double v = b[perm[T[q]]];
@@ -264,15 +285,24 @@ __global__ void mf_top_gather(int t, const int* __restrict__ T, const int* __res
 }
 
 // x_T = Sinv g (dense t x t, warp per row), scattered to xp[T[q]] and x[perm[T[q]]]
-__global__ void mf_top_solve(int t, const double* __restrict__ Sinv, const double* __restrict__ g,
+__global__ void mf_top_solve(int t, const double* __restrict__ Sinv, const double* g,
                              const int* __restrict__ T, const int* __restrict__ perm,
                              double* __restrict__ xp, double* __restrict__ x) {
+  pdl_wait();
+  pdl_trigger();
   const int w = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
   if (w >= t) return;
   const double* row = Sinv + (int64_t)w * t;
-  double s = 0.0;
-  for (int j = lane; j < t; j += 32) s = fma(row[j], g[j], s);
-  s = warp_sum(s);
+  double s0 = 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0;
+  int j = lane;
+  for (; j + 96 < t; j += 128) {
+    s0 = fma(__ldg(row + j), g[j], s0);
+    s1 = fma(__ldg(row + j + 32), g[j + 32], s1);
+    s2 = fma(__ldg(row + j + 64), g[j + 64], s2);
+    s3 = fma(__ldg(row + j + 96), g[j + 96], s3);
+  }
+  for (; j < t; j += 32) s0 = fma(__ldg(row + j), g[j], s0);
+  const double s = warp_sum((s0 + s1) + (s2 + s3));
   if (lane == 0) {
     xp[T[w]] = s;
     x[perm[T[w]]] = s;
@@ -286,10 +316,9 @@ MCS_API int mcs_mf_top(int t, const int* T, const int* perm, const double* b, co
                        double* xp, double* x, void* stream) {
   if (t <= 0) return 0;
   auto st = static_cast<cudaStream_t>(stream);
-  mf_top_gather<<<(t + 127) / 128, 128, 0, st>>>(t, T, perm, b, ptr, src, out, g);
-  int rc = launch_status();
+  int rc = launch_pdl_g(PDL_COARSE, mf_top_gather, (t + 127) / 128, 128, 0, st, t, T, perm, b, ptr, src, out, g);
   if (rc) return rc;
   const int64_t threads = (int64_t)t * 32;
-  mf_top_solve<<<(int)((threads + 255) / 256), 256, 0, st>>>(t, Sinv, g, T, perm, xp, x);
-  return launch_status();
+  return launch_pdl_g(PDL_COARSE, mf_top_solve, (int)((threads + 255) / 256), 256, 0, st, t, Sinv, g, T, perm,
+                    xp, x);
 }

@@ -35,6 +35,43 @@ struct Sizes {
 
 inline int err_code(cudaError_t e) { return e == cudaSuccess ? 0 : -static_cast<int>(e); }
 
+// ---- programmatic dependent launch (PDL) for the PCG kernel chain --------
+// Kernels launched with launch_pdl_g() may start while their predecessor in
+// the stream is still running: each calls pdl_wait() before it reads anything
+// an earlier kernel wrote or writes any global memory, and pdl_trigger()
+// right after it (so at most one kernel waits ahead of the running one: a
+// trigger at kernel entry lets a cascade of waiting grids pin SM slots that
+// multi-wave predecessors still need).  Before pdl_wait()
+// only static data is touched (element matrices, index maps, factors), so
+// index loads, bulk copies and L2 prefetches overlap the predecessor's tail
+// and the launch latency.  Stream capture turns the attribute into
+// programmatic graph edges.  MCS_NO_PDL=1 launches normally.
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void pdl_trigger() {
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+}
+
+// kernel groups (MCS_PDL_MASK bit): 1 vector kernels, 2 element operators,
+// 4 smoother / SpMV, 8 coarse solve
+enum PdlGroup { PDL_BLAS = 1, PDL_ELEM = 2, PDL_PREC = 4, PDL_COARSE = 8 };
+bool pdl_enabled(int group);
+
+template <class... KArgs, class... Args>
+inline int launch_pdl_g(int group, void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem,
+                        cudaStream_t st, Args... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = pdl_enabled(group) ? 1 : 0;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  return err_code(cudaLaunchKernelEx(&cfg, kern, static_cast<KArgs>(args)...));
+}
+
 // Return the pending launch error (if any) as a negative code.
 inline int launch_status() { return err_code(cudaGetLastError()); }
 

@@ -79,18 +79,21 @@ __global__ void jacobi_setup_kernel(const double* __restrict__ Sd, int sd_stride
 template <int B>
 __global__ void __launch_bounds__(64)
     jacobi_apply_kernel(const double* __restrict__ binv, const int* __restrict__ bidx, int nblk,
-                        const double* __restrict__ r, double* __restrict__ x, double scale_inv) {
+                        const double* r, double* __restrict__ x, double scale_inv) {
   const int b = blockIdx.x * blockDim.x + threadIdx.x;
-  if (b >= nblk) return;
   constexpr int NP = B * (B + 1) / 2;
   int id[B];
   double rl[B], a[NP];
+  const int bb = b < nblk ? b : nblk - 1;
 #pragma unroll
-  for (int j = 0; j < B; ++j) id[j] = __ldg(bidx + (int64_t)j * nblk + b);
+  for (int j = 0; j < B; ++j) id[j] = __ldg(bidx + (int64_t)j * nblk + bb);
 #pragma unroll
-  for (int p = 0; p < NP; ++p) a[p] = __ldg(binv + (int64_t)p * nblk + b);
+  for (int p = 0; p < NP; ++p) a[p] = __ldg(binv + (int64_t)p * nblk + bb);
+  pdl_wait();   // the block inverses and indices are in flight; r may now be read
+  pdl_trigger();
+  if (b >= nblk) return;
 #pragma unroll
-  for (int j = 0; j < B; ++j) rl[j] = id[j] >= 0 ? __ldg(r + id[j]) : 0.0;
+  for (int j = 0; j < B; ++j) rl[j] = id[j] >= 0 ? r[id[j]] : 0.0;
 #pragma unroll
   for (int i = 0; i < B; ++i) {
     double s = 0.0;
@@ -102,8 +105,10 @@ __global__ void __launch_bounds__(64)
 
 template <int LANES>
 __global__ void csr_spmv_kernel(int nrows, const int* __restrict__ ptr, const int* __restrict__ col,
-                                const double* __restrict__ val, const double* __restrict__ x,
+                                const double* __restrict__ val, const double* x,
                                 double* __restrict__ y, double alpha, double beta) {
+  pdl_wait();
+  pdl_trigger();
   const int tid = blockIdx.x * blockDim.x + threadIdx.x;
   const int row = tid / LANES, sub = tid % LANES;
   double s = 0.0;
@@ -142,11 +147,11 @@ MCS_API int mcs_jacobi_apply(int k, int nblk, const double* binv, const int* bid
   auto st = static_cast<cudaStream_t>(stream);
   const int grid = (nblk + 63) / 64;
   switch (k) {
-    case 2: jacobi_apply_kernel<5><<<grid, 64, 0, st>>>(binv, bidx, nblk, r, x, scale_inv); break;
-    case 3: jacobi_apply_kernel<7><<<grid, 64, 0, st>>>(binv, bidx, nblk, r, x, scale_inv); break;
-    case 4: jacobi_apply_kernel<9><<<grid, 64, 0, st>>>(binv, bidx, nblk, r, x, scale_inv); break;
-    case 5: jacobi_apply_kernel<11><<<grid, 64, 0, st>>>(binv, bidx, nblk, r, x, scale_inv); break;
-    case 6: jacobi_apply_kernel<13><<<grid, 64, 0, st>>>(binv, bidx, nblk, r, x, scale_inv); break;
+    case 2: return launch_pdl_g(PDL_PREC, jacobi_apply_kernel<5>, grid, 64, 0, st, binv, bidx, nblk, r, x, scale_inv);
+    case 3: return launch_pdl_g(PDL_PREC, jacobi_apply_kernel<7>, grid, 64, 0, st, binv, bidx, nblk, r, x, scale_inv);
+    case 4: return launch_pdl_g(PDL_PREC, jacobi_apply_kernel<9>, grid, 64, 0, st, binv, bidx, nblk, r, x, scale_inv);
+    case 5: return launch_pdl_g(PDL_PREC, jacobi_apply_kernel<11>, grid, 64, 0, st, binv, bidx, nblk, r, x, scale_inv);
+    case 6: return launch_pdl_g(PDL_PREC, jacobi_apply_kernel<13>, grid, 64, 0, st, binv, bidx, nblk, r, x, scale_inv);
     default: return -1000;
   }
   return launch_status();
@@ -159,18 +164,20 @@ MCS_API int mcs_csr_spmv(int nrows, const int* ptr, const int* col, const double
   const int64_t threads = (int64_t)nrows * lanes;
   const int grid = (int)((threads + 255) / 256);
   switch (lanes) {
-    case 1: csr_spmv_kernel<1><<<grid, 256, 0, st>>>(nrows, ptr, col, val, x, y, alpha, beta); break;
-    case 4: csr_spmv_kernel<4><<<grid, 256, 0, st>>>(nrows, ptr, col, val, x, y, alpha, beta); break;
-    case 8: csr_spmv_kernel<8><<<grid, 256, 0, st>>>(nrows, ptr, col, val, x, y, alpha, beta); break;
-    case 32: csr_spmv_kernel<32><<<grid, 256, 0, st>>>(nrows, ptr, col, val, x, y, alpha, beta); break;
+    case 1: return launch_pdl_g(PDL_PREC, csr_spmv_kernel<1>, grid, 256, 0, st, nrows, ptr, col, val, x, y, alpha, beta);
+    case 4: return launch_pdl_g(PDL_PREC, csr_spmv_kernel<4>, grid, 256, 0, st, nrows, ptr, col, val, x, y, alpha, beta);
+    case 8: return launch_pdl_g(PDL_PREC, csr_spmv_kernel<8>, grid, 256, 0, st, nrows, ptr, col, val, x, y, alpha, beta);
+    case 32: return launch_pdl_g(PDL_PREC, csr_spmv_kernel<32>, grid, 256, 0, st, nrows, ptr, col, val, x, y, alpha, beta);
     default: return -1000;
   }
   return launch_status();
 }
 
 // y = A x for a dense row-major n x n matrix (small exact coarse solves); warp per row
-__global__ void dense_gemv_kernel(int n, const double* __restrict__ A, const double* __restrict__ x,
+__global__ void dense_gemv_kernel(int n, const double* __restrict__ A, const double* x,
                                   double* __restrict__ y) {
+  pdl_wait();
+  pdl_trigger();
   const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
   if (warp >= n) return;
   const double* row = A + (int64_t)warp * n;
@@ -185,6 +192,5 @@ MCS_API int mcs_dense_gemv(int n, const double* A, const double* x, double* y, v
   if (n <= 0) return 0;
   auto st = static_cast<cudaStream_t>(stream);
   const int64_t threads = (int64_t)n * 32;
-  dense_gemv_kernel<<<(int)((threads + 255) / 256), 256, 0, st>>>(n, A, x, y);
-  return launch_status();
+  return launch_pdl_g(PDL_PREC, dense_gemv_kernel, (int)((threads + 255) / 256), 256, 0, st, n, A, x, y);
 }
