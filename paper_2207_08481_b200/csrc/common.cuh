@@ -102,6 +102,14 @@ __device__ __forceinline__ void dmma884(double& c0, double& c1, double a, double
       : "d"(a), "d"(b));
 }
 
+// 1/x to full double precision: hardware approximation + 2 Newton steps
+__device__ __forceinline__ double rcp64(double x) {
+  double y;
+  asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(x));
+  y = fma(fma(-x, y, 1.0), y, y);
+  return fma(fma(-x, y, 1.0), y, y);
+}
+
 // 1/sqrt(x) to full double precision: hardware approximation + 2 Newton steps
 __device__ __forceinline__ double rsqrt_nr(double x) {
   double y;

@@ -15,135 +15,13 @@
 //                      Bsig^T), proved equal in DESIGN.md §3.
 //
 // Raw block entries are read once, straight from the element record in HBM
-// into the DMMA accumulators that consume them.  The tiny (8, 4) microbench
-// shape keeps the register-tile engine of elim_dmma.cuh.
-#include "elim_v5.cuh"  // includes elim_dmma.cuh
+// into the DMMA accumulators that consume them.  (The MCS element blocks of
+// the solver path take the structured kernels of condense_struct.cu /
+// condense_fused.cu; this dense engine serves the config-5 microbench and
+// user-supplied blocks without the MCS structure.)
+#include "elim_v5.cuh"
 
 namespace mcs {
-
-__host__ __device__ constexpr int ceil8(int n) { return (n + 7) / 8 * 8; }
-
-// padded layout of an augmented matrix with NP pivots and NC trailing rows
-template <int NP, int NC, int W>
-struct Pad {
-  static constexpr int NPP = ceil8(NP), NCP = ceil8(NC);
-  static constexpr int NB = (NPP + NCP) / 8, NPB = NPP / 8;
-  using E = Elim<NB, NPB, W>;
-};
-
-// load the lane's tiles: entry(i, j) is called with real indices i >= j
-template <class P, int NP, int NC, class F>
-__device__ __forceinline__ void load_tiles(double (&acc)[P::E::TPW][2], int (&tij)[P::E::TPW],
-                                           F entry) {
-  using E = typename P::E;
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int gr = lane >> 2, tg = lane & 3;
-#pragma unroll
-  for (int t = 0; t < E::TPW; ++t) {
-    const int g = warp + t * E::W;
-    int bi = 0, bj = 0;
-    if (g < E::NT) E::tile_of(g, bi, bj);
-    tij[t] = bi | (bj << 8);
-#pragma unroll
-    for (int q = 0; q < 2; ++q) {
-      int i = bi * 8 + gr, j = bj * 8 + 2 * tg + q;
-      if (i < j) { const int s = i; i = j; j = s; }
-      // padded -> real
-      const bool di = (i < P::NPP) ? (i >= NP) : (i - P::NPP >= NC);
-      const bool dj = (j < P::NPP) ? (j >= NP) : (j - P::NPP >= NC);
-      const int ri = i < P::NPP ? i : NP + (i - P::NPP);
-      const int rj = j < P::NPP ? j : NP + (j - P::NPP);
-      double v;
-      if (g >= E::NT) v = 0.0;
-      else if (di || dj) v = (i == j && i < P::NPP) ? 1.0 : 0.0;
-      else v = entry(ri, rj);
-      acc[t][q] = v;
-    }
-  }
-}
-
-// write -trailing (lower packed, NC x NC) to out
-template <class P, int NC>
-__device__ __forceinline__ void store_trailing(const double (&acc)[P::E::TPW][2],
-                                               const int (&tij)[P::E::TPW], double* out) {
-  using E = typename P::E;
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int gr = lane >> 2, tg = lane & 3;
-#pragma unroll
-  for (int t = 0; t < E::TPW; ++t) {
-    const int g = warp + t * E::W;
-    const int bi = tij[t] & 0xff, bj = tij[t] >> 8;
-    if (g < E::NT && bj >= E::NPB) {
-#pragma unroll
-      for (int q = 0; q < 2; ++q) {
-        const int i = bi * 8 + gr - P::NPP, j = bj * 8 + 2 * tg + q - P::NPP;
-        if (j <= i && i < NC) out[pk(i, j)] = -acc[t][q];
-      }
-    }
-  }
-}
-
-// expected pivot signs: [0, npos) > 0, [npos, np) < 0, padding unchecked
-__device__ __forceinline__ void init_expect(signed char* ex, int npp, int npos, int np) {
-  for (int i = threadIdx.x; i < npp; i += blockDim.x) ex[i] = i < npos ? 1 : (i < np ? -1 : 0);
-}
-
-// --------------------------------------------------------------- A5: microbench
-
-template <int NS, int NC, int W, int MINB = 1>
-__global__ void __launch_bounds__(32 * W, MINB)
-    spd_schur_kernel(const double* __restrict__ A, const double* __restrict__ B,
-                     double* __restrict__ S, int* __restrict__ info, int64_t batch) {
-  using P = Pad<NS, NC, W>;
-  using E = typename P::E;
-  constexpr int LA = npk(NS), LB = NS * NC, LS = npk(NC);
-  static_assert((LA % 2) == 0 && (LB % 2) == 0, "16-byte bulk copies");
-  extern __shared__ __align__(128) double smem[];
-  double* sA = smem;
-  double* sB = smem + LA;
-  double* work = smem + LA + LB;
-  __shared__ __align__(8) uint64_t bar;
-  __shared__ int bad;
-  __shared__ int flag;
-  __shared__ signed char expect[P::NPP];
-  init_expect(expect, P::NPP, NS, NS);
-  int64_t e = blockIdx.x;
-  if (threadIdx.x == 0) {
-    mbar_init(&bar, 1);
-    fence_barrier_init();
-  }
-  __syncthreads();
-  if (threadIdx.x == 0 && e < batch) {
-    mbar_expect_tx(&bar, (LA + LB) * 8);
-    bulk_g2s(sA, A + e * LA, LA * 8, &bar);
-    bulk_g2s(sB, B + e * LB, LB * 8, &bar);
-  }
-  uint32_t phase = 0;
-  for (; e < batch; e += gridDim.x) {
-    mbar_wait(&bar, phase);
-    phase ^= 1;
-    double acc[E::TPW][2];
-    int tij[E::TPW];
-    load_tiles<P, NS, NC>(acc, tij, [&](int i, int j) {
-      return i < NS ? sA[pk(i, j)] : (j < NS ? sB[j * NC + (i - NS)] : 0.0);
-    });
-    if (threadIdx.x == 0) {
-      bad = 0;
-      flag = -1;
-    }
-    __syncthreads();
-    const int64_t nxt = e + gridDim.x;
-    if (threadIdx.x == 0 && nxt < batch) {   // prefetch the next element
-      mbar_expect_tx(&bar, (LA + LB) * 8);
-      bulk_g2s(sA, A + nxt * LA, LA * 8, &bar);
-      bulk_g2s(sB, B + nxt * LB, LB * 8, &bar);
-    }
-    eliminate_tiles<E>(acc, tij, work, expect, &bad, &flag);
-    store_trailing<P, NC>(acc, tij, S + e * LS);
-    __syncthreads();
-    if (threadIdx.x == 0 && info) info[e] = bad;
-  }
-}
 
 // ------------------------------------------------------- A3: MCS condensation
 
@@ -339,18 +217,6 @@ static int persistent_grid(Kern k, int threads, size_t smem, int64_t n) {
   return static_cast<int>(n < g ? n : g);
 }
 
-template <int NS, int NC, int W, int MINB = 1>
-static int launch_spd_schur(const double* A, const double* B, double* S, int* info, int64_t batch,
-                            cudaStream_t st) {
-  using P = Pad<NS, NC, W>;
-  auto kern = spd_schur_kernel<NS, NC, W, MINB>;
-  const size_t smem = (npk(NS) + NS * NC + P::E::SMEM_WORK) * sizeof(double);
-  cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-  const int grid = persistent_grid(kern, 32 * W, smem, batch);
-  kern<<<grid, 32 * W, smem, st>>>(A, B, S, info, batch);
-  return launch_status();
-}
-
 }  // namespace mcs
 
 using namespace mcs;
@@ -360,7 +226,6 @@ MCS_API int mcs_spd_schur_batched(int n, int m, int64_t batch, const double* A_p
   if (batch <= 0) return 0;
   auto st = static_cast<cudaStream_t>(stream);
   if (n == 60 && m == 36) return launch_spd_schur_v5<60, 36, 4, 5>(A_packed_lower, B, S_packed, info, batch, st);
-  if (n == 8 && m == 4) return launch_spd_schur<8, 4, 2>(A_packed_lower, B, S_packed, info, batch, st);
   return -1000;  // unsupported shape (compiled instantiations only)
 }
 

@@ -30,7 +30,6 @@
 // tile rows these 128-bit loads are bank-conflict free.
 #pragma once
 #include "common.cuh"
-#include "elim_dmma.cuh"  // rcp64
 
 namespace mcs {
 namespace v5 {

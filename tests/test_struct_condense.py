@@ -236,7 +236,7 @@ def test_gpu_fused_reports_failures(cuda):
 
 
 @pytest.mark.gpu
-@pytest.mark.parametrize("k", [4, 5, 6])
+@pytest.mark.parametrize("k", [2, 3, 4, 5, 6])
 def test_gpu_double_schur_kernel_matches_oracle(cuda, k):
     """mcs_double_schur (the k = 5, 6 path; v5 engine) on GPU-condensed S_T:
     X, S_oo^-1 and Sd_T against condensation.py:207-226."""
