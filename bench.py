@@ -365,7 +365,8 @@ def run_ours(args, rank, world):
         f_kern = (z_["nloc"] * (z_["nloc"] + 1) * ny_ + z_["nloc"] * (12 * (k * (k + 1) // 2)
                   + 3 * k * (3 * k + 1)))
     achieved = f_kern * nt / (t_kern * 1e-3) / 1e12
-    roofline = {"bound": "fp64", "kernel": kname, "achieved": achieved,
+    roofline = {"bound": "tensor", "pipe": "FP64 tensor cores (DMMA m8n8k4) + FP64 FMA",
+                "kernel": kname, "achieved": achieved,
                 "peak": peaks["fp64_tflops"], "unit": "TFLOP/s",
                 "frac": achieved / peaks["fp64_tflops"] if peaks["fp64_tflops"] else None,
                 "flops_per_element": f_kern,
