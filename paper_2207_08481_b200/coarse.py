@@ -28,6 +28,8 @@ from __future__ import annotations
 from dataclasses import dataclass, field
 from typing import List
 
+import os
+
 import numpy as np
 import scipy.linalg as sla
 import scipy.sparse as sp
@@ -36,7 +38,7 @@ from . import _abi, engine
 
 DENSE_MAX = 1024
 LEAF = 96
-TOP_MAX = 4096      # dofs of the separator-tree top handled by a dense inverse
+TOP_MAX = int(os.environ.get("MCS_TOP_MAX", "4096"))   # dense-inverse top (A/B in PCG: 4096 > 2048)
 
 
 @dataclass
