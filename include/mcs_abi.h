@@ -94,16 +94,23 @@ int mcs_spd_schur_batched(int n, int m, int64_t batch, const double* A_packed_lo
  *      y (length ny) is overwritten. */
 int mcs_apply_elem(int k, int which, int64_t nt, const double* M_packed, const int* codes,
                    const double* x, double* y, int64_t ny, void* stream);
+/* the same apply fused with the CG curvature: *out = x . y =
+ * sum_T x_T^T M_T x_T (fixed-order reduction over partials[grid] with the
+ * last-block counter; partials: >= 8 * number of SMs doubles) */
+int mcs_apply_elem_dot(int k, int which, int64_t nt, const double* M_packed, const int* codes,
+                       const double* x, double* y, int64_t ny, double* partials,
+                       unsigned* counter, double* out, void* stream);
 
 /* ---- ExtendedAsp outer factors (replaces preconditioners.py:353-378):
  *      restrict: bubble[e] = S_oo^-1 r_o, acc = sum X^T r_o (signed; acc
- *      overwritten, length nacc); prolong: out[bubble dofs] = bubble - X z_c. */
+ *      overwritten, length nacc); prolong: out[bubble dofs] = bubble - X z_c and
+ *      out[c2v[j]] = z_c[j] for the coupling dofs (the scatter, fused). */
 int mcs_ext_restrict(int k, int64_t nt, const double* ext, const int* bubble_idx,
                      const int* cpl_codes, const double* r, double* bubble, double* acc,
                      int64_t nacc, void* stream);
 int mcs_ext_prolong(int k, int64_t nt, const double* ext, const int* bubble_idx,
-                    const int* cpl_codes, const double* zc, const double* bubble, double* out,
-                    void* stream);
+                    const int* cpl_codes, const double* zc, const double* bubble, const int* c2v,
+                    double* out, void* stream);
 /* w[j] = r[map[j]] - acc[j];  out[map[j]] = z[j] */
 int mcs_gather_sub(int n, const double* r, const int* map, const double* acc, double* w,
                    void* stream);

@@ -46,8 +46,9 @@ SIGNATURES = {
     "mcs_double_schur": [_i, _l, _p, _p, _p, _p, _p],
     # apply.cu
     "mcs_apply_elem": [_i, _i, _l, _p, _p, _p, _p, _l, _p],
+    "mcs_apply_elem_dot": [_i, _i, _l, _p, _p, _p, _p, _l, _p, _p, _p, _p],
     "mcs_ext_restrict": [_i, _l, _p, _p, _p, _p, _p, _p, _l, _p],
-    "mcs_ext_prolong": [_i, _l, _p, _p, _p, _p, _p, _p, _p],
+    "mcs_ext_prolong": [_i, _l, _p, _p, _p, _p, _p, _p, _p, _p],
     "mcs_gather_sub": [_i, _p, _p, _p, _p, _p],
     "mcs_scatter": [_i, _p, _p, _p, _p],
     # precond.cu

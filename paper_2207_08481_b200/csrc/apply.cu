@@ -39,7 +39,9 @@ __device__ __forceinline__ double gather_signed(const double* x, int c) {
 template <int N, int STRIDE, int W, int NST>
 __global__ void __launch_bounds__(W * 32)
     elem_apply_kernel(const double* __restrict__ M, const int* __restrict__ codes,
-                      const double* x, double* __restrict__ y, int64_t nt) {
+                      const double* x, double* __restrict__ y, int64_t nt,
+                      double* __restrict__ dpart, unsigned* __restrict__ dcount,
+                      double* __restrict__ dout) {
   constexpr int R = (N + 31) / 32;
   extern __shared__ __align__(128) double sm[];
   __shared__ __align__(8) uint64_t bars[W][NST];
@@ -78,6 +80,7 @@ __global__ void __launch_bounds__(W * 32)
 #pragma unroll
   for (int r = 0; r < R; ++r) xv[r] = gather_signed(x, cd0[r]);
   int it = 0;
+  double energy = 0.0;
   for (int64_t e = gw; e < nt; e += nw, ++it) {
     const int s = it % NST;
 #pragma unroll
@@ -128,6 +131,34 @@ __global__ void __launch_bounds__(W * 32)
     for (int r = 0; r < R; ++r) {
       const int i = lane + 32 * r;
       if (i < N && cd[r] >= 0) atomicAdd(&y[code_index(cd[r])], code_sign(cd[r]) * acc[r]);
+      if (i < N) energy = fma(acc[r], xs[warp][i], energy);
+    }
+  }
+  if (dout) {   // x . (A x) = sum_T x_T^T S_T x_T, fixed-order reduction
+    __shared__ double wsum[W];
+    __shared__ bool last;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) energy += __shfl_xor_sync(0xffffffffu, energy, o);
+    if (lane == 0) wsum[warp] = energy;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      double b = 0.0;
+      for (int w = 0; w < W; ++w) b += wsum[w];
+      dpart[blockIdx.x] = b;
+      __threadfence();
+      last = atomicAdd(dcount, 1u) == gridDim.x - 1;
+    }
+    __syncthreads();
+    if (last && warp == 0) {
+      __threadfence();
+      double t = 0.0;
+      for (int b = lane; b < (int)gridDim.x; b += 32) t += __ldcg(dpart + b);
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) t += __shfl_xor_sync(0xffffffffu, t, o);
+      if (lane == 0) {
+        *dout = t;
+        *dcount = 0u;
+      }
     }
   }
 }
@@ -258,7 +289,8 @@ template <int K, int LEN, int W, int NST>
 __global__ void __launch_bounds__(W * 32)
     ext_prolong_kernel(const double* __restrict__ ext, const int* __restrict__ bidx,
                        const int* __restrict__ ccodes, const double* zc,
-                       const double* bubble, double* __restrict__ out, int64_t nt) {
+                       const double* bubble, const int* __restrict__ c2v,
+                       double* __restrict__ out, int64_t nt) {
   using Z = Sizes<K>;
   constexpr int NI = Z::n_int, NC = Z::ncpl, XL = NI * NC;
   constexpr int XLE = even(XL);
@@ -285,21 +317,18 @@ __global__ void __launch_bounds__(W * 32)
       }
     }
   }
-  int c1[RC];
+  int c0[RC], c1[RC];
   double zv[RC];
 #pragma unroll
   for (int q = 0; q < RC; ++q) {
     const int c = lane + 32 * q;
-    zv[q] = (double)((c < NC && gw < nt) ? __ldg(ccodes + gw * NC + c) : -1);
+    c0[q] = (c < NC && gw < nt) ? __ldg(ccodes + gw * NC + c) : -1;
     c1[q] = (c < NC && gw + nw < nt) ? __ldg(ccodes + (gw + nw) * NC + c) : -1;
   }
   pdl_wait();
   pdl_trigger();
 #pragma unroll
-  for (int q = 0; q < RC; ++q) {
-    const int c0 = (int)zv[q];
-    zv[q] = gather_signed(zc, c0);
-  }
+  for (int q = 0; q < RC; ++q) zv[q] = gather_signed(zc, c0[q]);
   int it = 0;
   for (int64_t e = gw; e < nt; e += nw, ++it) {
     const int s = it % NST;
@@ -307,12 +336,16 @@ __global__ void __launch_bounds__(W * 32)
     for (int q = 0; q < RC; ++q) {
       const int c = lane + 32 * q;
       if (c < NC) zl[warp][c] = zv[q];
+      // the coupling part of out = z_c (the ExtendedAsp scatter, fused):
+      // a dof shared by two elements receives the same value twice
+      if (c0[q] >= 0) out[__ldg(c2v + code_index(c0[q]))] = code_sign(c0[q]) * zv[q];
     }
     const int64_t e2 = e + 2 * nw;
 #pragma unroll
     for (int q = 0; q < RC; ++q) {
       const int c = lane + 32 * q;
       zv[q] = gather_signed(zc, c1[q]);
+      c0[q] = c1[q];
       c1[q] = (c < NC && e2 < nt) ? __ldg(ccodes + e2 * NC + c) : -1;
     }
     double bub[RI];
@@ -389,7 +422,7 @@ static int warp_grid(Kern k, size_t smem, int64_t nt) {
 
 template <int N, int STRIDE>
 static int launch_apply(const double* M, const int* codes, const double* x, double* y, int64_t nt,
-                        cudaStream_t st) {
+                        double* dpart, unsigned* dcount, double* dout, cudaStream_t st) {
   // one bulk stage per warp when a stage is large (k = 5, 6), two otherwise;
   // aim for ~64-96 KB of bulk copies in flight per SM
   // measured on B200 (tools/apply_variants.cu): warps in flight matter more
@@ -405,7 +438,8 @@ static int launch_apply(const double* M, const int* codes, const double* x, doub
   if (per_sm < 1) per_sm = 1;
   const int64_t want = (nt + W - 1) / W;
   const int64_t g = (int64_t)per_sm * sm_count();
-  return launch_pdl_g(PDL_ELEM, kern, (int)(want < g ? want : g), W * 32, smem, st, M, codes, x, y, nt);
+  return launch_pdl_g(PDL_ELEM, kern, (int)(want < g ? want : g), W * 32, smem, st, M, codes, x, y, nt,
+                      dpart, dcount, dout);
 }
 
 template <int K>
@@ -432,7 +466,8 @@ static int launch_restrict(const double* ext, const int* bidx, const int* cc, co
 
 template <int K>
 static int launch_prolong(const double* ext, const int* bidx, const int* cc, const double* zc,
-                          const double* bubble, double* out, int64_t nt, cudaStream_t st) {
+                          const double* bubble, const int* c2v, double* out, int64_t nt,
+                          cudaStream_t st) {
   constexpr int LEN = ExtLen<K>::len;
   using Z = Sizes<K>;
   constexpr int XLE = even(Z::n_int * Z::ncpl);
@@ -445,24 +480,26 @@ static int launch_prolong(const double* ext, const int* bidx, const int* cc, con
   if (per_sm < 1) per_sm = 1;
   const int64_t want = (nt + W - 1) / W, g = (int64_t)per_sm * sm_count();
   return launch_pdl_g(PDL_ELEM, kern, (int)(want < g ? want : g), W * 32, smem, st, ext, bidx, cc, zc, bubble,
-                    out, nt);
+                    c2v, out, nt);
 }
 
 }  // namespace mcs
 
 using namespace mcs;
 
-// which = 0: S (nloc, stride st_stride);  which = 1: S_d (ncpl, stride sd_stride)
-MCS_API int mcs_apply_elem(int k, int which, int64_t nt, const double* M_packed, const int* codes,
-                           const double* x, double* y, int64_t ny, void* stream) {
-  auto st = static_cast<cudaStream_t>(stream);
+static int apply_elem(int k, int which, int64_t nt, const double* M_packed, const int* codes,
+                      const double* x, double* y, int64_t ny, double* dpart, unsigned* dcount,
+                      double* dout, cudaStream_t st) {
   int rc = err_code(cudaMemsetAsync(y, 0, ny * sizeof(double), st));
   if (rc || nt <= 0) return rc;
-#define MCS_APPLY_CASE(KK)                                                                 \
-  case KK: {                                                                               \
-    using Z = Sizes<KK>;                                                                   \
-    if (which == 0) return launch_apply<Z::nloc, even(npk(Z::nloc))>(M_packed, codes, x, y, nt, st); \
-    return launch_apply<Z::ncpl, even(npk(Z::ncpl))>(M_packed, codes, x, y, nt, st);      \
+#define MCS_APPLY_CASE(KK)                                                                  \
+  case KK: {                                                                                \
+    using Z = Sizes<KK>;                                                                    \
+    if (which == 0)                                                                         \
+      return launch_apply<Z::nloc, even(npk(Z::nloc))>(M_packed, codes, x, y, nt, dpart,    \
+                                                       dcount, dout, st);                   \
+    return launch_apply<Z::ncpl, even(npk(Z::ncpl))>(M_packed, codes, x, y, nt, dpart,      \
+                                                     dcount, dout, st);                     \
   }
   switch (k) {
     MCS_APPLY_CASE(2)
@@ -473,6 +510,21 @@ MCS_API int mcs_apply_elem(int k, int which, int64_t nt, const double* M_packed,
   }
 #undef MCS_APPLY_CASE
   return -1000;
+}
+
+// which = 0: S (nloc, stride st_stride);  which = 1: S_d (ncpl, stride sd_stride)
+MCS_API int mcs_apply_elem(int k, int which, int64_t nt, const double* M_packed, const int* codes,
+                           const double* x, double* y, int64_t ny, void* stream) {
+  return apply_elem(k, which, nt, M_packed, codes, x, y, ny, nullptr, nullptr, nullptr,
+                    static_cast<cudaStream_t>(stream));
+}
+
+// the same apply, plus *out = x . y = sum_T x_T^T M_T x_T (deterministic)
+MCS_API int mcs_apply_elem_dot(int k, int which, int64_t nt, const double* M_packed,
+                               const int* codes, const double* x, double* y, int64_t ny,
+                               double* partials, unsigned* counter, double* out, void* stream) {
+  return apply_elem(k, which, nt, M_packed, codes, x, y, ny, partials, counter, out,
+                    static_cast<cudaStream_t>(stream));
 }
 
 MCS_API int mcs_ext_restrict(int k, int64_t nt, const double* ext, const int* bidx, const int* ccodes,
@@ -492,15 +544,16 @@ MCS_API int mcs_ext_restrict(int k, int64_t nt, const double* ext, const int* bi
 }
 
 MCS_API int mcs_ext_prolong(int k, int64_t nt, const double* ext, const int* bidx, const int* ccodes,
-                            const double* zc, const double* bubble, double* out, void* stream) {
+                            const double* zc, const double* bubble, const int* c2v, double* out,
+                            void* stream) {
   auto st = static_cast<cudaStream_t>(stream);
   if (nt <= 0) return 0;
   switch (k) {
-    case 2: return launch_prolong<2>(ext, bidx, ccodes, zc, bubble, out, nt, st);
-    case 3: return launch_prolong<3>(ext, bidx, ccodes, zc, bubble, out, nt, st);
-    case 4: return launch_prolong<4>(ext, bidx, ccodes, zc, bubble, out, nt, st);
-    case 5: return launch_prolong<5>(ext, bidx, ccodes, zc, bubble, out, nt, st);
-    case 6: return launch_prolong<6>(ext, bidx, ccodes, zc, bubble, out, nt, st);
+    case 2: return launch_prolong<2>(ext, bidx, ccodes, zc, bubble, c2v, out, nt, st);
+    case 3: return launch_prolong<3>(ext, bidx, ccodes, zc, bubble, c2v, out, nt, st);
+    case 4: return launch_prolong<4>(ext, bidx, ccodes, zc, bubble, c2v, out, nt, st);
+    case 5: return launch_prolong<5>(ext, bidx, ccodes, zc, bubble, c2v, out, nt, st);
+    case 6: return launch_prolong<6>(ext, bidx, ccodes, zc, bubble, c2v, out, nt, st);
   }
   return -1000;
 }

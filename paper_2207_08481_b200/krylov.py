@@ -69,8 +69,11 @@ class _PcgState:
     def step(self, rz, rz_new):
         ws = workspace()
         st = _abi.stream()
-        _apply(self.A, self.p, self.Ap)
-        ws.dot(self.p, self.Ap, ws.PAP)
+        if hasattr(self.A, "apply_dot"):      # p'Ap accumulated inside the apply kernel
+            self.A.apply_dot(self.p, self.Ap, ws.PAP)
+        else:
+            _apply(self.A, self.p, self.Ap)
+            ws.dot(self.p, self.Ap, ws.PAP)
         _abi.call("mcs_cg_update", self.n, _abi.ptr(self.x), _abi.ptr(self.r), _abi.ptr(self.p),
                   _abi.ptr(self.Ap), _abi.ptr(ws.sc), rz, ws.PAP, ws.RR, _abi.ptr(ws.partials),
                   _abi.ptr(ws.counter), st)

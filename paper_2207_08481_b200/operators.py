@@ -90,6 +90,16 @@ class _ElemOperator:
 
     __call__ = apply
 
+    def apply_dot(self, x, out, slot, stream=None):
+        """out = A x and workspace scalar `slot` = x . (A x), accumulated
+        element by element inside the apply kernel (no separate dot pass)."""
+        ws = workspace()
+        _abi.call("mcs_apply_elem_dot", self.k, self.which, self.nt, _abi.ptr(self.M),
+                  _abi.ptr(self.codes), _abi.ptr(x), _abi.ptr(out), self.n,
+                  _abi.ptr(ws.partials), _abi.ptr(ws.counter), ws.sc.data_ptr() + 8 * slot,
+                  _abi.stream(stream))
+        return out
+
     def __matmul__(self, x):
         return self.apply(x)
 

@@ -364,10 +364,10 @@ class ExtendedAsp:
         _abi.call("mcs_gather_sub", self.nc, _abi.ptr(rd), _abi.ptr(m["c2v"]),
                   _abi.ptr(self.acc), _abi.ptr(self.wc), st)
         self.inner.apply(self.wc, out=self.zc)
-        _abi.call("mcs_scatter", self.nc, _abi.ptr(self.zc), _abi.ptr(m["c2v"]), _abi.ptr(out), st)
+        # bubble dofs = bubble - X z_c, coupling dofs = z_c (scatter fused in)
         _abi.call("mcs_ext_prolong", s.k, self.nt, _abi.ptr(s.ext_dev), _abi.ptr(m["bubble_idx"]),
                   _abi.ptr(m["cpl_codes"]), _abi.ptr(self.zc), _abi.ptr(self.bubble),
-                  _abi.ptr(out), st)
+                  _abi.ptr(m["c2v"]), _abi.ptr(out), st)
         return out.cpu().numpy() if host else out
 
     __call__ = apply
