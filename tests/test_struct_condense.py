@@ -266,3 +266,34 @@ def test_gpu_double_schur_kernel_matches_oracle(cuda, k):
         Sinv = engine.unpack_sym(E[t, ni * nc:ni * nc + ni * (ni + 1) // 2], ni)
         assert rel(Sinv, np.linalg.inv(Soo)) <= 1e-10
         assert rel(Sd_got[t], Sd_ref) <= 1e-10
+
+
+@pytest.mark.gpu
+def test_gpu_condensation_edge_cases(cuda):
+    """Empty batches are no-ops (return 0, touch nothing); a single element
+    and a batch that is not a multiple of the warps per CTA condense like
+    the full mesh; the fused kernel is bitwise deterministic run to run."""
+    import torch
+    prob, fes = _setup(2, 3)
+    k = prob.k
+    refs = refblocks.build_refs(fes)
+    W = refblocks.element_weights(fes, prob.nu)
+    tab = engine.to_dev(engine.fused_tables(refs)[0])
+    Wd = engine.to_dev(W)
+    # empty batch
+    ST, ext, Sd, info = engine.condense_fused(k, 0, Wd, tab)
+    assert ST.shape[0] == 0 and info.shape[0] == 0
+    # full mesh reference
+    ST_all, ext_all, Sd_all, _ = engine.condense_fused(k, len(W), Wd, tab)
+    z = refblocks.local_sizes(k)
+    ne = z["n_int"] * z["ncpl"] + z["n_int"] * (z["n_int"] + 1) // 2   # ext payload (stride is even)
+    ext_all = ext_all[:, :ne]
+    torch.cuda.synchronize()
+    for sub in ([7], list(range(13))):            # single element, ragged batch
+        ST_s, ext_s, Sd_s, info_s = engine.condense_fused(k, len(sub), engine.to_dev(W[sub]), tab)
+        assert (info_s.cpu().numpy() == 0).all()
+        assert torch.equal(ST_s, ST_all[sub]) and torch.equal(ext_s[:, :ne], ext_all[sub])
+        assert torch.equal(Sd_s, Sd_all[sub])
+    ST2, ext2, Sd2, _ = engine.condense_fused(k, len(W), Wd, tab)
+    assert torch.equal(ST2, ST_all) and torch.equal(ext2[:, :ne], ext_all)
+    assert torch.equal(Sd2, Sd_all)
