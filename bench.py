@@ -190,7 +190,8 @@ def run_ours(args, rank, world):
     W = engine.to_dev(W_h)
     prog = [engine.to_dev(a) for a in engine.sblock_program(refs)]
     L = engine.srecord_layout(k)
-    rec = torch.empty((nt, L["len"]), dtype=torch.float64, device=dev)
+    unfused_path = args.unfused
+    rec = torch.empty((nt, L["len"]), dtype=torch.float64, device=dev) if unfused_path else None
     ST = torch.empty((nt, engine.st_stride(k)), dtype=torch.float64, device=dev)
     ext = torch.empty((nt, _abi.call("mcs_ext_stride", k)), dtype=torch.float64, device=dev)
     Sd = torch.empty((nt, _abi.call("mcs_sd_stride", k)), dtype=torch.float64, device=dev)
@@ -200,7 +201,8 @@ def run_ours(args, rank, world):
     st = _abi.stream(stream)
 
     fused = k in engine.FUSED_DEGREES and not args.unfused
-    if fused:
+    gen = k not in engine.FUSED_DEGREES and not args.unfused
+    if fused or gen:
         tab = engine.to_dev(engine.fused_tables(refs)[0])
 
     def step(ev=None):
@@ -214,10 +216,16 @@ def run_ours(args, rank, world):
                 ev[2].record(stream)
                 ev[3].record(stream)
             return
-        engine.element_srecords(nt, W, prog, k, out=rec, stream=stream)
-        if ev:
-            ev[1].record(stream)
-        _abi.call("mcs_condense_struct", k, nt, _abi.ptr(rec), _abi.ptr(ST), _abi.ptr(info), st)
+        if gen:     # A1 + A3 in one kernel (generation fused), then A4
+            if ev:
+                ev[1].record(stream)
+            _abi.call("mcs_condense_gen", k, nt, _abi.ptr(W), W.shape[1], _abi.ptr(tab),
+                      _abi.ptr(ST), _abi.ptr(info), st)
+        else:
+            engine.element_srecords(nt, W, prog, k, out=rec, stream=stream)
+            if ev:
+                ev[1].record(stream)
+            _abi.call("mcs_condense_struct", k, nt, _abi.ptr(rec), _abi.ptr(ST), _abi.ptr(info), st)
         if ev:
             ev[2].record(stream)
         _abi.call("mcs_double_schur", k, nt, _abi.ptr(ST), _abi.ptr(ext), _abi.ptr(Sd),
@@ -359,7 +367,8 @@ def run_ours(args, rank, world):
         kname, kpref = f"condense_fused (A1+A3+A4), k={k}", f"condense_fused_kernel<{k},"
     else:
         t_kern = t_a3.mean()
-        kname, kpref = f"condense_struct (A3), k={k}", f"condense_struct_kernel<{k},"
+        kname, kpref = ((f"condense_gen (A1+A3), k={k}", f"condense_gen_kernel<{k},") if gen else
+                        (f"condense_struct (A3), k={k}", f"condense_struct_kernel<{k},"))
         z_ = refblocks.local_sizes(k)
         ny_ = k * (k + 1) + 3 * k
         f_kern = (z_["nloc"] * (z_["nloc"] + 1) * ny_ + z_["nloc"] * (12 * (k * (k + 1) // 2)
@@ -397,7 +406,7 @@ def run_ours(args, rank, world):
         "e2e": {"value": world * nt / (e2e_ms * 1e-3), "unit": "elements/s",
                 "h2d_bytes_per_step": W_h.nbytes, "d2h_bytes_per_step": out_bytes,
                 "ms_per_step": e2e_ms},
-        "gpu_launches": (1 if fused else 3) * args.steps,
+        "gpu_launches": (1 if fused else (2 if gen else 3)) * args.steps,
         "clocks": clk,
     }
     if micro:

@@ -51,6 +51,13 @@ int mcs_srec_len(int k);
 int mcs_condense_struct(int k, int64_t nt, const double* srecords, double* S_packed, int* info,
                         void* stream);
 
+/* ---- generation-fused structured condensation for any k (used for k = 5, 6,
+ *      where Y does not fit a warp's registers): S_T from the geometry weights
+ *      W [nt][nwgt >= 30] and the tables [mcs_fused_table_len(k)], CTA per
+ *      element, Y in shared memory; the compact record never reaches HBM. */
+int mcs_condense_gen(int k, int64_t nt, const double* W, int nwgt, const double* tables,
+                     double* S_packed, int* info, void* stream);
+
 /* ---- fused element pipeline for k <= 4 (replaces assembly.py:49-91 +
  *      condensation.py:159-177 + condensation.py:207-226 per element): one
  *      warp per element generates Bsig from the reference-cell tables and the

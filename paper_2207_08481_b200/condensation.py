@@ -195,7 +195,6 @@ class CondensedSystem:
             raise RuntimeError(f"{what} on element {int(bad[0])}")
 
 
-_PROGRAMS = {}
 _FUSED = {}
 _RECOVERY = {}
 
@@ -206,14 +205,6 @@ def _fused_tables(k, refs):
         _FUSED[k] = engine.to_dev(engine.fused_tables(refs)[0])
     return _FUSED[k]
 STRUCT_TOL = 1e-10
-
-
-def _device_program(k, refs):
-    """Compact-record generation program of degree k on the device (the
-    reference matrices depend on k only; built once per process)."""
-    if k not in _PROGRAMS:
-        _PROGRAMS[k] = [engine.to_dev(a) for a in engine.sblock_program(refs)]
-    return _PROGRAMS[k]
 
 
 def condense_sigma_omega(fes, nu: float, body_force=None, blocks=None,
@@ -249,12 +240,9 @@ def condense_sigma_omega(fes, nu: float, body_force=None, blocks=None,
                                                      stream=stream)
         pending = (ext, Sd, info)
         loads = load_vectors(fes, refs, body_force)
-    else:
+    else:                                         # k = 5, 6: no record in HBM either
         W = engine.to_dev(element_weights(fes, nu))
-        prog = _device_program(k, refs)
-        records = engine.element_srecords(nt, W, prog, k, stream=stream)
-        S_dev, info = engine.condense_struct(k, records, stream=stream)
-        del records                               # blocks are not kept
+        S_dev, info = engine.condense_gen(k, nt, W, _fused_tables(k, refs), stream=stream)
         loads = load_vectors(fes, refs, body_force)
     maps = element_maps(fes)
     load = np.zeros(fes.n_vv)

@@ -94,6 +94,21 @@ __device__ __forceinline__ int cpl_local(int c) {
   return c < Z::n_em ? c : c + Z::n_int;
 }
 
+// reference-cell tables of the fused kernel (doubles):
+//   G4 [NR][ns][4] = (base, T_0, T_1, T_2) per Bsig entry | Adiv [nu][nu] |
+//   MbRef [6][nb][nb] | ARef [6][ml][9]      (rows >= nloc zero; segments even)
+template <int K>
+struct FTab {
+  using Z = Sizes<K>;
+  static constexpr int ml = K * (K + 1) / 2, nl = 3 * ml, nb = 3 * K;
+  static constexpr int NR = (Z::nloc + 7) / 8 * 8;
+  static constexpr int o_G4 = 0;
+  static constexpr int o_adiv = o_G4 + 4 * NR * Z::ns;
+  static constexpr int o_Mb = o_adiv + even(Z::nu * Z::nu);
+  static constexpr int o_A = o_Mb + even(6 * nb * nb);
+  static constexpr int len = o_A + even(6 * 9 * ml);
+};
+
 // FP64 tensor-core MMA, m8n8k4: lane (g, t) supplies A[g][t], B[t][g] and
 // owns C[g][2t], C[g][2t+1]
 __device__ __forceinline__ void dmma884(double& c0, double& c1, double a, double b) {

@@ -28,21 +28,6 @@
 
 namespace mcs {
 
-// reference-cell tables of the fused kernel (doubles):
-//   G4 [NR][ns][4] = (base, T_0, T_1, T_2) per Bsig entry | Adiv [nu][nu] |
-//   MbRef [6][nb][nb] | ARef [6][ml][9]      (rows >= nloc zero; segments even)
-template <int K>
-struct FTab {
-  using Z = Sizes<K>;
-  static constexpr int ml = K * (K + 1) / 2, nl = 3 * ml, nb = 3 * K;
-  static constexpr int NR = (Z::nloc + 7) / 8 * 8;
-  static constexpr int o_G4 = 0;
-  static constexpr int o_adiv = o_G4 + 4 * NR * Z::ns;
-  static constexpr int o_Mb = o_adiv + even(Z::nu * Z::nu);
-  static constexpr int o_A = o_Mb + even(6 * nb * nb);
-  static constexpr int len = o_A + even(6 * 9 * ml);
-};
-
 // optional per-phase clock accounting (tools/fused_prof.py builds a copy of
 // this file with MCS_FUSED_PROF defined; the library never does)
 #ifdef MCS_FUSED_PROF
@@ -584,6 +569,8 @@ MCS_API int mcs_fused_table_len(int k) {
     case 2: return FTab<2>::len;
     case 3: return FTab<3>::len;
     case 4: return FTab<4>::len;
+    case 5: return FTab<5>::len;
+    case 6: return FTab<6>::len;
   }
   return -1;
 }

@@ -203,6 +203,23 @@ def recover_stress(k: int, nt: int, W_dev, tables_dev, codes_dev, x_dev, sig=Non
     return sig, om, info
 
 
+def condense_gen(k: int, nt: int, W_dev, tables_dev, ST=None, info=None, stream=None):
+    """S_T from the geometry weights for any k (csrc/condense_struct.cu
+    condense_gen_kernel: Bsig regenerated from the fused tables, no record
+    in HBM); used for k = 5, 6."""
+    torch = _t()
+    if _abi.call("mcs_fused_table_len", k) != fused_table_layout(k)["len"]:
+        raise _abi.McsError("fused table layout mismatch between Python and libmcsgpu")
+    dev = W_dev.device
+    if ST is None:
+        ST = torch.empty((nt, st_stride(k)), dtype=torch.float64, device=dev)
+    if info is None:
+        info = torch.empty(nt, dtype=torch.int32, device=dev)
+    _abi.call("mcs_condense_gen", k, nt, _abi.ptr(W_dev), W_dev.shape[1], _abi.ptr(tables_dev),
+              _abi.ptr(ST), _abi.ptr(info), _abi.stream(stream))
+    return ST, info
+
+
 def condense_fused(k: int, nt: int, W_dev, tables_dev, ST=None, ext=None, Sd=None,
                    info=None, stream=None):
     """Weights -> S_T, ext = [X | S_oo^-1], Sd_T in one warp-per-element

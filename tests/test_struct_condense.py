@@ -297,3 +297,23 @@ def test_gpu_condensation_edge_cases(cuda):
     ST2, ext2, Sd2, _ = engine.condense_fused(k, len(W), Wd, tab)
     assert torch.equal(ST2, ST_all) and torch.equal(ext2[:, :ne], ext_all)
     assert torch.equal(Sd2, Sd_all)
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("cfg,n,k", [(2, 3, 4), (2, 3, 5), (3, 2, 6), (3, 4, 6)])
+def test_gpu_condense_gen_matches_oracle(cuda, cfg, n, k):
+    """Generation-fused structured condensation (the k = 5, 6 path) against
+    the reference's LU condensation (condensation.py:161-176)."""
+    prob, _ = _setup(cfg, n)
+    fes = FeSystem(prob.mesh, prob.regions, k)
+    refs = refblocks.build_refs(fes)
+    W = engine.to_dev(refblocks.element_weights(fes, prob.nu))
+    tab, _ = engine.fused_tables(refs)
+    nt = fes.mesh.num_triangles
+    ST, info = engine.condense_gen(k, nt, W, engine.to_dev(tab))
+    assert (info.cpu().numpy() == 0).all()
+    got = engine.unpack_sym(ST.cpu().numpy(), refblocks.local_sizes(k)["nloc"])
+    for t in range(0, nt, max(1, nt // 20)):
+        ob = O.element_blocks(fes, t, prob.nu)
+        S_ref, _ = O.condense_element(*ob[:5])
+        assert rel(got[t], S_ref) <= 1e-12, (t, rel(got[t], S_ref))
