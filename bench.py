@@ -622,7 +622,7 @@ def main():
         cc = CpuCondenser(args.cfg, args.n, 1)
         v, cnt = cc.rate(args.cpu_sample)
         out["cpu_baseline"] = {"value": v, "unit": "elements/s", "cores": 1, "kind": "port",
-                               "sample": f"{cnt} random cfg2 elements, quadrature blocks + "
+                               "sample": f"{cnt} random cfg{args.cfg} elements, quadrature blocks + "
                                          "LU condensation + double Schur, 1 thread"}
         print(json.dumps(out), flush=True)
     if world > 1:

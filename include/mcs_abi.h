@@ -82,6 +82,20 @@ int mcs_recover_stress(int k, int64_t nt, const double* W, int nwgt, const doubl
                        const int* vv_codes, const double* x_full, double* sigma, double* omega,
                        int* info, void* stream);
 
+/* ---- post-solve structural checks (replaces driver.py:183-218 post_checks):
+ *      out[0] = max |div u| over elements and quadrature points, out[1] / out[2]
+ *      = max nt jump / max |nt| over interior facets and edge points; part:
+ *      [nparts] per-warp partial sums of int |grad u|^2 (sum them in order).
+ *      geo: [nt][10] = (J, J^-1 row-major, detJ, pad); vcodes: [nt][nu] V-dof
+ *      codes over all V dofs; tab_div [nu][nq], tab_grad [nu][nq][2][2], wq [nq];
+ *      fac: [nif][4] = (t0, le0, t1, le1), frame: [nif][4] = (t_F, n_F),
+ *      flip: [nt][3], sigma: [nt][ns], tab_se: [ns][3][nqe][2][2], nqe <= 8. */
+int mcs_post_checks(int64_t nt, int nu, int nq, const double* geo, const int* vcodes,
+                    const double* u, const double* tab_div, const double* tab_grad,
+                    const double* wq, int nif, int ns, int nqe, const int* fac,
+                    const double* frame, const signed char* flip, const double* sigma,
+                    const double* tab_se, double* out, double* part, int nparts, void* stream);
+
 /* ---- double Schur (replaces condensation.py:207-226 double_schur per
  *      element): ext = [X = S_oo^-1 S_oc (n_int x ncpl) | S_oo^-1 packed],
  *      Sd_packed = S_cc - S_co X. */

@@ -163,6 +163,30 @@ def stokes_case(R, name, cfg, n, comps=("additive", "multiplicative")):
           {c: int(out[f'gmres_{c}_iters']) for c in comps})
 
 
+def postcheck_case(R, name, cfg, n):
+    """Reference driver.post_checks (driver.py:183-218) on seeded random
+    velocity / stress vectors and a fixed residual history."""
+    sys.path.insert(0, ROOT)
+    from paper_2207_08481_b200.problems import baseline_config
+    prob = baseline_config(cfg, n)
+    m = R["mesh"].from_arrays(prob.mesh.vertices, prob.mesh.triangles)
+    eps = 1e-12
+    key = "tilde_neumann" if cfg == 3 else "neumann"
+    regions = R["mesh"].classify_boundary(
+        m, dirichlet=lambda x: x[0] < 1 - eps, **{key: lambda x: x[0] >= 1 - eps})
+    fes = R["dofmap"].FeSystem(m, regions, prob.k)
+    rng = np.random.default_rng(31)
+    u = rng.standard_normal(fes.dof_v.ndof)
+    sigma = rng.standard_normal(fes.dof_sigma.ndof)
+    rep = R["krylov"].KrylovReport(residuals=[1.0, 0.5, 0.25, 0.3])
+    chk = R["driver"].post_checks(fes, None, u, sigma, rep)
+    path = os.path.join(OUT, name + ".npz")
+    np.savez_compressed(path, u=u, sigma=sigma, residuals=np.array(rep.residuals),
+                        max_div_scaled=chk["max_div_scaled"], nt_jump_scaled=chk["nt_jump_scaled"],
+                        residual_monotone=chk["residual_monotone"])
+    print(path, chk)
+
+
 def microbench(R):
     import scipy.linalg as sla
     sys.path.insert(0, ROOT)
@@ -180,6 +204,10 @@ def microbench(R):
 def main():
     os.makedirs(OUT, exist_ok=True)
     R = _ref()
+    if "--postcheck" in sys.argv:
+        postcheck_case(R, "postcheck_c2_n3", 2, 3)
+        postcheck_case(R, "postcheck_c3_n2", 3, 2)
+        return
     if "--stokes" in sys.argv:
         stokes_case(R, "stokes_c1_n2", 1, 2)
         stokes_case(R, "stokes_c2_n3", 2, 3)
@@ -193,6 +221,8 @@ def main():
     stokes_case(R, "stokes_c1_n2", 1, 2)
     stokes_case(R, "stokes_c2_n3", 2, 3)
     stokes_case(R, "stokes_c3_n2", 3, 2)
+    postcheck_case(R, "postcheck_c2_n3", 2, 3)
+    postcheck_case(R, "postcheck_c3_n2", 3, 2)
 
 
 if __name__ == "__main__":

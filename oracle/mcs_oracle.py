@@ -500,6 +500,42 @@ def gmres(apply_A, b, apply_M=None, rtol=1e-6, maxit=500, project=None):
     return x, j, res
 
 
+# ------------------------------------------------------------- post checks
+
+
+def post_checks(fes, u, sigma, residuals):
+    """`driver.py:183-218` (pointwise divergence over the H1 seminorm,
+    nt-jump of the stress across interior facets, residual monotonicity),
+    restated on this package's FeSystem tables (the same formulas as
+    assembly.py:362-387)."""
+    max_div, grad_scale = 0.0, 0.0
+    for t in range(fes.mesh.num_triangles):
+        uloc = u[fes.dof_v.loc2glob[t]] * fes.dof_v.signs[t]
+        max_div = max(max_div, float(np.abs(uloc @ fes.tab_u_div / fes.detJ[t]).max()))
+        grad = np.einsum("ia,upab,bj->upij", fes.J[t], fes.tab_u_grad, fes.Jinv[t]) / fes.detJ[t]
+        g = np.einsum("u,upij->pij", uloc, grad)
+        wq = fes.quad_tri.weights * fes.detJ[t]
+        grad_scale += float(np.einsum("pij,p->", g * g, wq))
+    grad_scale = max(1.0, np.sqrt(grad_scale))
+    jump_max, scale = 0.0, 1e-300
+    for f in fes.mesh.interior_facets:
+        vals = []
+        for t in fes.mesh.facet_tri[f]:
+            le = int(np.nonzero(fes.edge_facet[t] == f)[0][0])
+            sloc = sigma[fes.dof_sigma.loc2glob[t]] * fes.dof_sigma.signs[t]
+            sv = np.einsum("s,spij->pij", sloc, fes.map_stress(t, fes.tab_sigma_edge[:, le]))
+            nt = np.einsum("i,pij,j->p", fes.mesh.facet_tangent[f], sv, fes.mesh.facet_normal[f])
+            if fes.edge_flip[t, le]:
+                nt = nt[::-1]
+            vals.append(nt)
+        jump_max = max(jump_max, float(np.abs(vals[0] - vals[1]).max()))
+        scale = max(scale, float(np.abs(vals[0]).max()))
+    res = residuals
+    monotone = all(res[i + 1] <= res[i] * (1 + 1e-12) for i in range(len(res) - 1))
+    return {"max_div_scaled": max_div / grad_scale,
+            "nt_jump_scaled": jump_max / max(scale, 1.0), "residual_monotone": monotone}
+
+
 # -------------------------------------------------------------- microbench
 
 

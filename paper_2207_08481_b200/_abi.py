@@ -35,6 +35,9 @@ SIGNATURES = {
     "mcs_mdot_len": [],
     "mcs_mdot": [_i, _l, _l, _p, _p, _p, _p, _p],
     "mcs_gemv_acc": [_i, _l, _l, _p, _p, _d, _d, _p, _p],
+    # postcheck.cu
+    "mcs_post_checks": [_l, _i, _i, _p, _p, _p, _p, _p, _p, _i, _i, _i, _p, _p, _p, _p, _p, _p,
+                        _p, _i, _p],
     # recover.cu
     "mcs_recover_table_len": [_i],
     "mcs_recover_stress": [_i, _l, _p, _i, _p, _p, _p, _p, _p, _p, _p],

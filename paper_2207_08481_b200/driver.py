@@ -102,8 +102,55 @@ def solve_elliptic(problem, k, nu, opts: SolverOptions) -> EllipticResult:
     t_sol = time.perf_counter() - t1
     x_full = fes.vv_values.copy()
     x_full[fes.vv_free] = x
+    # reference driver.py:165-169: stress recovery and structural checks
+    sigma, w = sys_.recover_stress(x_full)
+    checks = post_checks(fes, sys_, x_full[:fes.n_v], sigma, report)
     return EllipticResult(fes, sys_, x, x_full[:fes.n_v], x_full[fes.n_v:], report,
-                          t_sup, t_sol)
+                          t_sup, t_sol, extras=dict(sigma=sigma, w=w, checks=checks))
+
+
+def post_checks(fes, sys_, u, sigma, report: KrylovReport) -> dict:
+    """Structural postconditions (reference `driver.py:183-218`): pointwise
+    divergence scaled by the H1 seminorm, nt-continuity of the recovered
+    stress across interior facets, residual monotonicity.  The element and
+    facet sweeps run on the GPU (csrc/postcheck.cu)."""
+    import torch
+    from . import _abi
+    dev = lambda a, dt=np.float64: torch.from_numpy(np.ascontiguousarray(a, dtype=dt)).cuda()
+    nt = fes.mesh.num_triangles
+    nu_l = fes.tab_u_div.shape[0]
+    nq = fes.tab_u_div.shape[1]
+    geo = np.zeros((nt, 10))
+    geo[:, 0:4] = fes.J.reshape(nt, 4)
+    geo[:, 4:8] = fes.Jinv.reshape(nt, 4)
+    geo[:, 8] = fes.detJ
+    dv = fes.dof_v
+    vcodes = (2 * dv.loc2glob + (dv.signs < 0)).astype(np.int32)
+    mesh = fes.mesh
+    fint = np.asarray(mesh.interior_facets)
+    t01 = mesh.facet_tri[fint]
+    le = np.stack([np.argmax(fes.edge_facet[t01[:, s_]] == fint[:, None], axis=1) for s_ in (0, 1)], 1)
+    fac = np.stack([t01[:, 0], le[:, 0], t01[:, 1], le[:, 1]], 1).astype(np.int32)
+    frame = np.concatenate([mesh.facet_tangent[fint], mesh.facet_normal[fint]], 1)
+    ns = fes.tab_sigma_edge.shape[0]
+    nqe = fes.tab_sigma_edge.shape[2]
+    nparts = 4 * 148 * 4
+    out = torch.zeros(4, dtype=torch.float64, device="cuda")
+    part = torch.zeros(nparts, dtype=torch.float64, device="cuda")
+    u_d, s_d = dev(u), dev(sigma)
+    args = [dev(geo), dev(vcodes, np.int32), u_d, dev(fes.tab_u_div), dev(fes.tab_u_grad),
+            dev(fes.quad_tri.weights), len(fint), ns, nqe, dev(fac, np.int32), dev(frame),
+            dev(fes.edge_flip.astype(np.int8), np.int8), s_d, dev(fes.tab_sigma_edge)]
+    ptrs = [a if isinstance(a, int) else _abi.ptr(a) for a in args]
+    _abi.call("mcs_post_checks", nt, nu_l, nq, *ptrs, _abi.ptr(out), _abi.ptr(part), nparts,
+              _abi.stream(None))
+    o = out.cpu().numpy()
+    grad_scale = max(1.0, float(np.sqrt(np.sum(part.cpu().numpy()))))
+    res = report.residuals
+    monotone = all(res[i + 1] <= res[i] * (1 + 1e-12) for i in range(len(res) - 1))
+    return {"max_div_scaled": float(o[0]) / grad_scale,
+            "nt_jump_scaled": float(o[1]) / max(float(o[2]), 1.0),
+            "residual_monotone": monotone}
 
 
 def pressure_projector(fes):
@@ -144,6 +191,7 @@ class StokesResult:
     report: KrylovReport
     t_sup: float
     t_sol: float
+    checks: dict = None
 
 
 def solve_stokes(problem, k, nu, opts: SolverOptions):
@@ -183,5 +231,6 @@ def solve_stokes(problem, k, nu, opts: SolverOptions):
     x_full = fes.vv_values.copy()
     x_full[fes.vv_free] = x_free
     sigma, w = sys_.recover_stress(x_full)
+    checks = post_checks(fes, sys_, x_full[:fes.n_v], sigma, report)
     return StokesResult(fes, sys_, x_free, x_full[:fes.n_v], x_full[fes.n_v:], p_phys, sigma, w,
-                        report, t_sup, t_sol)
+                        report, t_sup, t_sol, checks)

@@ -131,3 +131,10 @@ def test_gpu_solve_stokes_end_to_end(cuda):
     assert rel(np.asarray(r.x_free), x[:nv]) <= 1e-7
     assert rel(r.p, -x[nv:]) <= 1e-7
     assert r.sigma.shape == (fes.mesh.num_triangles * refblocks.local_sizes(prob.k)["ns"],)
+    # reference post_checks on the same (u, sigma, history), restated
+    ref = O.post_checks(fes, r.u, r.sigma, r.report.residuals)
+    np.testing.assert_allclose(r.checks["max_div_scaled"], ref["max_div_scaled"], rtol=1e-9,
+                               atol=1e-14)
+    np.testing.assert_allclose(r.checks["nt_jump_scaled"], ref["nt_jump_scaled"], rtol=1e-9,
+                               atol=1e-14)
+    assert r.checks["max_div_scaled"] < 1e-8          # MCS velocities are divergence-free
