@@ -69,7 +69,7 @@ class _PcgState:
     def step(self, rz, rz_new):
         ws = workspace()
         st = _abi.stream()
-        if hasattr(self.A, "apply_dot"):      # p'Ap accumulated inside the apply kernel
+        if hasattr(self.A, "apply_dot") and not _NO_FUSED_PAP:   # p'Ap inside the apply kernel
             self.A.apply_dot(self.p, self.Ap, ws.PAP)
         else:
             _apply(self.A, self.p, self.Ap)
@@ -106,6 +106,8 @@ class _PcgState:
 
 
 _STATES = {}
+# A/B switch for the fused curvature (MCS_NO_FUSED_PAP=1: separate dot kernel)
+_NO_FUSED_PAP = __import__("os").environ.get("MCS_NO_FUSED_PAP", "0") == "1"
 
 
 def cg(apply_A, b, apply_M=None, rtol=1e-8, maxit=1000, stream=None, use_graph=True):
