@@ -354,6 +354,10 @@ def run_ours(args, rank, world):
         if i >= 2:
             e2e_times.append(e0.elapsed_time(e1))
     e2e_ms = float(np.mean(e2e_times))
+    if world > 1:   # whole-job e2e: the slowest replica
+        t = torch.tensor([e2e_ms], device=dev)
+        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+        e2e_ms = float(t.item())
 
     # ---- config-5 microbench (SPD Schur S = B^T A^-1 B, n_s=60, n_c=36)
     micro = run_microbench(args, dev) if args.micro else None
