@@ -164,7 +164,10 @@ int mcs_mf_backward(int nnodes, const int* level_nodes, const void* nodes, const
                     const int* B, const int* perm, const double* y, double* xp, double* x,
                     int max_ns, int max_nb, void* stream);
 /* top of the tree (t dofs): g = b_T - frontier updates, x_T = Sinv g with the
- * dense inverse of the top Schur complement (= (A^-1)_TT) */
+ * dense inverse of the top Schur complement (= (A^-1)_TT).  Sinv is t rows of
+ * ld = mcs_mf_top_ld(t) doubles (zero padded), g holds ld doubles whose
+ * padding is zero (only g[0..t) is written). */
+int mcs_mf_top_ld(int t);
 int mcs_mf_top(int t, const int* T, const int* perm, const double* b, const int* ptr,
                const int* src, const double* out, double* g, const double* Sinv, double* xp,
                double* x, void* stream);

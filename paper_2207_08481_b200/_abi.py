@@ -63,6 +63,7 @@ SIGNATURES = {
     # coarse.cu
     "mcs_mf_forward": [_i, _p, _p, _p, _p, _p, _p, _p, _p, _p, _i, _i, _p],
     "mcs_mf_backward": [_i, _p, _p, _p, _p, _p, _p, _p, _p, _i, _i, _p],
+    "mcs_mf_top_ld": [_i],
     "mcs_mf_top": [_i, _p, _p, _p, _p, _p, _p, _p, _p, _p, _p, _p],
     # blas1.cu
     "mcs_reduce_workspace_len": [],

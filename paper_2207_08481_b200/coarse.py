@@ -209,8 +209,9 @@ def _upload_multifrontal(F: MultifrontalFactor):
         top_dev = dict(t=len(T), T=engine.to_dev(T.astype(np.int32)),
                        ptr=engine.to_dev(ptr.astype(np.int32)),
                        src=engine.to_dev(src.astype(np.int32) if len(src) else np.zeros(1, np.int32)),
-                       Sinv=engine.to_dev(Sinv),
-                       g=torch.empty(len(T), dtype=torch.float64, device="cuda"))
+                       Sinv=engine.to_dev(_pad_cols(Sinv, _abi.call("mcs_mf_top_ld", len(T)))),
+                       g=torch.zeros(_abi.call("mcs_mf_top_ld", len(T)), dtype=torch.float64,
+                                     device="cuda"))
     F.dev = dict(
         top=top_dev, H=H,
         mats=engine.to_dev(np.concatenate(mats) if mats else np.zeros(1)),
@@ -228,6 +229,13 @@ def _upload_multifrontal(F: MultifrontalFactor):
         bytes=8 * off,
     )
     return F
+
+
+def _pad_cols(S: np.ndarray, ld: int) -> np.ndarray:
+    """Rows of S padded with zeros to ld columns (coarse.cu mf_top_solve)."""
+    P = np.zeros((S.shape[0], ld))
+    P[:, :S.shape[1]] = S
+    return P
 
 
 def _top_split(F: MultifrontalFactor, top_max: int = None):

@@ -284,32 +284,62 @@ __global__ void mf_top_gather(int t, const int* __restrict__ T, const int* __res
   g[q] = v;
 }
 
-// x_T = Sinv g (dense t x t, warp per row), scattered to xp[T[q]] and x[perm[T[q]]]
-__global__ void mf_top_solve(int t, const double* __restrict__ Sinv, const double* g,
-                             const int* __restrict__ T, const int* __restrict__ perm,
-                             double* __restrict__ xp, double* __restrict__ x) {
+// x_T = Sinv g (dense t x ld, ld = t rounded up to 32, zero padded; g zero
+// padded to ld): CTA per row, 16-byte loads.  The row's first TOP_NT x TOP_U
+// pairs (the whole row for t <= 4096) are loaded before pdl_wait(): Sinv is
+// static, so its fetch overlaps the gather kernel and the launch latency.
+// The result goes to xp[T[r]] and x[perm[T[r]]].  Fixed-order reduction.
+constexpr int TOP_NT = 256, TOP_U = 8;
+
+__global__ void __launch_bounds__(TOP_NT)
+    mf_top_solve(int ld2, const double2* __restrict__ Sinv, const double* g,
+                 const int* __restrict__ T, const int* __restrict__ perm, double* __restrict__ xp,
+                 double* __restrict__ x) {
+  const int r = blockIdx.x;
+  const double2* row = Sinv + (int64_t)r * ld2;
+  const double2* g2 = reinterpret_cast<const double2*>(g);
+  double2 a[TOP_U];
+#pragma unroll
+  for (int u = 0; u < TOP_U; ++u) {
+    const int j = u * TOP_NT + threadIdx.x;
+    a[u] = j < ld2 ? __ldg(row + j) : make_double2(0.0, 0.0);
+  }
   pdl_wait();
   pdl_trigger();
-  const int w = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
-  if (w >= t) return;
-  const double* row = Sinv + (int64_t)w * t;
-  double s0 = 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0;
-  int j = lane;
-  for (; j + 96 < t; j += 128) {
-    s0 = fma(__ldg(row + j), g[j], s0);
-    s1 = fma(__ldg(row + j + 32), g[j + 32], s1);
-    s2 = fma(__ldg(row + j + 64), g[j + 64], s2);
-    s3 = fma(__ldg(row + j + 96), g[j + 96], s3);
+  double s = 0.0;
+  for (int base = 0;;) {
+#pragma unroll
+    for (int u = 0; u < TOP_U; ++u) {
+      const int j = base + u * TOP_NT + threadIdx.x;
+      if (j < ld2) {
+        const double2 b = g2[j];
+        s = fma(a[u].y, b.y, fma(a[u].x, b.x, s));
+      }
+    }
+    base += TOP_NT * TOP_U;
+    if (base >= ld2) break;
+#pragma unroll
+    for (int u = 0; u < TOP_U; ++u) {
+      const int j = base + u * TOP_NT + threadIdx.x;
+      a[u] = j < ld2 ? __ldg(row + j) : make_double2(0.0, 0.0);
+    }
   }
-  for (; j < t; j += 32) s0 = fma(__ldg(row + j), g[j], s0);
-  const double s = warp_sum((s0 + s1) + (s2 + s3));
-  if (lane == 0) {
-    xp[T[w]] = s;
-    x[perm[T[w]]] = s;
+  s = warp_sum(s);
+  __shared__ double red[TOP_NT / 32];
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = s;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double v = 0.0;
+#pragma unroll
+    for (int w = 0; w < TOP_NT / 32; ++w) v += red[w];
+    xp[T[r]] = v;
+    x[perm[T[r]]] = v;
   }
 }
 
 }  // namespace mcs
+
+MCS_API int mcs_mf_top_ld(int t) { return (t + 31) / 32 * 32; }
 
 MCS_API int mcs_mf_top(int t, const int* T, const int* perm, const double* b, const int* ptr,
                        const int* src, const double* out, double* g, const double* Sinv,
@@ -318,7 +348,8 @@ MCS_API int mcs_mf_top(int t, const int* T, const int* perm, const double* b, co
   auto st = static_cast<cudaStream_t>(stream);
   int rc = launch_pdl_g(PDL_COARSE, mf_top_gather, (t + 127) / 128, 128, 0, st, t, T, perm, b, ptr, src, out, g);
   if (rc) return rc;
-  const int64_t threads = (int64_t)t * 32;
-  return launch_pdl_g(PDL_COARSE, mf_top_solve, (int)((threads + 255) / 256), 256, 0, st, t, Sinv, g, T, perm,
-                    xp, x);
+  const int ld = mcs_mf_top_ld(t);
+  return launch_pdl_g(PDL_COARSE, mf_top_solve, t, TOP_NT, 0, st, ld / 2,
+                      reinterpret_cast<const double2*>(Sinv), static_cast<const double*>(g), T,
+                      perm, xp, x);
 }
