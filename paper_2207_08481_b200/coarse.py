@@ -178,10 +178,16 @@ def _upload_multifrontal(F: MultifrontalFactor):
         lo = nd.Linv[r, c]                                  # packed lower, row-major
         ru, cu = np.triu_indices(ns)
         up = nd.Linv.T[ru, cu]                              # packed upper, row-major
+        # forward block [Linv | W] and backward block [W^T | Linv^T], each
+        # starting on an even offset (16-byte aligned for the bulk copies of
+        # coarse.cu mf_forward_s / mf_backward_s) and padded to even length
+        pad = (len(lo) + nb * ns) % 2
         o_L = off; mats.append(lo); off += len(lo)
-        o_LT = off; mats.append(up); off += len(up)
         o_W = off; mats.append(nd.W.ravel()); off += nb * ns
+        mats.append(np.zeros(pad)); off += pad
         o_WT = off; mats.append(np.ascontiguousarray(nd.W.T).ravel()); off += nb * ns
+        o_LT = off; mats.append(up); off += len(up)
+        mats.append(np.zeros(pad)); off += pad
         node_tab[i] = [nd.s0, ns, nb, o_L, o_LT, o_W, o_WT, oo, bo, 0]
         out_off.append(oo)
         oo += nb

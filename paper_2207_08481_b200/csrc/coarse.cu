@@ -240,6 +240,207 @@ __global__ void __launch_bounds__(MF_THREADS)
       });
 }
 
+// ---- shared-memory staged variants (the default when a level's blocks fit) --
+// Each node's factor blocks are contiguous in `mats`, 16-byte aligned:
+//   forward block  [Linv packed lower | W (nb x ns)]    at off_Linv
+//   backward block [W^T (ns x nb) | Linv^T packed upper] at off_WT
+// One bulk copy (TMA engine) per CTA moves the block into shared memory and
+// the static gather indices go to registers, both before pdl_wait(): the
+// factor fetch overlaps the previous level, and after the wait a level costs
+// one dependent global round trip (the gathered right-hand side) plus
+// shared-memory GEMVs.
+
+// Rows r in [0, nrows) of a matrix in shared memory: v_r = sum_{j in [lo, hi)}
+// p_r[j] x[j], G lanes per row (G a power of two <= 8, chosen so that the
+// rows of one pass cover the block), fixed-order shuffle reduction.
+template <class ROW, class EMIT>
+__device__ __forceinline__ void smem_rows(int nrows, int width, const double* x, ROW row,
+                                          EMIT emit) {
+  int G = 1;
+  while (G < 8 && nrows * G * 2 <= MF_THREADS && G * 8 < width) G *= 2;
+  const int sub = threadIdx.x & (G - 1);
+  for (int r0 = 0; r0 < nrows; r0 += MF_THREADS / G) {
+    const int r = r0 + threadIdx.x / G;
+    double a0 = 0.0, a1 = 0.0;
+    if (r < nrows) {
+      const double* p;
+      int lo, hi;
+      row(r, p, lo, hi);
+      int j = lo + sub;
+      for (; j + G < hi; j += 2 * G) {
+        a0 = fma(p[j], x[j], a0);
+        a1 = fma(p[j + G], x[j + G], a1);
+      }
+      if (j < hi) a0 = fma(p[j], x[j], a0);
+    }
+    double v = a0 + a1;
+    for (int o = G >> 1; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    if (r < nrows && sub == 0) emit(r, v);
+  }
+}
+
+constexpr int MF_PRE = 2;   // gather indices preloaded per thread (ns + nb <= 512)
+
+__global__ void __launch_bounds__(MF_THREADS)
+    mf_forward_s(const int* __restrict__ level_nodes, const NodeRec* __restrict__ nodes,
+                 const double* __restrict__ mats, const int* __restrict__ src_t,
+                 const int* __restrict__ src_o, const int* __restrict__ perm, const double* b,
+                 double* __restrict__ y, double* out, int blk_max, int max_ns) {
+  extern __shared__ __align__(16) double sm[];
+  __shared__ uint64_t bar;
+  const NodeRec nd = nodes[level_nodes[blockIdx.x]];
+  const int ns = (int)nd.ns, nb = (int)nd.nb;
+  double* F = sm;
+  double* t = sm + blk_max;
+  double* ys = t + max_ns;
+  double* pass = ys + max_ns;
+  if (threadIdx.x == 0) {
+    const int len = even(npk(ns) + nb * ns);
+    mbar_init(&bar, 1);
+    fence_barrier_init();
+    mbar_expect_tx(&bar, len * 8);
+    if (len) bulk_g2s(F, mats + nd.oL, len * 8, &bar);
+  }
+  int ia[MF_PRE], ib[MF_PRE], ic[MF_PRE];
+#pragma unroll
+  for (int u = 0; u < MF_PRE; ++u) {
+    const int j = threadIdx.x + u * MF_THREADS;
+    ia[u] = ib[u] = ic[u] = -1;
+    if (j < ns) {
+      const int64_t p = nd.s0 + j;
+      ia[u] = __ldg(perm + p);
+      ib[u] = __ldg(src_t + 2 * p);
+      ic[u] = __ldg(src_t + 2 * p + 1);
+    } else if (j < ns + nb) {
+      const int64_t q = nd.oo + (j - ns);
+      ib[u] = __ldg(src_o + 2 * q);
+      ic[u] = __ldg(src_o + 2 * q + 1);
+    }
+  }
+  pdl_wait();
+  pdl_trigger();
+  auto gather = [&](int j, int pv, int a, int c) {
+    if (j < ns) {
+      double v = b[pv];
+      if (a >= 0) v -= out[a];
+      if (c >= 0) v -= out[c];
+      t[j] = v;
+    } else {
+      double v = 0.0;
+      if (a >= 0) v += out[a];
+      if (c >= 0) v += out[c];
+      pass[j - ns] = v;
+    }
+  };
+#pragma unroll
+  for (int u = 0; u < MF_PRE; ++u) {
+    const int j = threadIdx.x + u * MF_THREADS;
+    if (j < ns + nb) gather(j, ia[u], ib[u], ic[u]);
+  }
+  for (int j = threadIdx.x + MF_PRE * MF_THREADS; j < ns + nb; j += MF_THREADS) {
+    if (j < ns) {
+      const int64_t p = nd.s0 + j;
+      gather(j, __ldg(perm + p), __ldg(src_t + 2 * p), __ldg(src_t + 2 * p + 1));
+    } else {
+      const int64_t q = nd.oo + (j - ns);
+      gather(j, -1, __ldg(src_o + 2 * q), __ldg(src_o + 2 * q + 1));
+    }
+  }
+  __syncthreads();
+  mbar_wait(&bar, 0);
+  smem_rows(
+      ns, ns, t,
+      [&](int r, const double*& p, int& lo, int& hi) {
+        p = F + r * (r + 1) / 2;
+        lo = 0;
+        hi = r + 1;
+      },
+      [&](int r, double v) {
+        y[nd.s0 + r] = v;
+        ys[r] = v;
+      });
+  __syncthreads();
+  const double* W = F + npk(ns);
+  smem_rows(
+      nb, ns, ys,
+      [&](int r, const double*& p, int& lo, int& hi) {
+        p = W + r * ns;
+        lo = 0;
+        hi = ns;
+      },
+      [&](int r, double v) { out[nd.oo + r] = v + pass[r]; });
+}
+
+__global__ void __launch_bounds__(MF_THREADS)
+    mf_backward_s(const int* __restrict__ level_nodes, const NodeRec* __restrict__ nodes,
+                  const double* __restrict__ mats, const int* __restrict__ B,
+                  const int* __restrict__ perm, const double* y, double* xp,
+                  double* __restrict__ x, int blk_max, int max_ns) {
+  extern __shared__ __align__(16) double sm[];
+  __shared__ uint64_t bar;
+  const NodeRec nd = nodes[level_nodes[blockIdx.x]];
+  const int ns = (int)nd.ns, nb = (int)nd.nb;
+  double* F = sm;
+  double* s = sm + blk_max;
+  int* ps = reinterpret_cast<int*>(s + max_ns);   // perm of the own rows
+  double* xb = s + 2 * max_ns;
+  if (threadIdx.x == 0) {
+    const int len = even(npk(ns) + nb * ns);
+    mbar_init(&bar, 1);
+    fence_barrier_init();
+    mbar_expect_tx(&bar, len * 8);
+    if (len) bulk_g2s(F, mats + nd.oWT, len * 8, &bar);
+  }
+  int bi[MF_PRE];
+  const int* Bp = B + nd.ob;
+#pragma unroll
+  for (int u = 0; u < MF_PRE; ++u) {
+    const int j = threadIdx.x + u * MF_THREADS;
+    bi[u] = j < nb ? __ldg(Bp + j) : 0;
+  }
+  for (int j = threadIdx.x; j < ns; j += MF_THREADS) ps[j] = __ldg(perm + nd.s0 + j);
+  pdl_wait();
+  pdl_trigger();
+#pragma unroll
+  for (int u = 0; u < MF_PRE; ++u) {
+    const int j = threadIdx.x + u * MF_THREADS;
+    if (j < nb) xb[j] = xp[bi[u]];
+  }
+  for (int j = threadIdx.x + MF_PRE * MF_THREADS; j < nb; j += MF_THREADS) xb[j] = xp[__ldg(Bp + j)];
+  __syncthreads();
+  mbar_wait(&bar, 0);
+  smem_rows(
+      ns, nb, xb,
+      [&](int r, const double*& p, int& lo, int& hi) {
+        p = F + r * nb;
+        lo = 0;
+        hi = nb;
+      },
+      [&](int r, double v) { s[r] = y[nd.s0 + r] - v; });
+  __syncthreads();
+  const double* LT = F + ns * nb;   // packed upper, row r holds columns r..ns-1
+  smem_rows(
+      ns, ns, s,
+      [&](int r, const double*& p, int& lo, int& hi) {
+        p = LT + upk_row(r, ns);
+        lo = r;
+        hi = ns;
+      },
+      [&](int r, double v) {
+        xp[nd.s0 + r] = v;
+        x[ps[r]] = v;
+      });
+}
+
+// shared bytes of the staged kernels for a level (0: use the global variants)
+static size_t mf_stage_smem(int max_ns, int max_nb, int& blk_max) {
+  blk_max = even(npk(max_ns) + max_ns * max_nb);
+  // forward [block | t : max_ns | ys : max_ns | pass : max_nb],
+  // backward [block | s : max_ns | perm (ints) : max_ns | xb : max_nb]
+  const size_t bytes = ((size_t)blk_max + 2 * (size_t)max_ns + max_nb) * sizeof(double);
+  return bytes <= 200 * 1024 ? bytes : 0;
+}
+
 }  // namespace mcs
 
 using namespace mcs;
@@ -250,6 +451,14 @@ MCS_API int mcs_mf_forward(int nnodes, const int* level_nodes, const void* nodes
                            int max_nb, void* stream) {
   if (nnodes <= 0) return 0;
   auto st = static_cast<cudaStream_t>(stream);
+  int blk_max = 0;
+  const size_t staged = mf_stage_smem(max_ns, max_nb, blk_max);
+  if (staged) {
+    cudaFuncSetAttribute(mf_forward_s, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)staged);
+    return launch_pdl_g(PDL_COARSE, mf_forward_s, nnodes, MF_THREADS, staged, st, level_nodes,
+                        static_cast<const NodeRec*>(nodes), mats, src_t, src_o, perm, b, y, out,
+                        blk_max, max_ns);
+  }
   const size_t smem = (2 * (size_t)max_ns + max_nb) * sizeof(double);
   cudaFuncSetAttribute(mf_forward, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   return launch_pdl_g(PDL_COARSE, mf_forward, nnodes, MF_THREADS, smem, st, level_nodes,
@@ -261,6 +470,14 @@ MCS_API int mcs_mf_backward(int nnodes, const int* level_nodes, const void* node
                             double* xp, double* x, int max_ns, int max_nb, void* stream) {
   if (nnodes <= 0) return 0;
   auto st = static_cast<cudaStream_t>(stream);
+  int blk_max = 0;
+  const size_t staged = mf_stage_smem(max_ns, max_nb, blk_max);
+  if (staged) {
+    cudaFuncSetAttribute(mf_backward_s, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)staged);
+    return launch_pdl_g(PDL_COARSE, mf_backward_s, nnodes, MF_THREADS, staged, st, level_nodes,
+                        static_cast<const NodeRec*>(nodes), mats, B, perm, y, xp, x, blk_max,
+                        max_ns);
+  }
   const size_t smem = (2 * (size_t)max_ns + max_nb) * sizeof(double);
   cudaFuncSetAttribute(mf_backward, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   return launch_pdl_g(PDL_COARSE, mf_backward, nnodes, MF_THREADS, smem, st, level_nodes,
