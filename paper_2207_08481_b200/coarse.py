@@ -37,7 +37,7 @@ import scipy.sparse as sp
 from . import _abi, engine
 
 DENSE_MAX = 1024
-LEAF = int(os.environ.get("MCS_LEAF", "96"))         # max dofs of a nested-dissection leaf
+LEAF = int(os.environ.get("MCS_LEAF", "64"))   # max dofs of a nested-dissection leaf (A/B in PCG: 64 > 80 > 96)
 TOP_MAX = int(os.environ.get("MCS_TOP_MAX", "4096"))   # dense-inverse top (A/B in PCG: 4096 > 2048)
 
 
