@@ -103,22 +103,23 @@ __global__ void __launch_bounds__(W * 32)
     __syncwarp();
     mbar_wait(&bar[s], (it / NST) & 1);
     const double* P = stage + s * STRIDE;
+    // packed entry (i, j) sits at pk(i, 0) + j for j <= i and pk(j, 0) + i
+    // for j > i: walked incrementally (+1 while j < i, then + j + 1)
     double acc[R];
-    int rowb[R];
+    int ad[R], ir[R];
 #pragma unroll
     for (int r = 0; r < R; ++r) {
       acc[r] = 0.0;
-      const int i = min(lane + 32 * r, N - 1);
-      rowb[r] = pk(i, 0);
+      ir[r] = min(lane + 32 * r, N - 1);
+      ad[r] = pk(ir[r], 0);
     }
 #pragma unroll 2
     for (int j = 0; j < N; ++j) {
       const double xj = xs[warp][j];
-      const int cb = pk(j, 0);
 #pragma unroll
       for (int r = 0; r < R; ++r) {
-        const int i = min(lane + 32 * r, N - 1);
-        acc[r] = fma(P[j <= i ? rowb[r] + j : cb + i], xj, acc[r]);
+        acc[r] = fma(P[ad[r]], xj, acc[r]);
+        ad[r] += j < ir[r] ? 1 : j + 1;
       }
     }
     __syncwarp();
@@ -245,16 +246,20 @@ __global__ void __launch_bounds__(W * 32)
     const double* X = stage + s * LEN;
     const double* Sinv = X + XL;
     double a[RI];
+    int ad[RI], ir[RI];
 #pragma unroll
-    for (int q = 0; q < RI; ++q) a[q] = 0.0;
+    for (int q = 0; q < RI; ++q) {
+      a[q] = 0.0;
+      ir[q] = min(lane + 32 * q, NI - 1);
+      ad[q] = pk(ir[q], 0);
+    }
 #pragma unroll 2
-    for (int j = 0; j < NI; ++j) {
+    for (int j = 0; j < NI; ++j) {   // packed walk as in elem_apply_kernel
       const double xj = ro[warp][j];
-      const int cb = pk(j, 0);
 #pragma unroll
       for (int q = 0; q < RI; ++q) {
-        const int i = min(lane + 32 * q, NI - 1);
-        a[q] = fma(Sinv[j <= i ? pk(i, 0) + j : cb + i], xj, a[q]);
+        a[q] = fma(Sinv[ad[q]], xj, a[q]);
+        ad[q] += j < ir[q] ? 1 : j + 1;
       }
     }
     double c[RC];
@@ -427,7 +432,9 @@ static int launch_apply(const double* M, const int* codes, const double* x, doub
   // aim for ~64-96 KB of bulk copies in flight per SM
   // measured on B200 (tools/apply_variants.cu): warps in flight matter more
   // than per-warp ring depth; one stage per warp, 8 warps, fills the SM
-  // (3 CTAs/SM at k = 4: 66% of HBM; k = 6: 69%)
+  // (3 CTAs/SM at k = 4: 66% of HBM; k = 6: 69%).  A CTA-wide ring with one
+  // producer thread and 16 consumer warps (28 records in flight per SM) was
+  // measured slower (62.5 vs 58.4 us at cfg2); so was 2-stage x 4 warps.
   constexpr int W = 8;
   constexpr int NST = 1;
   auto kern = elem_apply_kernel<N, STRIDE, W, NST>;

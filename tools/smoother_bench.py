@@ -21,11 +21,13 @@ nc = sys_.maps.n_cpl_free
 r = torch.randn(nc, dtype=torch.float64, device="cuda")
 x = torch.empty_like(r)
 flush = torch.empty(256 * 2 ** 17, dtype=torch.float64, device="cuda")
+flush_rd = torch.ones(256 * 2 ** 17, dtype=torch.float64, device="cuda")   # as bench.py l2_flush
 for _ in range(5):
     sm.jacobi_apply(r, out=x)
 ts = []
 for i in range(50):
     flush.fill_(float(i))
+    flush_rd.sum()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e0.record()
     sm.jacobi_apply(r, out=x)
@@ -38,3 +40,23 @@ byt = sm.nblk * 8 * b * (b + 1) / 2 + 16 * nc
 t = float(np.median(ts))
 print(f"variant {os.environ.get('MCS_JAC_VARIANT', '0')}: jacobi {t:.2f} us  "
       f"{byt / t / 1e3:.0f} GB/s  ({byt / t / 1e3 / 6537:.2f} of HBM)")
+
+# condensed S apply (A6) alone, same protocol (bench.py apply_ms)
+from paper_2207_08481_b200.operators import SOperator  # noqa: E402
+S = SOperator(sys_)
+xs = torch.randn(sys_.maps.n_vv_free, dtype=torch.float64, device="cuda")
+ys = torch.empty_like(xs)
+for _ in range(5):
+    S.apply(xs, out=ys)
+ta = []
+for i in range(50):
+    flush.fill_(float(i))
+    flush_rd.sum()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    S.apply(xs, out=ys)
+    e1.record()
+    torch.cuda.synchronize()
+    ta.append(e0.elapsed_time(e1) * 1e3)
+t = float(np.median(ta))
+print(f"S apply {t:.2f} us")
