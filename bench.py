@@ -168,6 +168,17 @@ def flops_structured(k):
     return gen + fac + y + syrk + ds
 
 
+def max_over_ranks(x: float, world: int, device) -> float:
+    """Whole-job time of N replicas: the maximum over ranks (all_reduce MAX on
+    the process group's device; identity for one rank)."""
+    if world <= 1:
+        return x
+    import torch
+    t = torch.tensor([x], dtype=torch.float64, device=device)
+    torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+    return float(t.item())
+
+
 def run_ours(args, rank, world):
     import torch
     from paper_2207_08481_b200 import _abi, engine, refblocks
@@ -262,11 +273,7 @@ def run_ours(args, rank, world):
     t_a3 = np.array([e[1].elapsed_time(e[2]) for e in evs])
     t_a4 = np.array([e[2].elapsed_time(e[3]) for e in evs])
     t_step = t_a1 + t_a3 + t_a4
-    ms_per_step = float(t_step.mean())
-    if world > 1:
-        t = torch.tensor([ms_per_step], device=dev)
-        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
-        ms_per_step = float(t.item())
+    ms_per_step = max_over_ranks(float(t_step.mean()), world, dev)
     value = world * nt / (ms_per_step * 1e-3)
 
     # ---- condensed-operator apply (A6) and PCG (A8-A13), same run
@@ -362,11 +369,7 @@ def run_ours(args, rank, world):
         torch.cuda.synchronize()
         if i >= 2:
             e2e_times.append(e0.elapsed_time(e1))
-    e2e_ms = float(np.mean(e2e_times))
-    if world > 1:   # whole-job e2e: the slowest replica
-        t = torch.tensor([e2e_ms], device=dev)
-        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
-        e2e_ms = float(t.item())
+    e2e_ms = max_over_ranks(float(np.mean(e2e_times)), world, dev)   # the slowest replica
 
     # ---- config-5 microbench (SPD Schur S = B^T A^-1 B, n_s=60, n_c=36)
     micro = run_microbench(args, dev) if args.micro else None
