@@ -19,6 +19,7 @@ exact factorisation).
 
 from __future__ import annotations
 
+import os
 from dataclasses import dataclass
 from typing import List
 
@@ -267,6 +268,10 @@ class _DevCsr:
         return y
 
 
+# MCS_NO_FORK=1: A/B switch, additive ASP smoother and coarse chain in one stream
+FORK_ADDITIVE = os.environ.get("MCS_NO_FORK", "0") != "1"
+
+
 class AspPreconditioner:
     """Smoother + embedded exact coarse correction (reference `:286-336`)."""
 
@@ -281,6 +286,7 @@ class AspPreconditioner:
         self.n = n
         self._t, self._w = empty(n), empty(n)
         self._u, self._v = empty(nc), empty(nc)
+        self._side = self._ev = None
         self.jacobi_scale = 1.0
         if mode == "multiplicative":
             self.jacobi_scale = self._estimate_smoother_bound()
@@ -309,7 +315,24 @@ class AspPreconditioner:
     def apply(self, r, out=None):
         rd, host = as_device(r)
         x = out if out is not None else empty(self.n)
-        if self.mode == "additive":
+        if self.mode == "additive" and FORK_ADDITIVE:
+            # the smoother and the coarse chain are independent until the
+            # final x += E v: the smoother runs on a side stream (a graph
+            # branch under capture) while E^T r and the coarse solve run here
+            torch = __import__("torch")
+            main = torch.cuda.current_stream()
+            if self._side is None:
+                self._side = torch.cuda.Stream()
+                self._ev = (torch.cuda.Event(), torch.cuda.Event())
+            self._ev[0].record(main)
+            self._side.wait_event(self._ev[0])
+            self.smoother.jacobi_apply(rd, out=x, stream=self._side)
+            self._ev[1].record(self._side)
+            self.Et.mv(rd, self._u)
+            self.coarse.solve_dev(self._u, self._v)
+            main.wait_event(self._ev[1])
+            self.E.mv(self._v, x, 1.0, 1.0)
+        elif self.mode == "additive":
             self.smoother.jacobi_apply(rd, out=x)
             self.coarse_correction(rd, x, 1.0)
         else:
