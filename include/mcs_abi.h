@@ -196,6 +196,13 @@ int mcs_dot(int64_t n, const double* x, const double* y, double* partials, unsig
             double* out, void* stream);
 int mcs_cg_update(int64_t n, double* x, double* r, const double* p, const double* Ap, double* sc,
                   int rz, int pap, int rr, double* partials, unsigned* counter, void* stream);
+/* the same with a stop gate, for several PCG steps per CUDA graph: a no-op
+ * when sc[gate_in] != 0 (gate_in >= 0); sets sc[gate_out] = 1 when
+ * !(sc[pap] > 0) or sqrt(sc[rr]) / sc[bnorm_i] <= sc[rtol_i] (gate_out >= 0) */
+int mcs_cg_update_gated(int64_t n, double* x, double* r, const double* p, const double* Ap,
+                        double* sc, int rz, int pap, int rr, int gate_in, int gate_out,
+                        int bnorm_i, int rtol_i, double* partials, unsigned* counter,
+                        void* stream);
 int mcs_xpby(int64_t n, const double* z, double* p, const double* sc, int num, int den,
              void* stream);
 int mcs_axpby(int64_t n, double a, const double* x, double b, double* y, void* stream);

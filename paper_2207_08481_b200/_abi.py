@@ -69,6 +69,7 @@ SIGNATURES = {
     "mcs_reduce_workspace_len": [],
     "mcs_dot": [_l, _p, _p, _p, _p, _p, _p],
     "mcs_cg_update": [_l, _p, _p, _p, _p, _p, _i, _i, _i, _p, _p, _p],
+    "mcs_cg_update_gated": [_l, _p, _p, _p, _p, _p, _i, _i, _i, _i, _i, _i, _i, _p, _p, _p],
     "mcs_xpby": [_l, _p, _p, _p, _i, _i, _p],
     "mcs_axpby": [_l, _d, _p, _d, _p, _p],
 }

@@ -35,7 +35,8 @@ __device__ __forceinline__ double block_sum(double v) {
 // strided assignment + the fixed block_sum tree: deterministic).  Partials
 // are read through L2 (ld.global.cg) after the fence, batched, instead of
 // one volatile round trip at a time.
-__device__ __forceinline__ void finish(double part, double* partials, unsigned* counter,
+// Returns true in thread 0 of the last block, after *out is written.
+__device__ __forceinline__ bool finish(double part, double* partials, unsigned* counter,
                                        double* out) {
   __shared__ bool last;
   if (threadIdx.x == 0) {
@@ -44,7 +45,7 @@ __device__ __forceinline__ void finish(double part, double* partials, unsigned* 
     last = atomicAdd(counter, 1u) == gridDim.x - 1;
   }
   __syncthreads();
-  if (!last) return;
+  if (!last) return false;
   __threadfence();
   double s = 0.0;
   for (int b = threadIdx.x; b < (int)gridDim.x; b += RED_THREADS) s += __ldcg(partials + b);
@@ -52,7 +53,9 @@ __device__ __forceinline__ void finish(double part, double* partials, unsigned* 
   if (threadIdx.x == 0) {
     *out = s;
     *counter = 0u;
+    return true;
   }
+  return false;
 }
 
 __global__ void __launch_bounds__(RED_THREADS)
@@ -69,12 +72,19 @@ __global__ void __launch_bounds__(RED_THREADS)
 }
 
 // alpha = sc[rz]/sc[pap];  x += alpha p;  r -= alpha Ap;  sc[rr] = r.r
+// Gating (several PCG steps per CUDA graph, krylov.py): gate_in >= 0 and
+// sc[gate_in] != 0 -> the step is a no-op (the previous step stopped the
+// loop); gate_out >= 0 -> sc[gate_out] = 1 when this step stops the loop,
+// with the host's own test: !(pAp > 0) or sqrt(rr) / bnorm <= rtol (IEEE
+// sqrt and division, so device and host decide identically).
 __global__ void __launch_bounds__(RED_THREADS)
     cg_update_kernel(int64_t n, double* __restrict__ x, double* __restrict__ r,
                      const double* __restrict__ p, const double* __restrict__ Ap, double* sc,
-                     int rz, int pap, int rr, double* partials, unsigned* counter) {
+                     int rz, int pap, int rr, int gate_in, int gate_out, int bnorm_i, int rtol_i,
+                     double* partials, unsigned* counter) {
   pdl_wait();
   pdl_trigger();
+  if (gate_in >= 0 && sc[gate_in] != 0.0) return;
   const double alpha = sc[rz] / sc[pap];
   double s = 0.0;
   for (int64_t i = (int64_t)blockIdx.x * RED_THREADS + threadIdx.x; i < n;
@@ -85,7 +95,10 @@ __global__ void __launch_bounds__(RED_THREADS)
     s = fma(ri, ri, s);
   }
   s = block_sum(s);
-  finish(s, partials, counter, sc + rr);
+  if (finish(s, partials, counter, sc + rr) && gate_out >= 0) {
+    const double rrv = sc[rr], pv = sc[pap];
+    sc[gate_out] = (!(pv > 0.0) || __dsqrt_rn(rrv) / sc[bnorm_i] <= sc[rtol_i]) ? 1.0 : 0.0;
+  }
 }
 
 // p = z + (sc[num]/sc[den]) p
@@ -146,7 +159,16 @@ MCS_API int mcs_cg_update(int64_t n, double* x, double* r, const double* p, cons
                           int rz, int pap, int rr, double* partials, unsigned* counter, void* stream) {
   auto st = static_cast<cudaStream_t>(stream);
   return launch_pdl_g(PDL_BLAS, cg_update_kernel, RED_BLOCKS, RED_THREADS, 0, st, n, x, r, p, Ap, sc, rz, pap,
-                    rr, partials, counter);
+                    rr, -1, -1, 0, 0, partials, counter);
+}
+
+MCS_API int mcs_cg_update_gated(int64_t n, double* x, double* r, const double* p, const double* Ap,
+                                double* sc, int rz, int pap, int rr, int gate_in, int gate_out,
+                                int bnorm_i, int rtol_i, double* partials, unsigned* counter,
+                                void* stream) {
+  auto st = static_cast<cudaStream_t>(stream);
+  return launch_pdl_g(PDL_BLAS, cg_update_kernel, RED_BLOCKS, RED_THREADS, 0, st, n, x, r, p, Ap, sc, rz, pap,
+                    rr, gate_in, gate_out, bnorm_i, rtol_i, partials, counter);
 }
 
 MCS_API int mcs_xpby(int64_t n, const double* z, double* p, const double* sc, int num, int den,

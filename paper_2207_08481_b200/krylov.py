@@ -58,7 +58,7 @@ class _PcgState:
         f64 = dict(dtype=torch.float64, device="cuda")
         self.x, self.r, self.p = (torch.zeros(n, **f64) for _ in range(3))
         self.z, self.Ap = torch.zeros(n, **f64), torch.zeros(n, **f64)
-        self.graphs = None
+        self.graphs = self.pair = None
 
     def precond(self):
         if self.M is None:
@@ -66,17 +66,19 @@ class _PcgState:
         else:
             _apply(self.M, self.r, self.z)
 
-    def step(self, rz, rz_new):
+    def step(self, rz, rz_new, pap=None, rr=None, gate_in=-1, gate_out=-1):
         ws = workspace()
         st = _abi.stream()
+        pap = ws.PAP if pap is None else pap
+        rr = ws.RR if rr is None else rr
         if hasattr(self.A, "apply_dot") and not _NO_FUSED_PAP:   # p'Ap inside the apply kernel
-            self.A.apply_dot(self.p, self.Ap, ws.PAP)
+            self.A.apply_dot(self.p, self.Ap, pap)
         else:
             _apply(self.A, self.p, self.Ap)
-            ws.dot(self.p, self.Ap, ws.PAP)
-        _abi.call("mcs_cg_update", self.n, _abi.ptr(self.x), _abi.ptr(self.r), _abi.ptr(self.p),
-                  _abi.ptr(self.Ap), _abi.ptr(ws.sc), rz, ws.PAP, ws.RR, _abi.ptr(ws.partials),
-                  _abi.ptr(ws.counter), st)
+            ws.dot(self.p, self.Ap, pap)
+        _abi.call("mcs_cg_update_gated", self.n, _abi.ptr(self.x), _abi.ptr(self.r),
+                  _abi.ptr(self.p), _abi.ptr(self.Ap), _abi.ptr(ws.sc), rz, pap, rr, gate_in,
+                  gate_out, ws.BNORM, ws.RTOL, _abi.ptr(ws.partials), _abi.ptr(ws.counter), st)
         self.precond()
         ws.dot(self.r, self.z, rz_new)
         _abi.call("mcs_xpby", self.n, _abi.ptr(self.z), _abi.ptr(self.p), _abi.ptr(ws.sc),
@@ -99,15 +101,24 @@ class _PcgState:
                 with torch.cuda.graph(g, stream=side):
                     self.step(rz, rzn)
                 graphs.append(g)
+            # two steps per replay: the second is gated off on the device when
+            # the first one stops the loop (one host read-back per two steps)
+            pair = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(pair, stream=side):
+                self.step(ws.RZ0, ws.RZ1, gate_out=ws.GATE)
+                self.step(ws.RZ1, ws.RZ0, ws.PAP2, ws.RR2, gate_in=ws.GATE)
         cur.wait_stream(side)
         for t, v in zip((self.x, self.r, self.p, self.z, ws.sc), saved):
             t.copy_(v)
         self.graphs = graphs
+        self.pair = None if _NO_PAIR else pair
 
 
 _STATES = {}
 # A/B switch for the fused curvature (MCS_NO_FUSED_PAP=1: separate dot kernel)
 _NO_FUSED_PAP = __import__("os").environ.get("MCS_NO_FUSED_PAP", "0") == "1"
+# A/B switch for the two-step graph (MCS_NO_PAIR=1: one read-back per step)
+_NO_PAIR = __import__("os").environ.get("MCS_NO_PAIR", "0") == "1"
 
 
 def cg(apply_A, b, apply_M=None, rtol=1e-8, maxit=1000, stream=None, use_graph=True):
@@ -117,11 +128,15 @@ def cg(apply_A, b, apply_M=None, rtol=1e-8, maxit=1000, stream=None, use_graph=T
 
     When both operators are this package's device operators, one PCG step
     (A p, p'Ap, the x/r update with ||r||^2, z = M r, r'z, the p update) is
-    captured into a CUDA graph per parity of the rz slot (once per operator
-    pair, cached) and replayed: one graph launch and one 16-byte read-back
-    per iteration.  The step computes z = M r before the host has seen the
-    stopping test; when the test then stops the loop that z is unused, so x,
-    the residual history and the iteration count are the reference loop's."""
+    captured into CUDA graphs (once per operator pair, cached).  The main
+    graph holds TWO steps: the first one's x/r update kernel evaluates the
+    host's stopping test (negative curvature, or sqrt(rr)/bnorm <= rtol,
+    same IEEE operations) into a device gate, and the second step's update
+    is a no-op when the gate is set, so one graph launch and one read-back
+    serve two iterations (single-step graphs per rz parity finish an odd
+    maxit).  A step computes z = M r before the host has seen the stopping
+    test; when the test stops the loop that z is unused, so x, the residual
+    history and the iteration count are the reference loop's."""
     import os
     bd, host = as_device(b)
     n = bd.numel()
@@ -152,21 +167,31 @@ def cg(apply_A, b, apply_M=None, rtol=1e-8, maxit=1000, stream=None, use_graph=T
     if graphable and S.graphs is None and maxit > 2:
         S.capture()
     rz, rz_new = ws.RZ0, ws.RZ1
-    for it in range(1, maxit + 1):
-        if S.graphs is not None:
-            S.graphs[0 if rz == ws.RZ0 else 1].replay()
+    sc[ws.BNORM] = bnorm
+    sc[ws.RTOL] = rtol
+    it = 0
+    while it < maxit and not report.converged:
+        if S.pair is not None and rz == ws.RZ0 and it + 2 <= maxit:
+            S.pair.replay()
+            v = sc[ws.PAP:ws.RR2 + 1].tolist()
+            steps = ((v[0], v[1]), (v[ws.PAP2 - ws.PAP], v[ws.RR2 - ws.PAP]))
         else:
-            S.step(rz, rz_new)
-        pap, rr = sc[ws.PAP:ws.RR + 1].tolist()
-        if pap <= 0:
-            raise NegativeCurvatureError(f"p'Ap = {pap:.3e} at iteration {it}")
-        res = float(np.sqrt(rr) / bnorm)
-        report.residuals.append(res)
-        report.iterations = it
-        if res <= rtol:
-            report.converged = True
-            break
-        rz, rz_new = rz_new, rz
+            if S.graphs is not None:
+                S.graphs[0 if rz == ws.RZ0 else 1].replay()
+            else:
+                S.step(rz, rz_new)
+            steps = (tuple(sc[ws.PAP:ws.RR + 1].tolist()),)
+        for pap, rr in steps:
+            it += 1
+            if pap <= 0:
+                raise NegativeCurvatureError(f"p'Ap = {pap:.3e} at iteration {it}")
+            res = float(np.sqrt(rr) / bnorm)
+            report.residuals.append(res)
+            report.iterations = it
+            if res <= rtol:
+                report.converged = True
+                break
+            rz, rz_new = rz_new, rz
     x = S.x.clone()
     return (x.cpu().numpy() if host else x), report
 
