@@ -107,6 +107,31 @@ def test_pcg_bitwise_reproducible(cuda):
     assert np.array_equal(x1, x2)
 
 
+@pytest.mark.parametrize("comp", ["additive", "multiplicative"])
+def test_pcg_two_step_graph_matches_eager(cuda, comp):
+    """The two-steps-per-graph loop with its device stop gate against eager
+    launches: stopping on the first step of a pair (odd iteration count),
+    on the second, and at an odd maxit give the same iterations, residual
+    history and x, bit for bit."""
+    g = golden("c2_n3")
+    prob, fes, sys_ = _system(g)
+    M = velocity_preconditioner(fes, sys_, prob.nu, SolverOptions(composition=comp))
+    S = SOperator(sys_)
+    b = condensed_rhs(fes, sys_)[0]
+    _, full = cg(S, b, M, rtol=1e-10, maxit=1000, use_graph=False)
+    res = full.residuals
+    for parity in (1, 0):     # a new running minimum at an odd / even iteration
+        k = next(k for k in range(3, len(res)) if k % 2 == parity and res[k] < min(res[:k]))
+        xe, re = cg(S, b, M, rtol=res[k], maxit=1000, use_graph=False)
+        xg, rg = cg(S, b, M, rtol=res[k], maxit=1000)
+        assert re.iterations == rg.iterations == k and re.converged and rg.converged
+        assert re.residuals == rg.residuals and np.array_equal(xe, xg)
+    xe, re = cg(S, b, M, rtol=1e-30, maxit=7, use_graph=False)
+    xg, rg = cg(S, b, M, rtol=1e-30, maxit=7)
+    assert rg.iterations == 7 and not rg.converged
+    assert re.residuals == rg.residuals and np.array_equal(xe, xg)
+
+
 @pytest.mark.parametrize("cfg,n,leaf", [(1, 16, 48), (2, 40, 128), (3, 24, 96)])
 def test_multifrontal_coarse_solve_exact(cuda, cfg, n, leaf):
     """GPU multifrontal triangular solves vs a direct sparse solve."""
