@@ -267,21 +267,27 @@ def gmres(apply_A, b, apply_M=None, rtol=1e-6, maxit=500, project=None, x0=None)
         if project is not None:
             w = project(w)
         m = j + 1
-        wnorm = _norm(ws, w)
         # classical Gram-Schmidt, repeated once when the first pass lost more
         # than half the norm (DGKS criterion 1/sqrt(2)): MGS-quality
-        # orthogonality at the cost of one or two V w / V^T h pairs per step
-        h2.zero_()
-        for hh in (h1, h2):
+        # orthogonality at the cost of one or two V w / V^T h pairs per step.
+        # ||w|| before and after the pass and the h column come back in ONE
+        # read-back (a second one only when the second pass runs).
+        ws.dot(w, w, ws.TMP)
+        _abi.call("mcs_mdot", m, n, n, _abi.ptr(V), _abi.ptr(w), _abi.ptr(partial),
+                  _abi.ptr(h1), _abi.stream(None))
+        _abi.call("mcs_gemv_acc", m, n, n, _abi.ptr(V), _abi.ptr(h1), -1.0, 1.0,
+                  _abi.ptr(w), _abi.stream(None))
+        ws.dot(w, w, ws.TMP2)
+        back = torch.cat((ws.sc[ws.TMP:ws.TMP2 + 1], h1[:m])).cpu().numpy()
+        wnorm, hnext = float(np.sqrt(back[0])), float(np.sqrt(back[ws.TMP2 - ws.TMP]))
+        hcol = back[ws.TMP2 - ws.TMP + 1:]
+        if not hnext > 0.7071067811865476 * wnorm:
             _abi.call("mcs_mdot", m, n, n, _abi.ptr(V), _abi.ptr(w), _abi.ptr(partial),
-                      _abi.ptr(hh), _abi.stream(None))
-            _abi.call("mcs_gemv_acc", m, n, n, _abi.ptr(V), _abi.ptr(hh), -1.0, 1.0,
+                      _abi.ptr(h2), _abi.stream(None))
+            _abi.call("mcs_gemv_acc", m, n, n, _abi.ptr(V), _abi.ptr(h2), -1.0, 1.0,
                       _abi.ptr(w), _abi.stream(None))
             hnext = _norm(ws, w)
-            if hnext > 0.7071067811865476 * wnorm:
-                break
-            wnorm = hnext
-        hcol = (h1[:m] + h2[:m]).cpu().numpy()
+            hcol = hcol + h2[:m].cpu().numpy()
         H[:m, j] = hcol
         H[j + 1, j] = hnext
         if not np.isfinite(hnext) or not np.all(np.isfinite(hcol)):

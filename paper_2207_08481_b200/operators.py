@@ -38,6 +38,7 @@ class Workspace:
 
     RZ0, RZ1, PAP, RR, BB, TMP = 0, 1, 2, 3, 4, 5
     PAP2, RR2, GATE, BNORM, RTOL = 6, 7, 8, 9, 10   # second step of a graphed pair
+    TMP2 = 11
 
     def __init__(self):
         torch = torch_mod()
