@@ -330,36 +330,59 @@ __global__ void __launch_bounds__(W * 32)
     c0[q] = (c < NC && gw < nt) ? __ldg(ccodes + gw * NC + c) : -1;
     c1[q] = (c < NC && gw + nw < nt) ? __ldg(ccodes + (gw + nw) * NC + c) : -1;
   }
+  // static indices of the first element before the wait: bubble targets
+  // and the scatter targets of the coupling dofs
+  int bin[RI], cvn[RC];
+#pragma unroll
+  for (int q = 0; q < RI; ++q) {
+    const int i = lane + 32 * q;
+    bin[q] = (i < NI && gw < nt) ? __ldg(bidx + gw * NI + i) : 0;
+  }
+#pragma unroll
+  for (int q = 0; q < RC; ++q) cvn[q] = c0[q] >= 0 ? __ldg(c2v + code_index(c0[q])) : 0;
   pdl_wait();
   pdl_trigger();
+  double bubn[RI];
 #pragma unroll
   for (int q = 0; q < RC; ++q) zv[q] = gather_signed(zc, c0[q]);
+#pragma unroll
+  for (int q = 0; q < RI; ++q) {
+    const int i = lane + 32 * q;
+    bubn[q] = (i < NI && gw < nt) ? bubble[gw * NI + i] : 0.0;
+  }
   int it = 0;
   for (int64_t e = gw; e < nt; e += nw, ++it) {
     const int s = it % NST;
+    double bub[RI];
+    int bi[RI];
+#pragma unroll
+    for (int q = 0; q < RI; ++q) {
+      bub[q] = bubn[q];
+      bi[q] = bin[q];
+    }
 #pragma unroll
     for (int q = 0; q < RC; ++q) {
       const int c = lane + 32 * q;
       if (c < NC) zl[warp][c] = zv[q];
       // the coupling part of out = z_c (the ExtendedAsp scatter, fused):
       // a dof shared by two elements receives the same value twice
-      if (c0[q] >= 0) out[__ldg(c2v + code_index(c0[q]))] = code_sign(c0[q]) * zv[q];
+      if (c0[q] >= 0) out[cvn[q]] = code_sign(c0[q]) * zv[q];
     }
-    const int64_t e2 = e + 2 * nw;
+    // next element's gathers, bubble entries and indices one element ahead
+    const int64_t e1 = e + nw, e2 = e + 2 * nw;
 #pragma unroll
     for (int q = 0; q < RC; ++q) {
       const int c = lane + 32 * q;
       zv[q] = gather_signed(zc, c1[q]);
+      cvn[q] = c1[q] >= 0 ? __ldg(c2v + code_index(c1[q])) : 0;
       c0[q] = c1[q];
       c1[q] = (c < NC && e2 < nt) ? __ldg(ccodes + e2 * NC + c) : -1;
     }
-    double bub[RI];
-    int bi[RI];
 #pragma unroll
     for (int q = 0; q < RI; ++q) {
       const int i = lane + 32 * q;
-      bub[q] = i < NI ? bubble[e * NI + i] : 0.0;
-      bi[q] = i < NI ? __ldg(bidx + e * NI + i) : 0;
+      bubn[q] = (i < NI && e1 < nt) ? bubble[e1 * NI + i] : 0.0;
+      bin[q] = (i < NI && e1 < nt) ? __ldg(bidx + e1 * NI + i) : 0;
     }
     __syncwarp();
     mbar_wait(&bar[s], (it / NST) & 1);
