@@ -20,8 +20,6 @@
 
 namespace mcs {
 
-constexpr int WARPS = 4;
-
 struct WarpRing {
   uint64_t bar[2];
 };
@@ -436,16 +434,6 @@ static int sm_count() {
     cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
   }
   return n;
-}
-
-template <class Kern>
-static int warp_grid(Kern k, size_t smem, int64_t nt) {
-  int per_sm = 1;
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k, WARPS * 32, smem);
-  if (per_sm < 1) per_sm = 1;
-  const int64_t want = (nt + WARPS - 1) / WARPS;
-  const int64_t g = (int64_t)per_sm * sm_count();
-  return (int)(want < g ? want : g);
 }
 
 template <int N, int STRIDE>
