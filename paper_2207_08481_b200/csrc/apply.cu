@@ -8,8 +8,9 @@
 //      prolong:   out_o = bubble_T - X z_c
 //
 // One warp per element.  The element's packed matrix (or ext record) moves
-// HBM -> shared memory with a 1-D bulk async copy into a 2-stage per-warp ring
-// so the next element streams in while the current one is multiplied.  Each
+// HBM -> shared memory with a 1-D bulk async copy into a per-warp stage ring
+// (one stage at k = 4: measured best, see launch_apply) while the next
+// element's indices and gathered values are prefetched into registers.  Each
 // lane owns rows l, l+32, ...; the symmetric packed entry (i, j) is read at
 // pk(max, min) (triangular-number addressing is bank-conflict free for 32
 // consecutive rows).  Scatter targets are free-dof indices with the sign in
@@ -19,10 +20,6 @@
 #include "common.cuh"
 
 namespace mcs {
-
-struct WarpRing {
-  uint64_t bar[2];
-};
 
 // Signed gather x_loc[j] = sign * x[idx] (0 for constrained dofs).
 __device__ __forceinline__ double gather_signed(const double* x, int c) {
