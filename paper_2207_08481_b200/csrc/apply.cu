@@ -453,7 +453,7 @@ static int launch_apply(const double* M, const int* codes, const double* x, doub
   if (per_sm < 1) per_sm = 1;
   const int64_t want = (nt + W - 1) / W;
   const int64_t g = (int64_t)per_sm * sm_count();
-  return launch_pdl_g(PDL_ELEM, kern, (int)(want < g ? want : g), W * 32, smem, st, M, codes, x, y, nt,
+  return launch_pdl_g(PDL_APPLY, kern, (int)(want < g ? want : g), W * 32, smem, st, M, codes, x, y, nt,
                       dpart, dcount, dout);
 }
 

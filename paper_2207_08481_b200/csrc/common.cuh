@@ -51,9 +51,9 @@ __device__ __forceinline__ void pdl_trigger() {
   asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
 }
 
-// kernel groups (MCS_PDL_MASK bit): 1 vector kernels, 2 element operators,
-// 4 smoother / SpMV, 8 coarse solve
-enum PdlGroup { PDL_BLAS = 1, PDL_ELEM = 2, PDL_PREC = 4, PDL_COARSE = 8 };
+// kernel groups (MCS_PDL_MASK bit): 1 vector kernels, 2 ExtendedAsp element
+// kernels, 4 smoother / SpMV, 8 coarse solve, 16 the S / S_d element apply
+enum PdlGroup { PDL_BLAS = 1, PDL_ELEM = 2, PDL_PREC = 4, PDL_COARSE = 8, PDL_APPLY = 16 };
 bool pdl_enabled(int group);
 
 template <class... KArgs, class... Args>
