@@ -131,10 +131,11 @@ bool mcs::pdl_enabled(int group) {
   if (mask < 0) {
     const char* e = getenv("MCS_NO_PDL");
     const char* m = getenv("MCS_PDL_MASK");
-    // default 13: PDL for the vector, smoother/SpMV and coarse kernels; the
-    // element kernels launch normally (early-launched element kernels pin
-    // 3 CTAs/SM of shared memory while they wait: measured ~1% slower)
-    mask = (e && e[0] == '1') ? 0 : (m ? atoi(m) : 13);
+    // default 29: every group but the ExtendedAsp element kernels (launched
+    // early they pin 3 CTAs/SM of shared memory while they wait: measured
+    // ~1% slower on the multiplicative PCG; the S / S_d apply keeps PDL,
+    // 60.4 vs 62.4 us standalone)
+    mask = (e && e[0] == '1') ? 0 : (m ? atoi(m) : 29);
   }
   return (mask & group) != 0;
 }
