@@ -207,6 +207,19 @@ int mcs_xpby(int64_t n, const double* z, double* p, const double* sc, int num, i
              void* stream);
 int mcs_axpby(int64_t n, double a, const double* x, double b, double* y, void* stream);
 
+/* ---- A13 PCG loop as one CUDA graph (csrc/pcg_loop.cu) ------------------
+ * Replaces the host iteration loop of krylov.py:103-137 (one Python
+ * iteration per step) with a conditional WHILE graph around the captured
+ * two-step PCG graph `pair_graph` (a cudaGraph_t).  After each pair a record
+ * kernel appends (sc[pap], sc[rr]) of the steps that ran to `hist`
+ * ([0] steps, [1] maxit, then two doubles per step, room for `cap` steps) and
+ * stops the loop on !(p'Ap > 0), sqrt(rr) / sc[bnorm_i] <= sc[rtol_i], or
+ * maxit.  build: *exec_out = the instantiated graph (cudaGraphExec_t). */
+int mcs_pcg_loop_build(void* pair_graph, const double* sc, double* hist, int pap, int rr,
+                       int pap2, int rr2, int bnorm_i, int rtol_i, int cap, void** exec_out);
+int mcs_pcg_loop_launch(void* exec, double* hist, int maxit, void* stream);
+int mcs_pcg_loop_destroy(void* exec);
+
 #ifdef __cplusplus
 }
 #endif

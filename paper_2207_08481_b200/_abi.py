@@ -72,6 +72,10 @@ SIGNATURES = {
     "mcs_cg_update_gated": [_l, _p, _p, _p, _p, _p, _i, _i, _i, _i, _i, _i, _i, _p, _p, _p],
     "mcs_xpby": [_l, _p, _p, _p, _i, _i, _p],
     "mcs_axpby": [_l, _d, _p, _d, _p, _p],
+    # pcg_loop.cu
+    "mcs_pcg_loop_build": [_p, _p, _p, _i, _i, _i, _i, _i, _i, _i, _p],
+    "mcs_pcg_loop_launch": [_p, _p, _i, _p],
+    "mcs_pcg_loop_destroy": [_p],
 }
 
 _lib = None

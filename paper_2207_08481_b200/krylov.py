@@ -58,7 +58,7 @@ class _PcgState:
         f64 = dict(dtype=torch.float64, device="cuda")
         self.x, self.r, self.p = (torch.zeros(n, **f64) for _ in range(3))
         self.z, self.Ap = torch.zeros(n, **f64), torch.zeros(n, **f64)
-        self.graphs = self.pair = None
+        self.graphs = self.pair = self.loop = None
 
     def precond(self):
         if self.M is None:
@@ -103,15 +103,33 @@ class _PcgState:
                 graphs.append(g)
             # two steps per replay: the second is gated off on the device when
             # the first one stops the loop (one host read-back per two steps)
-            pair = torch.cuda.CUDAGraph()
+            pair = torch.cuda.CUDAGraph(keep_graph=True)
             with torch.cuda.graph(pair, stream=side):
                 self.step(ws.RZ0, ws.RZ1, gate_out=ws.GATE)
                 self.step(ws.RZ1, ws.RZ0, ws.PAP2, ws.RR2, gate_in=ws.GATE)
+            pair.instantiate()
         cur.wait_stream(side)
         for t, v in zip((self.x, self.r, self.p, self.z, ws.sc), saved):
             t.copy_(v)
         self.graphs = graphs
         self.pair = None if _NO_PAIR else pair
+        if self.pair is not None and not _NO_LOOP:
+            # the whole loop as one launch: a conditional WHILE node around the
+            # pair graph (csrc/pcg_loop.cu)
+            import ctypes
+            self.hist = torch.zeros(2 + 2 * _LOOP_CAP, dtype=torch.float64, device="cuda")
+            out = ctypes.c_void_p()
+            _abi.call("mcs_pcg_loop_build", pair.raw_cuda_graph(), _abi.ptr(ws.sc),
+                      _abi.ptr(self.hist), ws.PAP, ws.RR, ws.PAP2, ws.RR2, ws.BNORM, ws.RTOL,
+                      _LOOP_CAP, ctypes.byref(out))
+            self.loop = out.value
+
+    def __del__(self):
+        try:
+            if getattr(self, "loop", None):
+                _abi.call("mcs_pcg_loop_destroy", self.loop)
+        except Exception:
+            pass
 
 
 _STATES = {}
@@ -119,6 +137,9 @@ _STATES = {}
 _NO_FUSED_PAP = __import__("os").environ.get("MCS_NO_FUSED_PAP", "0") == "1"
 # A/B switch for the two-step graph (MCS_NO_PAIR=1: one read-back per step)
 _NO_PAIR = __import__("os").environ.get("MCS_NO_PAIR", "0") == "1"
+# A/B switch for the single-launch loop (MCS_NO_LOOP=1: one launch per pair)
+_NO_LOOP = __import__("os").environ.get("MCS_NO_LOOP", "0") == "1"
+_LOOP_CAP = 4096   # steps of device-side (p'Ap, rr) history
 
 
 def cg(apply_A, b, apply_M=None, rtol=1e-8, maxit=1000, stream=None, use_graph=True):
@@ -136,7 +157,11 @@ def cg(apply_A, b, apply_M=None, rtol=1e-8, maxit=1000, stream=None, use_graph=T
     serve two iterations (single-step graphs per rz parity finish an odd
     maxit).  A step computes z = M r before the host has seen the stopping
     test; when the test stops the loop that z is unused, so x, the residual
-    history and the iteration count are the reference loop's."""
+    history and the iteration count are the reference loop's.  By default the
+    pairs themselves run inside ONE launch: a conditional WHILE graph node
+    around the pair graph, with a record kernel that appends each step's
+    (p'Ap, rr) to a device history and applies the same stopping test
+    (csrc/pcg_loop.cu); the host reads the history once per solve."""
     import os
     bd, host = as_device(b)
     n = bd.numel()
@@ -170,6 +195,29 @@ def cg(apply_A, b, apply_M=None, rtol=1e-8, maxit=1000, stream=None, use_graph=T
     sc[ws.BNORM] = bnorm
     sc[ws.RTOL] = rtol
     it = 0
+
+    def record(pap, rr):
+        """The reference loop's per-step control flow; True = stop."""
+        if pap <= 0:
+            raise NegativeCurvatureError(f"p'Ap = {pap:.3e} at iteration {it}")
+        res = float(np.sqrt(rr) / bnorm)
+        report.residuals.append(res)
+        report.iterations = it
+        report.converged = res <= rtol
+        return report.converged
+
+    if S.loop is not None and maxit >= 2:
+        # one launch runs pairs until the device-side test stops; the host
+        # replays the same test over the recorded (p'Ap, rr) history
+        _abi.call("mcs_pcg_loop_launch", S.loop, _abi.ptr(S.hist), min(maxit, _LOOP_CAP),
+                  _abi.stream())
+        ns = int(S.hist[0].item())
+        v = S.hist[2:2 + 2 * ns].tolist()
+        for q in range(ns):
+            it += 1
+            if record(v[2 * q], v[2 * q + 1]):
+                break
+            rz, rz_new = rz_new, rz
     while it < maxit and not report.converged:
         if S.pair is not None and rz == ws.RZ0 and it + 2 <= maxit:
             S.pair.replay()
@@ -183,13 +231,7 @@ def cg(apply_A, b, apply_M=None, rtol=1e-8, maxit=1000, stream=None, use_graph=T
             steps = (tuple(sc[ws.PAP:ws.RR + 1].tolist()),)
         for pap, rr in steps:
             it += 1
-            if pap <= 0:
-                raise NegativeCurvatureError(f"p'Ap = {pap:.3e} at iteration {it}")
-            res = float(np.sqrt(rr) / bnorm)
-            report.residuals.append(res)
-            report.iterations = it
-            if res <= rtol:
-                report.converged = True
+            if record(pap, rr):
                 break
             rz, rz_new = rz_new, rz
     x = S.x.clone()

@@ -132,6 +132,35 @@ def test_pcg_two_step_graph_matches_eager(cuda, comp):
     assert re.residuals == rg.residuals and np.array_equal(xe, xg)
 
 
+def test_pcg_single_launch_loop_matches_pair_loop(cuda, monkeypatch):
+    """The whole PCG loop as one conditional-WHILE graph launch
+    (csrc/pcg_loop.cu) against one launch per pair: same iterations,
+    residual history and x, bit for bit, including a stop on the first step
+    of a pair and a maxit cap below the convergence point."""
+    from paper_2207_08481_b200 import krylov
+    g = golden("c2_n3")
+    prob, fes, sys_ = _system(g)
+    M = velocity_preconditioner(fes, sys_, prob.nu, SolverOptions(composition="additive"))
+    S = SOperator(sys_)
+    b = condensed_rhs(fes, sys_)[0]
+    _, full = cg(S, b, M, rtol=1e-10, maxit=1000, use_graph=False)
+    res = full.residuals
+    k = next(k for k in range(3, len(res)) if k % 2 == 1 and res[k] < min(res[:k]))
+    cases = [(1e-8, 1000), (res[k], 1000), (1e-30, 9)]
+    out = {}
+    for no_loop in (False, True):
+        monkeypatch.setattr(krylov, "_NO_LOOP", no_loop)
+        krylov._STATES.clear()
+        out[no_loop] = [cg(S, b, M, rtol=rt, maxit=mi) for rt, mi in cases]
+        st = next(iter(krylov._STATES.values()))
+        assert (st.loop is None) == no_loop
+    krylov._STATES.clear()
+    for (xa, ra), (xb, rb) in zip(out[False], out[True]):
+        assert ra.iterations == rb.iterations and ra.converged == rb.converged
+        assert ra.residuals == rb.residuals and np.array_equal(xa, xb)
+    assert out[False][1][1].iterations == k and out[False][2][1].iterations == 9
+
+
 @pytest.mark.parametrize("cfg,n,leaf", [(1, 16, 48), (2, 40, 128), (3, 24, 96)])
 def test_multifrontal_coarse_solve_exact(cuda, cfg, n, leaf):
     """GPU multifrontal triangular solves vs a direct sparse solve."""
