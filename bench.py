@@ -359,7 +359,7 @@ def run_ours(args, rank, world):
     # fused path: the elements go through in chunks; chunk c's results leave
     # for the host on a copy stream (its own DMA engine) while chunk c+1 is
     # condensed, so the step costs the PCIe read-back plus one chunk of compute
-    nch = args.e2e_chunks if fused else 1
+    nch = args.e2e_chunks if (fused or gen) else 1
     chk = [0, nt // 3, nt // 2, nt - 1]
     ref_rows = [t[chk].cpu() for t in (ST, ext, Sd)]   # from the full-grid launches above
     bounds = [nt * c // nch for c in range(nch + 1)]
@@ -372,9 +372,14 @@ def run_ours(args, rank, world):
             W[a:b].copy_(W_pin[a:b], non_blocking=True)
             if nch == 1:
                 step()
-            else:
+            elif fused:
                 _abi.call("mcs_condense_fused", k, b - a, _abi.ptr(W[a:b]), W.shape[1],
                           _abi.ptr(tab), _abi.ptr(ST[a:b]), _abi.ptr(ext[a:b]),
+                          _abi.ptr(Sd[a:b]), _abi.ptr(info[a:b]), st)
+            else:   # gen: A1 + A3 kernel, then the double Schur, on the chunk
+                _abi.call("mcs_condense_gen", k, b - a, _abi.ptr(W[a:b]), W.shape[1],
+                          _abi.ptr(tab), _abi.ptr(ST[a:b]), _abi.ptr(info[a:b]), st)
+                _abi.call("mcs_double_schur", k, b - a, _abi.ptr(ST[a:b]), _abi.ptr(ext[a:b]),
                           _abi.ptr(Sd[a:b]), _abi.ptr(info[a:b]), st)
             done[c].record(stream)
             d2h.wait_event(done[c])
