@@ -154,11 +154,15 @@ def test_pcg_single_launch_loop_matches_pair_loop(cuda, monkeypatch):
         out[no_loop] = [cg(S, b, M, rtol=rt, maxit=mi) for rt, mi in cases]
         st = next(iter(krylov._STATES.values()))
         assert (st.loop is None) == no_loop
+        x0, r0 = cg(S, np.zeros_like(b), M)          # b = 0 after the graphs exist
+        assert r0.converged and r0.iterations == 0 and not np.any(x0)
+        out[no_loop].append(cg(S, b, M, rtol=1e-8, maxit=1000))   # state after b = 0
     krylov._STATES.clear()
     for (xa, ra), (xb, rb) in zip(out[False], out[True]):
         assert ra.iterations == rb.iterations and ra.converged == rb.converged
         assert ra.residuals == rb.residuals and np.array_equal(xa, xb)
     assert out[False][1][1].iterations == k and out[False][2][1].iterations == 9
+    assert out[False][3][1].residuals == out[False][0][1].residuals
 
 
 @pytest.mark.parametrize("cfg,n,leaf", [(1, 16, 48), (2, 40, 128), (3, 24, 96)])
