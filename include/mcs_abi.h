@@ -188,6 +188,15 @@ int mcs_mdot(int m, int64_t n, int64_t ld, const double* V, const double* w, dou
              double* h, void* stream);
 int mcs_gemv_acc(int m, int64_t n, int64_t ld, const double* V, const double* h, double alpha,
                  double beta, double* w, void* stream);
+/* the same, skipped (h = 0, w unchanged) when *gate != 0; mcs_gs_gate sets
+ * sc[gate] = 1 when sqrt(sc[after]) > sqrt(sc[before]) / sqrt(2) (the DGKS
+ * test of krylov.py gmres), so the second Gram-Schmidt pass needs no host
+ * decision (replaces the reorthogonalisation branch of krylov.py:25-100) */
+int mcs_mdot_gated(int m, int64_t n, int64_t ld, const double* V, const double* w,
+                   double* partial, double* h, const double* gate, void* stream);
+int mcs_gemv_acc_gated(int m, int64_t n, int64_t ld, const double* V, const double* h,
+                       double alpha, double beta, double* w, const double* gate, void* stream);
+int mcs_gs_gate(double* sc, int before, int after, int gate, void* stream);
 
 /* ---- PCG vector algebra (replaces krylov.py:103-137 NumPy ops); deterministic
  *      reductions into device scalars sc[]. */

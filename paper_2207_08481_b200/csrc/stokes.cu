@@ -64,7 +64,9 @@ constexpr int MD_CHUNKS = 64;
 // partial[i][c] = sum over chunk c of V[i] . w
 __global__ void __launch_bounds__(SK_THREADS)
     mdot_partial_kernel(int64_t n, int64_t ld, const double* __restrict__ V,
-                        const double* __restrict__ w, double* __restrict__ partial) {
+                        const double* __restrict__ w, double* __restrict__ partial,
+                        const double* __restrict__ gate) {
+  if (gate && *gate != 0.0) return;
   const int i = blockIdx.y, c = blockIdx.x;
   const int64_t len = (n + MD_CHUNKS - 1) / MD_CHUNKS;
   const int64_t lo = c * len, hi = lo + len < n ? lo + len : n;
@@ -84,9 +86,13 @@ __global__ void __launch_bounds__(SK_THREADS)
 }
 
 __global__ void mdot_final_kernel(int m, const double* __restrict__ partial,
-                                  double* __restrict__ h) {
+                                  double* __restrict__ h, const double* __restrict__ gate) {
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= m) return;
+  if (gate && *gate != 0.0) {
+    h[i] = 0.0;
+    return;
+  }
   double s = 0.0;
   for (int c = 0; c < MD_CHUNKS; ++c) s += partial[i * MD_CHUNKS + c];
   h[i] = s;
@@ -96,13 +102,21 @@ __global__ void mdot_final_kernel(int m, const double* __restrict__ partial,
 __global__ void __launch_bounds__(SK_THREADS)
     gemv_acc_kernel(int m, int64_t n, int64_t ld, const double* __restrict__ V,
                     const double* __restrict__ h, double alpha, double beta,
-                    double* __restrict__ w) {
+                    double* __restrict__ w, const double* __restrict__ gate) {
+  if (gate && *gate != 0.0) return;
   for (int64_t k = (int64_t)blockIdx.x * SK_THREADS + threadIdx.x; k < n;
        k += (int64_t)gridDim.x * SK_THREADS) {
     double s = 0.0;
     for (int i = 0; i < m; ++i) s = fma(__ldg(h + i), V[i * ld + k], s);
     w[k] = beta == 0.0 ? alpha * s : fma(alpha, s, beta * w[k]);
   }
+}
+
+// DGKS test of classical Gram-Schmidt on the device (krylov.py gmres): the
+// second pass is skipped (sc[g] = 1) when ||w_after|| > ||w_before|| / sqrt(2),
+// the host's comparison with the same IEEE operations.
+__global__ void gs_gate_kernel(double* sc, int before, int after, int g) {
+  sc[g] = (sqrt(sc[after]) > 0.7071067811865476 * sqrt(sc[before])) ? 1.0 : 0.0;
 }
 
 static int sk_grid(int64_t n) {
@@ -134,21 +148,37 @@ MCS_API int mcs_apply_BT(int nq, int nu, int nloc, int64_t nt, const double* Bpu
 
 MCS_API int mcs_mdot_len(void) { return MD_CHUNKS; }
 
-MCS_API int mcs_mdot(int m, int64_t n, int64_t ld, const double* V, const double* w,
-                     double* partial, double* h, void* stream) {
+MCS_API int mcs_mdot_gated(int m, int64_t n, int64_t ld, const double* V, const double* w,
+                           double* partial, double* h, const double* gate, void* stream) {
   if (m <= 0) return 0;
   auto st = static_cast<cudaStream_t>(stream);
-  mdot_partial_kernel<<<dim3(MD_CHUNKS, m), SK_THREADS, 0, st>>>(n, ld, V, w, partial);
+  mdot_partial_kernel<<<dim3(MD_CHUNKS, m), SK_THREADS, 0, st>>>(n, ld, V, w, partial, gate);
   int rc = launch_status();
   if (rc) return rc;
-  mdot_final_kernel<<<(m + 127) / 128, 128, 0, st>>>(m, partial, h);
+  mdot_final_kernel<<<(m + 127) / 128, 128, 0, st>>>(m, partial, h, gate);
+  return launch_status();
+}
+
+MCS_API int mcs_mdot(int m, int64_t n, int64_t ld, const double* V, const double* w,
+                     double* partial, double* h, void* stream) {
+  return mcs_mdot_gated(m, n, ld, V, w, partial, h, nullptr, stream);
+}
+
+MCS_API int mcs_gemv_acc_gated(int m, int64_t n, int64_t ld, const double* V, const double* h,
+                               double alpha, double beta, double* w, const double* gate,
+                               void* stream) {
+  if (n <= 0) return 0;
+  auto st = static_cast<cudaStream_t>(stream);
+  gemv_acc_kernel<<<sk_grid(n), SK_THREADS, 0, st>>>(m, n, ld, V, h, alpha, beta, w, gate);
   return launch_status();
 }
 
 MCS_API int mcs_gemv_acc(int m, int64_t n, int64_t ld, const double* V, const double* h,
                          double alpha, double beta, double* w, void* stream) {
-  if (n <= 0) return 0;
-  auto st = static_cast<cudaStream_t>(stream);
-  gemv_acc_kernel<<<sk_grid(n), SK_THREADS, 0, st>>>(m, n, ld, V, h, alpha, beta, w);
+  return mcs_gemv_acc_gated(m, n, ld, V, h, alpha, beta, w, nullptr, stream);
+}
+
+MCS_API int mcs_gs_gate(double* sc, int before, int after, int gate, void* stream) {
+  gs_gate_kernel<<<1, 1, 0, static_cast<cudaStream_t>(stream)>>>(sc, before, after, gate);
   return launch_status();
 }

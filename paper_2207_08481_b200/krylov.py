@@ -250,6 +250,10 @@ def _op(op, v, out):
     return out
 
 
+# Gram-Schmidt accounting of `gmres` (diagnostics: tools/gmres_prof.py)
+_GS_STATS = {"steps": 0, "second_pass": 0}
+
+
 def gmres(apply_A, b, apply_M=None, rtol=1e-6, maxit=500, project=None, x0=None):
     """Full (non-restarted) right-preconditioned GMRES (reference
     `krylov.py:25-100`) with the Krylov basis in HBM.
@@ -320,16 +324,27 @@ def gmres(apply_A, b, apply_M=None, rtol=1e-6, maxit=500, project=None, x0=None)
         _abi.call("mcs_gemv_acc", m, n, n, _abi.ptr(V), _abi.ptr(h1), -1.0, 1.0,
                   _abi.ptr(w), _abi.stream(None))
         ws.dot(w, w, ws.TMP2)
-        back = torch.cat((ws.sc[ws.TMP:ws.TMP2 + 1], h1[:m])).cpu().numpy()
+        # the DGKS decision on the device: the second pass is launched always
+        # and skipped by its kernels when the first one kept enough of ||w||
+        gate = ws.sc.data_ptr() + 8 * ws.GS_GATE
+        _abi.call("mcs_gs_gate", _abi.ptr(ws.sc), ws.TMP, ws.TMP2, ws.GS_GATE, _abi.stream(None))
+        _abi.call("mcs_mdot_gated", m, n, n, _abi.ptr(V), _abi.ptr(w), _abi.ptr(partial),
+                  _abi.ptr(h2), gate, _abi.stream(None))
+        _abi.call("mcs_gemv_acc_gated", m, n, n, _abi.ptr(V), _abi.ptr(h2), -1.0, 1.0,
+                  _abi.ptr(w), gate, _abi.stream(None))
+        ws.dot(w, w, ws.TMP3)
+        back = torch.cat((ws.sc[ws.TMP:ws.TMP3 + 1], h1[:m], h2[:m])).cpu().numpy()
         wnorm, hnext = float(np.sqrt(back[0])), float(np.sqrt(back[ws.TMP2 - ws.TMP]))
-        hcol = back[ws.TMP2 - ws.TMP + 1:]
-        if not hnext > 0.7071067811865476 * wnorm:
-            _abi.call("mcs_mdot", m, n, n, _abi.ptr(V), _abi.ptr(w), _abi.ptr(partial),
-                      _abi.ptr(h2), _abi.stream(None))
-            _abi.call("mcs_gemv_acc", m, n, n, _abi.ptr(V), _abi.ptr(h2), -1.0, 1.0,
-                      _abi.ptr(w), _abi.stream(None))
-            hnext = _norm(ws, w)
-            hcol = hcol + h2[:m].cpu().numpy()
+        o = ws.TMP3 - ws.TMP + 1
+        hcol = back[o:o + m]
+        _GS_STATS["steps"] += 1
+        second = not hnext > 0.7071067811865476 * wnorm
+        if second != (back[ws.GS_GATE - ws.TMP] == 0.0):
+            raise RuntimeError("device and host Gram-Schmidt decisions differ")
+        if second:
+            _GS_STATS["second_pass"] += 1
+            hnext = float(np.sqrt(back[ws.TMP3 - ws.TMP]))
+            hcol = hcol + back[o + m:o + 2 * m]
         H[:m, j] = hcol
         H[j + 1, j] = hnext
         if not np.isfinite(hnext) or not np.all(np.isfinite(hcol)):

@@ -39,6 +39,7 @@ class Workspace:
     RZ0, RZ1, PAP, RR, BB, TMP = 0, 1, 2, 3, 4, 5
     PAP2, RR2, GATE, BNORM, RTOL = 6, 7, 8, 9, 10   # second step of a graphed pair
     TMP2 = 11
+    GS_GATE, TMP3 = 12, 13   # GMRES: device DGKS decision, ||w||^2 after the second pass
 
     def __init__(self):
         torch = torch_mod()

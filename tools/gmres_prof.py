@@ -13,7 +13,7 @@ from paper_2207_08481_b200 import preconditioners as pc  # noqa: E402
 from paper_2207_08481_b200.condensation import condense_sigma_omega, double_schur  # noqa: E402
 from paper_2207_08481_b200.dofmap import FeSystem  # noqa: E402
 from paper_2207_08481_b200.driver import SolverOptions, condensed_rhs, velocity_preconditioner  # noqa: E402
-from paper_2207_08481_b200.krylov import gmres  # noqa: E402
+from paper_2207_08481_b200.krylov import _GS_STATS, gmres  # noqa: E402
 from paper_2207_08481_b200.operators import SaddleOperator  # noqa: E402
 from paper_2207_08481_b200.problems import baseline_config  # noqa: E402
 
@@ -37,3 +37,4 @@ for _ in range(2):
     torch.cuda.synchronize()
     print(f"iterations {rep.iterations} device {e0.elapsed_time(e1):.1f} ms wall "
           f"{1e3 * (time.perf_counter() - t0):.1f} ms  per it {e0.elapsed_time(e1) / rep.iterations:.3f} ms")
+print("Gram-Schmidt:", _GS_STATS)
