@@ -169,7 +169,7 @@ MCS_API int mcs_gemv_acc_gated(int m, int64_t n, int64_t ld, const double* V, co
                                void* stream) {
   if (n <= 0) return 0;
   auto st = static_cast<cudaStream_t>(stream);
-  gemv_acc_kernel<<<sk_grid(n), SK_THREADS, 0, st>>>(m, n, ld, V, h, alpha, beta, w, gate);
+  gemv_acc_kernel<<<(int)((n + SK_THREADS - 1) / SK_THREADS), SK_THREADS, 0, st>>>(m, n, ld, V, h, alpha, beta, w, gate);
   return launch_status();
 }
 
