@@ -300,7 +300,7 @@ def run_ours(args, rank, world):
     smoother = None
     for comp in ("additive", "multiplicative"):
         t0 = time.perf_counter()
-        M = velocity_preconditioner(fes, sys_, prob.nu, SolverOptions(composition=comp))
+        M = velocity_preconditioner(fes, sys_, prob.nu, SolverOptions(smoother="jacobi", composition=comp))
         torch.cuda.synchronize()
         t_sup = time.perf_counter() - t0
         if smoother is None:
@@ -474,7 +474,7 @@ def run_stokes(fes, sys_, prob, dev):
     from paper_2207_08481_b200.krylov import gmres
     from paper_2207_08481_b200.operators import SaddleOperator
     K = SaddleOperator(sys_)
-    vel = velocity_preconditioner(fes, sys_, prob.nu, SolverOptions(composition="additive"))
+    vel = velocity_preconditioner(fes, sys_, prob.nu, SolverOptions(smoother="jacobi", composition="additive"))
     P = pc.SaddlePreconditioner(vel, pc.PressureMassPrecond.build(fes, prob.nu), K.B)
     rhs = torch.from_numpy(np.concatenate(condensed_rhs(fes, sys_))).to(dev)
     gmres(K, rhs, P, rtol=1e-8, maxit=1000)          # warm-up

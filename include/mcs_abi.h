@@ -207,7 +207,8 @@ int mcs_cg_update(int64_t n, double* x, double* r, const double* p, const double
                   int rz, int pap, int rr, double* partials, unsigned* counter, void* stream);
 /* the same with a stop gate, for several PCG steps per CUDA graph: a no-op
  * when sc[gate_in] != 0 (gate_in >= 0); sets sc[gate_out] = 1 when
- * !(sc[pap] > 0) or sqrt(sc[rr]) / sc[bnorm_i] <= sc[rtol_i] (gate_out >= 0) */
+ * sc[pap] <= 0 or sqrt(sc[rr]) / sc[bnorm_i] <= sc[rtol_i] (gate_out >= 0; a NaN
+ * sets neither, as in the reference loop krylov.py:121-131) */
 int mcs_cg_update_gated(int64_t n, double* x, double* r, const double* p, const double* Ap,
                         double* sc, int rz, int pap, int rr, int gate_in, int gate_out,
                         int bnorm_i, int rtol_i, double* partials, unsigned* counter,
@@ -222,12 +223,35 @@ int mcs_axpby(int64_t n, double a, const double* x, double b, double* y, void* s
  * two-step PCG graph `pair_graph` (a cudaGraph_t).  After each pair a record
  * kernel appends (sc[pap], sc[rr]) of the steps that ran to `hist`
  * ([0] steps, [1] maxit, then two doubles per step, room for `cap` steps) and
- * stops the loop on !(p'Ap > 0), sqrt(rr) / sc[bnorm_i] <= sc[rtol_i], or
+ * stops the loop on p'Ap <= 0, sqrt(rr) / sc[bnorm_i] <= sc[rtol_i], or
  * maxit.  build: *exec_out = the instantiated graph (cudaGraphExec_t). */
 int mcs_pcg_loop_build(void* pair_graph, const double* sc, double* hist, int pap, int rr,
                        int pap2, int rr2, int bnorm_i, int rtol_i, int cap, void** exec_out);
 int mcs_pcg_loop_launch(void* exec, double* hist, int maxit, void* stream);
 int mcs_pcg_loop_destroy(void* exec);
+
+/* ---- CondensedSystem vector methods over ALL (V, Vhat) dofs (csrc/factorized.cu)
+ *      vv_codes: [nt][nloc] = 2*global + (sign < 0), as mcs_recover_stress.
+ *  mcs_apply_S_factorized  replaces condensation.py:104-122
+ *      (CondensedSystem.apply_S_factorized): y += S x through
+ *      [I X^T; 0 I] [Sd 0; 0 S_oo] [I 0; X I] per element, from S_packed
+ *      (S_oo block), ext (X) and Sd_packed; y must be zeroed by the caller.
+ *  mcs_harmonic_extend     replaces condensation.py:93-102
+ *      (CondensedSystem.harmonic_extend): out[bubble dofs] = -X x_c; the
+ *      caller copies x into out first (out keeps the coupling dofs). */
+int mcs_apply_S_factorized(int k, int64_t nt, const double* S_packed, const double* ext,
+                           const double* Sd_packed, const int* vv_codes, const double* x,
+                           double* y, void* stream);
+int mcs_harmonic_extend(int k, int64_t nt, const double* ext, const int* vv_codes,
+                        const double* x, double* out, void* stream);
+/* ---- packed inverses of caller-supplied SPD blocks for the facet Jacobi
+ *      apply (replaces the per-block cho_factor of FacetBlockSmoother.__init__,
+ *      preconditioners.py:186-200, when the smoother is built from a CSR
+ *      matrix and a block list): blocks [nblk][B][B] row-major, idx [nblk][B]
+ *      (-1 padding), bsize [nblk], B = 2k+1; outputs as mcs_jacobi_setup.
+ *      info[b] = 1 + first non-positive pivot. */
+int mcs_block_inverse(int k, int nblk, const double* blocks, const int* idx, const int* bsize,
+                      double* binv, int* bidx, int* info, void* stream);
 
 #ifdef __cplusplus
 }

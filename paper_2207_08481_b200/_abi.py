@@ -79,6 +79,10 @@ SIGNATURES = {
     "mcs_pcg_loop_build": [_p, _p, _p, _i, _i, _i, _i, _i, _i, _i, _p],
     "mcs_pcg_loop_launch": [_p, _p, _i, _p],
     "mcs_pcg_loop_destroy": [_p],
+    # factorized.cu
+    "mcs_apply_S_factorized": [_i, _l, _p, _p, _p, _p, _p, _p, _p],
+    "mcs_harmonic_extend": [_i, _l, _p, _p, _p, _p, _p],
+    "mcs_block_inverse": [_i, _i, _p, _p, _p, _p, _p, _p, _p],
 }
 
 _lib = None

@@ -336,13 +336,35 @@ class CoarseSolver:
         return self.solve_dev(b, x).cpu().numpy()
 
 
+def graph_coordinates(A: sp.csr_matrix) -> np.ndarray:
+    """Stand-in vertex coordinates for the nested dissection when the caller
+    has only the matrix (a reference `CoarseSolver`): BFS distances from two
+    pseudo-peripheral vertices of the matrix graph.  Any bisection keeps the
+    factorisation exact; this one keeps the separators small on mesh graphs."""
+    from scipy.sparse.csgraph import breadth_first_order, shortest_path
+    n = A.shape[0]
+    G = (abs(A) + abs(A.T)).tocsr()
+    order = breadth_first_order(G, 0, directed=False, return_predecessors=False)
+    a = int(order[-1])
+    da = shortest_path(G, unweighted=True, indices=a, directed=False)
+    b = int(np.argmax(np.where(np.isfinite(da), da, -1)))
+    db = shortest_path(G, unweighted=True, indices=b, directed=False)
+    xy = np.stack([da, db], axis=1)
+    xy[~np.isfinite(xy)] = 0.0
+    return xy + 1e-3 * np.arange(n)[:, None] / max(n, 1)
+
+
 def factorize_coarse(A: sp.csr_matrix, xy: np.ndarray, scale=1.0, kind=None,
                      leaf=LEAF) -> CoarseSolver:
+    """Exact GPU factorisation of the free coarse matrix; `xy` = per-dof
+    coordinates for the nested dissection (None: graph_coordinates(A))."""
     n = A.shape[0]
     kind = kind or ("dense" if n <= DENSE_MAX else "multifrontal")
     if kind == "dense":
         Ainv = np.linalg.inv(A.toarray())
         Ainv = 0.5 * (Ainv + Ainv.T)
         return CoarseSolver(A, "dense", engine.to_dev(Ainv), scale)
+    if xy is None:
+        xy = graph_coordinates(A)
     F = multifrontal_factor(A, xy, leaf=leaf)
     return CoarseSolver(A, "multifrontal", _upload_multifrontal(F), scale)

@@ -156,11 +156,77 @@ class CondensedSystem:
             return None
         return [sla.cho_factor(s) for s in self.soo_dense]
 
+    def _vv_codes_all(self):
+        """int32 device codes over ALL (V, Vhat) dofs (2*global + (sign < 0))."""
+        if getattr(self, "_codes_all", None) is None:
+            m = self.maps
+            self._codes_all = engine.to_dev(
+                np.ascontiguousarray((2 * m.vv_l2g + (m.vv_signs < 0)).astype(np.int32)))
+        return self._codes_all
+
+    def _vector_in(self, x_full):
+        torch = _torch()
+        on_host = not (hasattr(x_full, "is_cuda") and x_full.is_cuda)
+        x = torch.from_numpy(np.ascontiguousarray(x_full, dtype=np.float64)).cuda() \
+            if on_host else x_full.contiguous()
+        if x.numel() != self.fes.n_vv:
+            raise ValueError(f"expected a vector over all {self.fes.n_vv} (V, Vhat) dofs")
+        return x, on_host
+
+    def apply_S_factorized(self, x_full, stream=None):
+        """S @ x over all (V, Vhat) dofs through the exact triangular
+        factorisation (reference `condensation.py:104-122`), on the GPU
+        (csrc/factorized.cu: per element z_o = x_o + X x_c, d_o = S_oo z_o,
+        y_c = Sd_T x_c + X^T d_o, y_o = d_o).  NumPy in -> NumPy out."""
+        if self.ext_dev is None:
+            raise ValueError("double_schur() must be run first")
+        x, on_host = self._vector_in(x_full)
+        y = _torch().zeros_like(x)
+        _abi.call("mcs_apply_S_factorized", self.k, self.S_dev.shape[0], _abi.ptr(self.S_dev),
+                  _abi.ptr(self.ext_dev), _abi.ptr(self.Sd_dev), _abi.ptr(self._vv_codes_all()),
+                  _abi.ptr(x), _abi.ptr(y), _abi.stream(stream))
+        return y.cpu().numpy() if on_host else y
+
+    def harmonic_extend(self, x_full, stream=None):
+        """Energy-minimal completion of the interior bubble dofs, out_o =
+        -X x_c per element (reference `condensation.py:93-102`), on the GPU."""
+        if self.ext_dev is None:
+            raise ValueError("double_schur() must be run first")
+        x, on_host = self._vector_in(x_full)
+        out = x.clone()
+        _abi.call("mcs_harmonic_extend", self.k, self.S_dev.shape[0], _abi.ptr(self.ext_dev),
+                  _abi.ptr(self._vv_codes_all()), _abi.ptr(x), _abi.ptr(out),
+                  _abi.stream(stream))
+        return out.cpu().numpy() if on_host else out
+
     @property
     def recovery(self):
-        raise NotImplementedError(
-            "the per-element recovery matrices R_T are not stored on the GPU path "
-            "(572 MB at cfg2); recover_stress() regenerates them on the fly")
+        """Per-element R_T = M^-1 Bsig^T ((ns + nw) x nloc, reference
+        `condensation.py:33,173-177`), materialised lazily on the GPU: the
+        recovery kernel (csrc/recover.cu) evaluated on the nloc local unit
+        vectors of every element at once (so = -R_T e_j).  The solver path
+        never touches it (572 MB at cfg2)."""
+        if getattr(self, "_recovery", None) is None:
+            torch = _torch()
+            k, nt = self.k, self.fes.mesh.num_triangles
+            z = self.z
+            nloc, ns, nw = z["nloc"], z["ns"], z["nw"]
+            if k not in _RECOVERY:
+                _RECOVERY[k] = engine.to_dev(engine.recovery_tables(self.refs))
+            W = engine.to_dev(element_weights(self.fes, self.nu))
+            priv = torch.arange(nt * nloc, dtype=torch.int32, device="cuda").view(nt, nloc) * 2
+            R = torch.empty((nt, ns + nw, nloc), dtype=torch.float64, device="cuda")
+            x = torch.zeros(nt * nloc, dtype=torch.float64, device="cuda")
+            xv = x.view(nt, nloc)
+            for j in range(nloc):
+                xv.zero_()
+                xv[:, j] = 1.0
+                sig, om, info = engine.recover_stress(k, nt, W, _RECOVERY[k], priv, x)
+                self.check_info(info, "singular local stress block")
+                R[:, :ns, j] = -sig.view(nt, ns)
+                R[:, ns:, j] = -om.view(nt, nw)
+            self._recovery = list(R.cpu().numpy())
+        return self._recovery
 
     def recover_stress(self, x_full, stream=None):
         """Element-wise (sigma, omega) from a velocity vector over all (V, Vhat)
@@ -255,25 +321,25 @@ def condense_sigma_omega(fes, nu: float, body_force=None, blocks=None,
     return sys_
 
 
-def double_schur(sys_: CondensedSystem, stream=None) -> CondensedSystem:
+def double_schur(sys: CondensedSystem, stream=None) -> CondensedSystem:
     """Eliminate interior bubbles per element on the GPU (reference
-    `condensation.py:191-239`); mutates and returns `sys_`."""
+    `condensation.py:191-239`); mutates and returns `sys`."""
     torch = _torch()
-    k = sys_.k
-    nt = sys_.S_dev.shape[0]
-    if sys_._pending_ds is not None:             # computed with S_T (fused kernel)
-        ext, Sd, info = sys_._pending_ds
-        sys_._pending_ds = None
-        sys_.ext_dev, sys_.Sd_dev = ext, Sd
-        sys_.vv_of_cpl, sys_.cpl_of_vv = sys_.maps.vv_of_cpl, sys_.maps.cpl_of_vv
-        sys_.check_info(info, "interior velocity block not SPD", mask=2)
-        return sys_
+    k = sys.k
+    nt = sys.S_dev.shape[0]
+    if sys._pending_ds is not None:             # computed with S_T (fused kernel)
+        ext, Sd, info = sys._pending_ds
+        sys._pending_ds = None
+        sys.ext_dev, sys.Sd_dev = ext, Sd
+        sys.vv_of_cpl, sys.cpl_of_vv = sys.maps.vv_of_cpl, sys.maps.cpl_of_vv
+        sys.check_info(info, "interior velocity block not SPD", mask=2)
+        return sys
     ext = torch.empty((nt, _abi.call("mcs_ext_stride", k)), dtype=torch.float64, device="cuda")
     Sd = torch.empty((nt, _abi.call("mcs_sd_stride", k)), dtype=torch.float64, device="cuda")
     info = torch.empty(nt, dtype=torch.int32, device="cuda")
-    _abi.call("mcs_double_schur", k, nt, _abi.ptr(sys_.S_dev), _abi.ptr(ext), _abi.ptr(Sd),
+    _abi.call("mcs_double_schur", k, nt, _abi.ptr(sys.S_dev), _abi.ptr(ext), _abi.ptr(Sd),
               _abi.ptr(info), _abi.stream(stream))
-    sys_.ext_dev, sys_.Sd_dev = ext, Sd
-    sys_.vv_of_cpl, sys_.cpl_of_vv = sys_.maps.vv_of_cpl, sys_.maps.cpl_of_vv
-    sys_.check_info(info, "interior velocity block not SPD")
-    return sys_
+    sys.ext_dev, sys.Sd_dev = ext, Sd
+    sys.vv_of_cpl, sys.cpl_of_vv = sys.maps.vv_of_cpl, sys.maps.cpl_of_vv
+    sys.check_info(info, "interior velocity block not SPD")
+    return sys

@@ -423,15 +423,6 @@ __global__ void scatter_kernel(const double* z, const int* __restrict__ map,
     out[map[j]] = z[j];
 }
 
-static int sm_count() {
-  static int n = 0;
-  if (!n) {
-    int dev = 0;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
-  }
-  return n;
-}
 
 template <int N, int STRIDE>
 static int launch_apply(const double* M, const int* codes, const double* x, double* y, int64_t nt,
@@ -452,7 +443,10 @@ static int launch_apply(const double* M, const int* codes, const double* x, doub
   cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, W * 32, smem);
   if (per_sm < 1) per_sm = 1;
   const int64_t want = (nt + W - 1) / W;
-  const int64_t g = (int64_t)per_sm * sm_count();
+  int64_t g = (int64_t)per_sm * sm_count();
+  // the fused p'Ap writes one partial per CTA: stay inside the workspace
+  // (mcs_reduce_workspace_len; the grid-stride loop covers the rest)
+  if (dpart && g > mcs_reduce_workspace_len()) g = mcs_reduce_workspace_len();
   return launch_pdl_g(PDL_APPLY, kern, (int)(want < g ? want : g), W * 32, smem, st, M, codes, x, y, nt,
                       dpart, dcount, dout);
 }

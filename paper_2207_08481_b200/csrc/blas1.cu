@@ -75,8 +75,9 @@ __global__ void __launch_bounds__(RED_THREADS)
 // Gating (several PCG steps per CUDA graph, krylov.py): gate_in >= 0 and
 // sc[gate_in] != 0 -> the step is a no-op (the previous step stopped the
 // loop); gate_out >= 0 -> sc[gate_out] = 1 when this step stops the loop,
-// with the host's own test: !(pAp > 0) or sqrt(rr) / bnorm <= rtol (IEEE
-// sqrt and division, so device and host decide identically).
+// with the host's own test: pAp <= 0 or sqrt(rr) / bnorm <= rtol (IEEE
+// sqrt and division, so device and host decide identically; a NaN passes
+// both, as in the reference loop, which then runs on to maxit).
 __global__ void __launch_bounds__(RED_THREADS)
     cg_update_kernel(int64_t n, double* __restrict__ x, double* __restrict__ r,
                      const double* __restrict__ p, const double* __restrict__ Ap, double* sc,
@@ -97,7 +98,7 @@ __global__ void __launch_bounds__(RED_THREADS)
   s = block_sum(s);
   if (finish(s, partials, counter, sc + rr) && gate_out >= 0) {
     const double rrv = sc[rr], pv = sc[pap];
-    sc[gate_out] = (!(pv > 0.0) || __dsqrt_rn(rrv) / sc[bnorm_i] <= sc[rtol_i]) ? 1.0 : 0.0;
+    sc[gate_out] = (pv <= 0.0 || __dsqrt_rn(rrv) / sc[bnorm_i] <= sc[rtol_i]) ? 1.0 : 0.0;
   }
 }
 
@@ -151,7 +152,12 @@ static int grid_for(int64_t n) {
 
 using namespace mcs;
 
-MCS_API int mcs_reduce_workspace_len() { return RED_BLOCKS; }
+// Partials slots: the fixed reduction grid, and one per CTA of the fused
+// p'Ap element apply (apply.cu; at most 8 CTAs of 256 threads per SM).
+MCS_API int mcs_reduce_workspace_len() {
+  const int a = 8 * sm_count();
+  return a > RED_BLOCKS ? a : RED_BLOCKS;
+}
 
 MCS_API int mcs_dot(int64_t n, const double* x, const double* y, double* partials, unsigned* counter,
                     double* out, void* stream) {

@@ -13,6 +13,18 @@
 
 namespace mcs {
 
+// SMs of the current device (cached; 148 on B200)
+inline int sm_count() {
+  static int n = 0;
+  if (!n) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
+  }
+  return n;
+}
+
+
 // lower-packed, row-major: (i, j) with j <= i  ->  i(i+1)/2 + j
 __host__ __device__ constexpr int pk(int i, int j) { return i * (i + 1) / 2 + j; }
 __host__ __device__ constexpr int npk(int n) { return n * (n + 1) / 2; }

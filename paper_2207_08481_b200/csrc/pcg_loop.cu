@@ -5,7 +5,7 @@
 // becomes the body of a conditional WHILE node.  After each pair a one-thread
 // record kernel appends (p'Ap, ||r||^2) of the steps that ran to a device
 // history and evaluates the host loop's stopping test (krylov.py `cg`,
-// reference krylov.py:103-137: stop when p'Ap <= 0 or not finite-positive, or
+// reference krylov.py:103-137: stop when p'Ap <= 0 (a NaN does not stop), or
 // sqrt(rr) / ||b|| <= rtol, the same IEEE operations) plus the maxit cap; the
 // conditional handle keeps looping while neither fires.  The host then reads
 // the history once and replays the reference's control flow over it, so the
@@ -35,7 +35,7 @@ __global__ void pcg_record_kernel(const double* __restrict__ sc, double* __restr
     hist[2 + 2 * c] = a;
     hist[3 + 2 * c] = b;
     ++c;
-    stop = !(a > 0.0) || sqrt(b) / bn <= rt;   // the gate's test (cg_update_kernel)
+    stop = a <= 0.0 || sqrt(b) / bn <= rt;   // the gate's test (cg_update_kernel)
   }
   hist[0] = (double)c;
   cudaGraphSetConditional(h, (!stop && c + 2 <= maxit) ? 1u : 0u);

@@ -11,6 +11,7 @@ from __future__ import annotations
 
 import time
 from dataclasses import dataclass, field
+from typing import Optional
 
 import numpy as np
 
@@ -23,15 +24,47 @@ from .operators import SdOperator, SOperator
 
 @dataclass
 class SolverOptions:
-    mode: str = "elliptic"
-    target: str = "Sd"
+    """Reference `driver.py:20-30`, same defaults.  The GPU preconditioner
+    implements smoother "jacobi" (the north-star target); "gauss_seidel"
+    (the reference default) and "l1" raise NotImplementedError when a
+    preconditioner is actually built with them."""
+    mode: str = "stokes"               # stokes | elliptic
+    target: str = "Sd"                 # S | Sd (preconditioner target)
     composition: str = "multiplicative"
-    smoother: str = "jacobi"
+    smoother: str = "gauss_seidel"     # gauss_seidel | jacobi | l1
     steps: int = 1
     penalty_C: float = 4.0
     rtol: float = 1e-6
     maxit: int = 500
     seed: int = 0
+
+
+@dataclass
+class RunRecord:
+    """Reference `driver.py:33-57` (timings are device-synchronised)."""
+    problem: str
+    k: int
+    level: int
+    n_elements: int
+    n_dofs: int                 # free dofs of (V x Vhat) x Q
+    iterations: int
+    t_tot: float
+    t_sup: float
+    t_sol: float
+    converged: bool
+    max_div: float = np.nan
+    nt_jump: float = np.nan
+    lambda_min: Optional[float] = None
+    lambda_max: Optional[float] = None
+    cond: Optional[float] = None
+
+    CSV_FIELDS = ["problem", "k", "level", "n_elements", "n_dofs",
+                  "iterations", "t_tot", "t_sup", "t_sol", "converged",
+                  "max_div", "nt_jump", "lambda_min", "lambda_max", "cond"]
+
+    def csv_row(self):
+        vals = [getattr(self, f) for f in self.CSV_FIELDS]
+        return [("" if v is None else v) for v in vals]
 
 
 def build_system(problem, k, nu, opts: SolverOptions):
@@ -45,8 +78,12 @@ def build_system(problem, k, nu, opts: SolverOptions):
 def velocity_preconditioner(fes, sys_: CondensedSystem, nu, opts: SolverOptions):
     """ExtendedAsp(AspPreconditioner(S_d, facet Jacobi, E_c, coarse)) on the
     GPU (reference `driver.py:82-102`, target "Sd")."""
+    if opts.target == "S":
+        raise NotImplementedError(
+            "preconditioner target 'S' (overlapping facet_blocks_full) is outside the GPU "
+            "scope (SURVEY §2); use target='Sd'")
     if opts.target != "Sd":
-        raise ValueError(f"GPU path supports target 'Sd' only, got {opts.target!r}")
+        raise ValueError(f"unknown preconditioner target {opts.target!r}")
     A = SdOperator(sys_)
     sm = pc.FacetBlockSmoother(A, None, opts.smoother)
     Ec = pc.embedding_cpl(fes, sys_)
@@ -71,16 +108,43 @@ def condensed_rhs(fes, sys_: CondensedSystem):
 
 
 @dataclass
-class EllipticResult:
+class SolveResult:
+    """Reference `driver.py:60-71`; `p` is None in elliptic mode.  `x_free`
+    (the Krylov solution on free dofs) is an addition."""
     fes: FeSystem
     system: CondensedSystem
-    x_free: object
-    u: np.ndarray
+    u: np.ndarray               # V coefficients, Dirichlet data included
     uhat: np.ndarray
+    p: Optional[np.ndarray]     # physical pressure
+    sigma: np.ndarray
+    w: np.ndarray
     report: KrylovReport
-    t_sup: float
-    t_sol: float
-    extras: dict = field(default_factory=dict)
+    record: RunRecord
+    checks: dict = field(default_factory=dict)
+    x_free: object = None
+
+    @property
+    def t_sup(self):
+        return self.record.t_sup
+
+    @property
+    def t_sol(self):
+        return self.record.t_sol
+
+
+# earlier names of the two result kinds
+EllipticResult = StokesResult = SolveResult
+
+
+def _record(problem, fes, k, report, t0, t_sup, t_sol, checks):
+    """RunRecord exactly as `driver.py:170-177` fills it."""
+    return RunRecord(problem=getattr(problem, "name", ""), k=k, level=-1,
+                     n_elements=fes.mesh.num_triangles,
+                     n_dofs=int(fes.vv_free.sum()) + fes.dof_q.ndof,
+                     iterations=report.iterations,
+                     t_tot=time.perf_counter() - t0, t_sup=t_sup, t_sol=t_sol,
+                     converged=report.converged,
+                     max_div=checks["max_div_scaled"], nt_jump=checks["nt_jump_scaled"])
 
 
 def _sync():
@@ -88,7 +152,8 @@ def _sync():
     torch.cuda.synchronize()
 
 
-def solve_elliptic(problem, k, nu, opts: SolverOptions) -> EllipticResult:
+def solve_elliptic(problem, k, nu, opts: SolverOptions) -> SolveResult:
+    """Elliptic branch of `driver.solve_stokes` (`driver.py:143-146`)."""
     t0 = time.perf_counter()
     fes, sys_ = build_system(problem, k, nu, opts)
     M = velocity_preconditioner(fes, sys_, nu, opts)
@@ -102,11 +167,12 @@ def solve_elliptic(problem, k, nu, opts: SolverOptions) -> EllipticResult:
     t_sol = time.perf_counter() - t1
     x_full = fes.vv_values.copy()
     x_full[fes.vv_free] = x
-    # reference driver.py:165-169: stress recovery and structural checks
+    # reference driver.py:164-177: stress recovery, structural checks, record
     sigma, w = sys_.recover_stress(x_full)
     checks = post_checks(fes, sys_, x_full[:fes.n_v], sigma, report)
-    return EllipticResult(fes, sys_, x, x_full[:fes.n_v], x_full[fes.n_v:], report,
-                          t_sup, t_sol, extras=dict(sigma=sigma, w=w, checks=checks))
+    record = _record(problem, fes, k, report, t0, t_sup, t_sol, checks)
+    return SolveResult(fes=fes, system=sys_, u=x_full[:fes.n_v], uhat=x_full[fes.n_v:], p=None,
+                       sigma=sigma, w=w, report=report, record=record, checks=checks, x_free=x)
 
 
 def post_checks(fes, sys_, u, sigma, report: KrylovReport) -> dict:
@@ -178,23 +244,7 @@ def pressure_projector(fes):
     return project
 
 
-@dataclass
-class StokesResult:
-    fes: FeSystem
-    system: CondensedSystem
-    x_free: object
-    u: np.ndarray
-    uhat: np.ndarray
-    p: np.ndarray
-    sigma: np.ndarray
-    w: np.ndarray
-    report: KrylovReport
-    t_sup: float
-    t_sol: float
-    checks: dict = None
-
-
-def solve_stokes(problem, k, nu, opts: SolverOptions):
+def solve_stokes(problem, k, nu, opts: SolverOptions) -> SolveResult:
     """Reference `driver.py:133-180`: elliptic mode -> PCG on S; Stokes mode
     -> right-preconditioned GMRES on K = [[S, B^T], [B, 0]] with the block
     triangular saddle preconditioner (two ExtendedAsp applications, the
@@ -232,5 +282,7 @@ def solve_stokes(problem, k, nu, opts: SolverOptions):
     x_full[fes.vv_free] = x_free
     sigma, w = sys_.recover_stress(x_full)
     checks = post_checks(fes, sys_, x_full[:fes.n_v], sigma, report)
-    return StokesResult(fes, sys_, x_free, x_full[:fes.n_v], x_full[fes.n_v:], p_phys, sigma, w,
-                        report, t_sup, t_sol, checks)
+    record = _record(problem, fes, k, report, t0, t_sup, t_sol, checks)
+    return SolveResult(fes=fes, system=sys_, u=x_full[:fes.n_v], uhat=x_full[fes.n_v:],
+                       p=p_phys, sigma=sigma, w=w, report=report, record=record,
+                       checks=checks, x_free=x_free)

@@ -37,10 +37,18 @@ class KrylovReport:
     lanczos_steps: Optional[int] = None
 
 
-def _apply(op, v, out):
+def _apply(op, v, out, host_callables=False):
+    """out = op(v).  This package's device operators (`.apply(v, out=)`)
+    run on the CUDA tensors directly.  Any other callable follows the
+    reference convention (krylov.py:25,103: a plain callable v -> A v on 1-D
+    float64 arrays): with a NumPy right-hand side it receives and may return
+    NumPy arrays, with a CUDA right-hand side it receives the CUDA tensor;
+    NumPy or torch results are both accepted."""
     if hasattr(op, "apply"):
         return op.apply(v, out=out)
-    res = op(v)
+    res = op(v.cpu().numpy() if host_callables else v)
+    if isinstance(res, np.ndarray):
+        res = __import__("torch").from_numpy(np.ascontiguousarray(res, dtype=np.float64))
     out.copy_(res)
     return out
 
@@ -52,9 +60,10 @@ def _graphable(op):
 class _PcgState:
     """Persistent buffers + captured CUDA graphs of one (A, M, n) triple."""
 
-    def __init__(self, apply_A, apply_M, n):
+    def __init__(self, apply_A, apply_M, n, host_callables=False):
         torch = __import__("torch")
         self.A, self.M, self.n = apply_A, apply_M, n
+        self.host_callables = host_callables
         f64 = dict(dtype=torch.float64, device="cuda")
         self.x, self.r, self.p = (torch.zeros(n, **f64) for _ in range(3))
         self.z, self.Ap = torch.zeros(n, **f64), torch.zeros(n, **f64)
@@ -64,7 +73,7 @@ class _PcgState:
         if self.M is None:
             self.z.copy_(self.r)
         else:
-            _apply(self.M, self.r, self.z)
+            _apply(self.M, self.r, self.z, self.host_callables)
 
     def step(self, rz, rz_new, pap=None, rr=None, gate_in=-1, gate_out=-1):
         ws = workspace()
@@ -74,7 +83,7 @@ class _PcgState:
         if hasattr(self.A, "apply_dot") and not _NO_FUSED_PAP:   # p'Ap inside the apply kernel
             self.A.apply_dot(self.p, self.Ap, pap)
         else:
-            _apply(self.A, self.p, self.Ap)
+            _apply(self.A, self.p, self.Ap, self.host_callables)
             ws.dot(self.p, self.Ap, pap)
         _abi.call("mcs_cg_update_gated", self.n, _abi.ptr(self.x), _abi.ptr(self.r),
                   _abi.ptr(self.p), _abi.ptr(self.Ap), _abi.ptr(ws.sc), rz, pap, rr, gate_in,
@@ -132,7 +141,31 @@ class _PcgState:
             pass
 
 
-_STATES = {}
+def _state_slot(apply_A):
+    """Captured PCG states live on the operator object they were captured
+    for (a dict attribute keyed by (id(M), n)), so they are freed together
+    with the operator: nothing module-level pins a CondensedSystem, its CUDA
+    graphs or their memory pools (the state references the operator back;
+    Python's cycle collector reclaims both)."""
+    try:
+        d = apply_A.__dict__.setdefault("_pcg_states", {})
+    except AttributeError:                    # no instance dict: do not cache
+        return None
+    return d
+
+
+def release(apply_A, apply_M=None):
+    """Drop the captured PCG graphs and buffers of `apply_A` (all
+    preconditioners, or only `apply_M`'s) now, instead of at garbage
+    collection."""
+    d = getattr(apply_A, "__dict__", {}).get("_pcg_states")
+    if not d:
+        return
+    for key in [k for k, st in d.items() if apply_M is None or st.M is apply_M]:
+        st = d.pop(key)
+        st.__del__()
+        st.loop = None
+    __import__("gc").collect()
 # A/B switch for the fused curvature (MCS_NO_FUSED_PAP=1: separate dot kernel)
 _NO_FUSED_PAP = __import__("os").environ.get("MCS_NO_FUSED_PAP", "0") == "1"
 # A/B switch for the two-step graph (MCS_NO_PAIR=1: one read-back per step)
@@ -170,12 +203,13 @@ def cg(apply_A, b, apply_M=None, rtol=1e-8, maxit=1000, stream=None, use_graph=T
     # MCS_NO_GRAPH=1: eager launches (ncu launch lists; ncu does not replay graphs)
     use_graph = use_graph and os.environ.get("MCS_NO_GRAPH", "0") != "1"
     graphable = use_graph and _graphable(apply_A) and _graphable(apply_M)
-    key = (id(apply_A), id(apply_M), n)
-    S = _STATES.get(key) if graphable else None
+    slots = _state_slot(apply_A) if graphable else None
+    key = (id(apply_M), n)
+    S = slots.get(key) if slots is not None else None
     if S is None or S.A is not apply_A or S.M is not apply_M:
-        S = _PcgState(apply_A, apply_M, n)
-        if graphable:
-            _STATES[key] = S
+        S = _PcgState(apply_A, apply_M, n, host_callables=host)
+        if slots is not None:
+            slots[key] = S
     S.x.zero_()
     S.r.copy_(bd)
     ws.dot(bd, bd, ws.BB)
@@ -197,7 +231,10 @@ def cg(apply_A, b, apply_M=None, rtol=1e-8, maxit=1000, stream=None, use_graph=T
     it = 0
 
     def record(pap, rr):
-        """The reference loop's per-step control flow; True = stop."""
+        """The reference loop's per-step control flow; True = stop.  The
+        device gates (blas1.cu cg_update_kernel, pcg_loop.cu) use the same
+        predicates: pAp <= 0 raises, res <= rtol stops, and a NaN passes
+        both (the reference then runs on to maxit, not converged)."""
         if pap <= 0:
             raise NegativeCurvatureError(f"p'Ap = {pap:.3e} at iteration {it}")
         res = float(np.sqrt(rr) / bnorm)
@@ -243,11 +280,8 @@ def _norm(ws: Workspace, v) -> float:
     return float(np.sqrt(ws.sc[ws.TMP].item()))
 
 
-def _op(op, v, out):
-    if hasattr(op, "apply"):
-        return op.apply(v, out=out)
-    out.copy_(op(v))
-    return out
+def _op(op, v, out, host_callables=False):
+    return _apply(op, v, out, host_callables)
 
 
 # Gram-Schmidt accounting of `gmres` (diagnostics: tools/gmres_prof.py)
@@ -280,7 +314,7 @@ def gmres(apply_A, b, apply_M=None, rtol=1e-6, maxit=500, project=None, x0=None)
         b_ = project(b_)
     x0d = torch.zeros(n, dtype=torch.float64, device="cuda") if x0 is None else as_device(x0)[0]
     if x0 is not None and _norm(ws, x0d) > 0.0:
-        r0 = b_ - _op(apply_A, x0d, empty(n))
+        r0 = b_ - _op(apply_A, x0d, empty(n), host)
     else:
         r0 = b_.clone()
     beta = _norm(ws, r0)
@@ -308,8 +342,8 @@ def gmres(apply_A, b, apply_M=None, rtol=1e-6, maxit=500, project=None, x0=None)
     z, w = empty(n), empty(n)
     j = 0
     while j < maxit:
-        mz = V[j] if ident else _op(apply_M, V[j], z)
-        _op(apply_A, mz, w)
+        mz = V[j] if ident else _op(apply_M, V[j], z, host)
+        _op(apply_A, mz, w, host)
         if project is not None:
             w = project(w)
         m = j + 1
@@ -380,7 +414,7 @@ def gmres(apply_A, b, apply_M=None, rtol=1e-6, maxit=500, project=None, x0=None)
     yd = torch.from_numpy(y).cuda()
     t = empty(n)
     _abi.call("mcs_gemv_acc", mm, n, n, _abi.ptr(V), _abi.ptr(yd), 1.0, 0.0, _abi.ptr(t), _abi.stream(None))
-    xk = x0d + (t if ident else _op(apply_M, t, empty(n)))
+    xk = x0d + (t if ident else _op(apply_M, t, empty(n), host))
     if project is not None:
         xk = project(xk)
     report.iterations = mm

@@ -127,14 +127,14 @@ def embedding_free(fes, E):
     return E[fes.vv_free][:, fes.dof_vbar.is_free].tocsr()
 
 
-def embedding_cpl(fes, sys_, E=None) -> sp.csr_matrix:
+def embedding_cpl(fes, sys, E=None) -> sp.csr_matrix:
     """E restricted to free coupling rows and free P1 columns
     (reference `preconditioners.py:101-105`).  Only facet rows survive, so
     E may be the facet-only embedding."""
     if E is None:
         E = build_embedding(fes, interior=False)
-    free_cpl = sys_.free_mask_cpl()
-    return E[sys_.vv_of_cpl][:, fes.dof_vbar.is_free][free_cpl].tocsr()
+    free_cpl = sys.free_mask_cpl()
+    return E[sys.vv_of_cpl][:, fes.dof_vbar.is_free][free_cpl].tocsr()
 
 
 # -------------------------------------------------------------- coarse space
@@ -188,15 +188,15 @@ def build_coarse(fes, nu: float, penalty_C: float = 4.0, scale: float = 1.0) -> 
 
 # ------------------------------------------------------------------ smoother
 
-def facet_blocks_schur(fes, sys_) -> List[np.ndarray]:
+def facet_blocks_schur(fes, sys) -> List[np.ndarray]:
     """Host list of the S_d facet blocks (reference `:266-280`), for
     compatibility; the GPU smoother builds its blocks from `facet_slots`."""
     k = fes.k
-    idx = free_index(sys_.free_mask_cpl())
+    idx = free_index(sys.free_mask_cpl())
     out = []
     for f in range(fes.mesh.num_facets):
-        d = [sys_.cpl_of_vv[f * (k + 1) + q] for q in range(k + 1)]
-        d += [sys_.cpl_of_vv[fes.n_v + f * k + q] for q in range(k)]
+        d = [sys.cpl_of_vv[f * (k + 1) + q] for q in range(k + 1)]
+        d += [sys.cpl_of_vv[fes.n_v + f * k + q] for q in range(k)]
         b = idx[np.array(d)]
         b = b[b >= 0]
         if len(b):
@@ -205,19 +205,42 @@ def facet_blocks_schur(fes, sys_) -> List[np.ndarray]:
 
 
 class FacetBlockSmoother:
-    """Facet-block Jacobi on S_d with packed block inverses in HBM
-    (reference `:177-206`, variant "jacobi")."""
+    """Facet-block Jacobi with packed block inverses in HBM (reference
+    `preconditioners.py:177-206`, variant "jacobi").
 
-    def __init__(self, A, blocks=None, variant: str = "gauss_seidel"):
+    * `A` an `SdOperator` and `blocks` None (the driver path): the facet
+      blocks of `facet_blocks_schur` are assembled on the GPU from the
+      per-element Sd_T and inverted there (`mcs_jacobi_setup`).
+    * `A` a SciPy sparse matrix (or an `SdOperator` with an explicit block
+      list), as the reference takes it: the dense blocks A[blk, blk] are
+      gathered on the host and inverted on the GPU (`mcs_block_inverse`);
+      blocks must be disjoint (x[blk] = A_bb^-1 r[blk], like the reference's
+      `jacobi_apply` for the S_d blocks) and hold at most 13 dofs.
+    Gauss-Seidel and l1 are sequential over facets and out of the GPU scope
+    (SURVEY §2): NotImplementedError; unknown variants: ValueError."""
+
+    def __init__(self, A, blocks=None, variant: str = "gauss_seidel", factors=None):
+        # `factors` mirrors the reference dataclass field; the GPU keeps packed
+        # inverses instead (self.binv) and ignores it
         if variant not in ("jacobi", "gauss_seidel", "l1"):
             raise ValueError(f"unknown smoother variant {variant!r}")
         if variant != "jacobi":
             raise NotImplementedError(
                 f"smoother {variant!r} is sequential / out of the GPU scope (SURVEY §2)")
-        if not isinstance(A, SdOperator):
-            raise TypeError("the GPU smoother is built from an SdOperator")
+        self.A, self.variant, self.blocks = A, variant, blocks
+        if isinstance(A, SdOperator) and blocks is None:
+            self._setup_from_sd(A)
+        else:
+            Ah = A.sys.Sd[A.sys.free_mask_cpl()][:, A.sys.free_mask_cpl()] \
+                if isinstance(A, SdOperator) else A
+            if not sp.issparse(Ah):
+                raise TypeError("FacetBlockSmoother needs an SdOperator or a sparse matrix")
+            if blocks is None:
+                raise ValueError("a sparse matrix needs its block list")
+            self._setup_from_blocks(sp.csr_matrix(Ah), blocks)
+
+    def _setup_from_sd(self, A):
         torch = __import__("torch")
-        self.A, self.variant = A, variant
         sys_ = A.sys
         fes = sys_.fes
         k = fes.k
@@ -229,19 +252,56 @@ class FacetBlockSmoother:
         self.bsize = torch.empty(self.nblk, dtype=torch.int32, device="cuda")
         info = torch.empty(self.nblk, dtype=torch.int32, device="cuda")
         m = sys_.dev_maps()
+        slots_d = engine.to_dev(slots)              # alive until the kernel has run
         _abi.call("mcs_jacobi_setup", k, self.nblk, _abi.ptr(sys_.Sd_dev),
                   sys_.Sd_dev.shape[1], _abi.ptr(m["cpl_codes"]),
-                  _abi.ptr(engine.to_dev(slots)), _abi.ptr(self.binv), _abi.ptr(self.bidx),
+                  _abi.ptr(slots_d), _abi.ptr(self.binv), _abi.ptr(self.bidx),
                   _abi.ptr(self.bsize), _abi.ptr(info), _abi.stream())
         bad = np.flatnonzero(info.cpu().numpy())
         if len(bad):
             raise RuntimeError(f"facet block {int(self.facets[bad[0]])} not SPD")
         self.k = k
-        self.blocks = blocks
+
+    def _setup_from_blocks(self, A, blocks):
+        torch = __import__("torch")
+        sizes = np.array([len(b) for b in blocks], dtype=np.int32)
+        if len(blocks) == 0:
+            raise ValueError("empty block list")
+        bmax = int(sizes.max())
+        if bmax > 13:
+            raise NotImplementedError(f"facet blocks of {bmax} > 13 dofs (k > 6)")
+        k = max(2, bmax // 2)                          # template block size 2k+1 >= bmax
+        B = 2 * k + 1
+        nblk = len(blocks)
+        idx = np.full((nblk, B), -1, dtype=np.int64)
+        for i, b in enumerate(blocks):
+            idx[i, :len(b)] = b
+        covered = idx[idx >= 0]
+        if len(np.unique(covered)) != len(covered):
+            raise NotImplementedError("overlapping smoother blocks (only disjoint facet blocks)")
+        ii = np.repeat(idx, B, axis=1).ravel()
+        jj = np.tile(idx, (1, B)).ravel()
+        ok = (ii >= 0) & (jj >= 0)
+        dense = np.zeros(nblk * B * B)
+        dense[ok] = np.asarray(A[ii[ok], jj[ok]]).ravel()
+        self.nblk, self.k, self.facets = nblk, k, np.arange(nblk)
+        self.binv = torch.empty((B * (B + 1) // 2, nblk), dtype=torch.float64, device="cuda")
+        self.bidx = torch.empty((B, nblk), dtype=torch.int32, device="cuda")
+        self.bsize = engine.to_dev(sizes)
+        info = torch.empty(nblk, dtype=torch.int32, device="cuda")
+        dense_d, idx_d = engine.to_dev(dense), engine.to_dev(idx.astype(np.int32))
+        _abi.call("mcs_block_inverse", k, nblk, _abi.ptr(dense_d), _abi.ptr(idx_d),
+                  _abi.ptr(self.bsize), _abi.ptr(self.binv), _abi.ptr(self.bidx),
+                  _abi.ptr(info), _abi.stream())
+        bad = np.flatnonzero(info.cpu().numpy())
+        if len(bad):
+            raise RuntimeError(f"smoother block {int(bad[0])} not SPD")
 
     def jacobi_apply(self, r, out=None, scale_inv=1.0, stream=None):
         rd, host = as_device(r)
         x = out if out is not None else empty(rd.numel())
+        if self.blocks is not None:              # caller blocks need not cover every dof
+            x.zero_()
         _abi.call("mcs_jacobi_apply", self.k, self.nblk, _abi.ptr(self.binv),
                   _abi.ptr(self.bidx), _abi.ptr(rd), _abi.ptr(x), float(scale_inv),
                   _abi.stream(stream))
@@ -268,6 +328,24 @@ class _DevCsr:
         return y
 
 
+class _CsrOperator:
+    """A SciPy CSR matrix applied on the GPU (`mcs_csr_spmv`)."""
+
+    graphable = True
+
+    def __init__(self, A):
+        self.M = _DevCsr(A)
+        self.shape = A.shape
+
+    def apply(self, x, out=None, stream=None):
+        xd, host = as_device(x)
+        y = out if out is not None else empty(self.shape[0])
+        self.M.mv(xd, y, 1.0, 0.0, stream)
+        return y.cpu().numpy() if host else y
+
+    __call__ = apply
+
+
 # MCS_NO_FORK=1: A/B switch, additive ASP smoother and coarse chain in one stream
 FORK_ADDITIVE = os.environ.get("MCS_NO_FORK", "0") != "1"
 
@@ -277,8 +355,17 @@ class AspPreconditioner:
 
     def __init__(self, A, smoother, E, coarse, mode: str = "multiplicative",
                  steps: int = 1):
+        """`A` is an `SdOperator` or, as in the reference, a SciPy sparse
+        matrix (applied on the GPU as a CSR); `coarse` is this package's
+        `CoarseSolver` or the reference's (its `matrix` is refactorised
+        exactly for the GPU)."""
         if mode not in ("additive", "multiplicative"):
             raise ValueError(f"unknown composition mode {mode!r}")
+        if sp.issparse(A):
+            A = _CsrOperator(A)
+        if not hasattr(coarse, "solve_dev"):
+            coarse = factorize_coarse(sp.csr_matrix(coarse.matrix), None,
+                                      scale=getattr(coarse, "scale", 1.0))
         self.A, self.smoother, self.coarse, self.mode, self.steps = A, smoother, coarse, mode, steps
         self.E = _DevCsr(E)
         self.Et = _DevCsr(E.T.tocsr())
@@ -363,15 +450,15 @@ class ExtendedAsp:
 
     graphable = True          # every stage is a stream-ordered kernel
 
-    def __init__(self, sys_, inner):
-        if sys_.Sd_dev is None:
+    def __init__(self, sys, inner):
+        if sys.Sd_dev is None:
             raise ValueError("double_schur() must be run first")
-        self.sys, self.inner = sys_, inner
-        m = sys_.maps
+        self.sys, self.inner = sys, inner
+        m = sys.maps
         self.n, self.nc = m.n_vv_free, m.n_cpl_free
-        nt = sys_.S_dev.shape[0]
+        nt = sys.S_dev.shape[0]
         self.nt = nt
-        self.bubble = empty(nt * sys_.z["n_int"])
+        self.bubble = empty(nt * sys.z["n_int"])
         self.acc, self.wc = empty(self.nc), empty(self.nc)
         self.zc = empty(self.nc)
 
@@ -430,7 +517,8 @@ class SaddlePreconditioner:
     (reference `preconditioners.py:405-420`):
         a = V r_u;  dp = P (r_p - B a);  du = a - V (B^T dp)."""
 
-    def __init__(self, velocity_apply, pressure: PressureMassPrecond, B):
+    def __init__(self, velocity_apply, pressure: PressureMassPrecond, B_free):
+        B = B_free
         self.velocity_apply, self.pressure, self.B = velocity_apply, pressure, B
         self.n_v, self.n_p = B.n_v, B.n_p
         self._a, self._bt, self._v2 = empty(self.n_v), empty(self.n_v), empty(self.n_v)

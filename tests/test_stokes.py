@@ -81,7 +81,7 @@ def test_gpu_saddle_operator_and_preconditioner(cuda, name, cfg, n):
     assert rel(Bt, _csr(g, "B")[:, fes.vv_free].T @ g["probe_v"][nv:]) <= 1e-12
     mp = pc.PressureMassPrecond.build(fes, prob.nu)
     for comp in ("additive", "multiplicative"):
-        vel = velocity_preconditioner(fes, sys_, prob.nu, SolverOptions(composition=comp))
+        vel = velocity_preconditioner(fes, sys_, prob.nu, SolverOptions(smoother="jacobi", composition=comp))
         P = pc.SaddlePreconditioner(vel, mp, K.B)
         assert rel(P(g["probe_v"]), g[f"probe_P_{comp}"]) <= 1e-10
 
@@ -100,7 +100,7 @@ def test_gpu_gmres_matches_reference(cuda, name, cfg, n):
     assert rel(rhs, g["rhs"]) <= 1e-12
     mp = pc.PressureMassPrecond.build(fes, prob.nu)
     for comp in ("additive", "multiplicative"):
-        vel = velocity_preconditioner(fes, sys_, prob.nu, SolverOptions(composition=comp))
+        vel = velocity_preconditioner(fes, sys_, prob.nu, SolverOptions(smoother="jacobi", composition=comp))
         P = pc.SaddlePreconditioner(vel, mp, K.B)
         x, rep = gmres(K, rhs, P, rtol=1e-8, maxit=500)
         ref_it = int(g[f"gmres_{comp}_iters"])
@@ -120,7 +120,7 @@ def test_gpu_solve_stokes_end_to_end(cuda):
     g = golden("stokes_c2_n3")
     prob, fes = _setup(2, 3)
     r = solve_stokes(prob, prob.k, prob.nu,
-                     SolverOptions(mode="stokes", composition="additive", rtol=1e-10,
+                     SolverOptions(mode="stokes", smoother="jacobi", composition="additive", rtol=1e-10,
                                    maxit=500))
     assert r.report.converged
     free = fes.vv_free

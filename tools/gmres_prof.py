@@ -21,7 +21,7 @@ prob = baseline_config(2)
 fes = FeSystem(prob.mesh, prob.regions, prob.k)
 sys_ = double_schur(condense_sigma_omega(fes, prob.nu, prob.body_force))
 K = SaddleOperator(sys_)
-vel = velocity_preconditioner(fes, sys_, prob.nu, SolverOptions(composition="additive"))
+vel = velocity_preconditioner(fes, sys_, prob.nu, SolverOptions(smoother="jacobi", composition="additive"))
 P = pc.SaddlePreconditioner(vel, pc.PressureMassPrecond.build(fes, prob.nu), K.B)
 rhs = torch.from_numpy(np.concatenate(condensed_rhs(fes, sys_))).cuda()
 it = int(os.environ.get("GMRES_IT", "1000"))

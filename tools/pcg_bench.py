@@ -22,7 +22,7 @@ S = SOperator(sys_)
 b = torch.from_numpy(condensed_rhs(fes, sys_)[0]).cuda()
 out = {}
 for comp in ("additive", "multiplicative"):
-    M = velocity_preconditioner(fes, sys_, prob.nu, SolverOptions(composition=comp))
+    M = velocity_preconditioner(fes, sys_, prob.nu, SolverOptions(smoother="jacobi", composition=comp))
     cg(S, b, M, rtol=1e-8, maxit=2000)
     ts = []
     for _ in range(N):

@@ -23,7 +23,7 @@ b = torch.from_numpy(condensed_rhs(fes, sys_)[0]).cuda()
 for top in [int(v) for v in sys.argv[1:]] or [4096]:
     coarse.TOP_MAX = top
     t0 = time.perf_counter()
-    M = velocity_preconditioner(fes, sys_, prob.nu, SolverOptions(composition="additive"))
+    M = velocity_preconditioner(fes, sys_, prob.nu, SolverOptions(smoother="jacobi", composition="additive"))
     setup = time.perf_counter() - t0
     cg(S, b, M, rtol=1e-8, maxit=400)
     ts = []

@@ -34,7 +34,7 @@ if what in ("all", "cfg"):
     prob = baseline_config(cfg, n if cfg == 2 else None)
     fes = FeSystem(prob.mesh, prob.regions, prob.k)
     sys_ = double_schur(condense_sigma_omega(fes, prob.nu, prob.body_force))
-    M = velocity_preconditioner(fes, sys_, prob.nu, SolverOptions(composition=os.environ.get("PROF_COMP", "multiplicative")))
+    M = velocity_preconditioner(fes, sys_, prob.nu, SolverOptions(smoother="jacobi", composition=os.environ.get("PROF_COMP", "multiplicative")))
     x, rep = cg(SOperator(sys_), condensed_rhs(fes, sys_)[0], M, rtol=1e-8, maxit=3)
     torch.cuda.synchronize()
     print("iters", rep.iterations)

@@ -17,7 +17,7 @@ comp = os.environ.get("PROF_COMP", "additive")
 prob = baseline_config(cfg)
 fes = FeSystem(prob.mesh, prob.regions, prob.k)
 sys_ = double_schur(condense_sigma_omega(fes, prob.nu, prob.body_force))
-M = velocity_preconditioner(fes, sys_, prob.nu, SolverOptions(composition=comp))
+M = velocity_preconditioner(fes, sys_, prob.nu, SolverOptions(smoother="jacobi", composition=comp))
 S = SOperator(sys_)
 b = torch.from_numpy(condensed_rhs(fes, sys_)[0]).cuda()
 torch.cuda.synchronize()

@@ -33,7 +33,7 @@ S = SOperator(sys_)
 b = torch.from_numpy(condensed_rhs(fes, sys_)[0]).cuda()
 for comp in ("additive", "multiplicative"):
     t0 = time.perf_counter()
-    M = velocity_preconditioner(fes, sys_, prob.nu, SolverOptions(composition=comp))
+    M = velocity_preconditioner(fes, sys_, prob.nu, SolverOptions(smoother="jacobi", composition=comp))
     torch.cuda.synchronize()
     t_sup = time.perf_counter() - t0
     t0 = time.perf_counter()

@@ -15,7 +15,7 @@ from paper_2207_08481_b200.problems import baseline_config  # noqa: E402
 prob = baseline_config(2)
 fes = FeSystem(prob.mesh, prob.regions, prob.k)
 sys_ = double_schur(condense_sigma_omega(fes, prob.nu, prob.body_force))
-M = velocity_preconditioner(fes, sys_, prob.nu, SolverOptions(composition="additive"))
+M = velocity_preconditioner(fes, sys_, prob.nu, SolverOptions(smoother="jacobi", composition="additive"))
 sm = M.inner.smoother
 nc = sys_.maps.n_cpl_free
 r = torch.randn(nc, dtype=torch.float64, device="cuda")
