@@ -201,12 +201,32 @@ def microbench(R):
     print(path)
 
 
+def microbench_stream(R, keep=256, chunk=65536):
+    """The first `keep` elements of the SURVEY §8d config-5 stream as the
+    full-size run draws it: default_rng(3), G for a whole 65,536-element
+    chunk, then B for that chunk; S by the reference idiom
+    (condensation.py:216-224).  A and B are regenerated by the readers."""
+    import scipy.linalg as sla
+    rng = np.random.default_rng(3)
+    G = rng.standard_normal((chunk, 60, 60))[:keep]
+    B = rng.standard_normal((chunk, 60, 36))[:keep]
+    A = G @ np.swapaxes(G, 1, 2) + 60 * np.eye(60)
+    S = np.array([B[i].T @ sla.cho_solve(sla.cho_factor(A[i], check_finite=False),
+                                         B[i], check_finite=False) for i in range(keep)])
+    path = os.path.join(OUT, "micro_stream.npz")
+    np.savez_compressed(path, S=S, keep=keep, chunk=chunk, seed=3)
+    print(path)
+
+
 def main():
     os.makedirs(OUT, exist_ok=True)
     R = _ref()
     if "--postcheck" in sys.argv:
         postcheck_case(R, "postcheck_c2_n3", 2, 3)
         postcheck_case(R, "postcheck_c3_n2", 3, 2)
+        return
+    if "--micro-stream" in sys.argv:
+        microbench_stream(R)
         return
     if "--stokes" in sys.argv:
         stokes_case(R, "stokes_c1_n2", 1, 2)
@@ -218,6 +238,7 @@ def main():
     case(R, "c3_n2", 3, 2)
     case(R, "cfg1", 1, 16, with_matrices=False)
     microbench(R)
+    microbench_stream(R)
     stokes_case(R, "stokes_c1_n2", 1, 2)
     stokes_case(R, "stokes_c2_n3", 2, 3)
     stokes_case(R, "stokes_c3_n2", 3, 2)

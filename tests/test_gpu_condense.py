@@ -69,3 +69,25 @@ def test_condense_matches_oracle(cuda, cfg, n):
         ob = O.element_blocks(fes, t, prob.nu)
         S_ref, _ = O.condense_element(*ob[:5])
         assert rel(got[t], S_ref) <= TOL, (t, rel(got[t], S_ref))
+
+
+def test_spd_schur_survey_stream_matches_reference(cuda):
+    """The first 256 elements of the SURVEY §8d config-5 stream exactly as
+    the full-size bench draws it (default_rng(3): G for the whole 65,536
+    chunk, then B) against the reference idiom's S (micro_stream.npz)."""
+    import torch
+    from paper_2207_08481_b200 import engine
+    g = golden("micro_stream")
+    keep, chunk = int(g["keep"]), int(g["chunk"])
+    rng = np.random.default_rng(int(g["seed"]))
+    G = rng.standard_normal((chunk, 60, 60))[:keep]
+    B = rng.standard_normal((keep, 60, 36))          # = the first keep of the chunk's B
+    A = G @ np.swapaxes(G, 1, 2) + 60 * np.eye(60)
+    r, c = np.tril_indices(60)
+    S = torch.empty((keep, 36 * 37 // 2), dtype=torch.float64, device="cuda")
+    info = torch.empty(keep, dtype=torch.int32, device="cuda")
+    engine.spd_schur(60, 36, engine.to_dev(np.ascontiguousarray(A[:, r, c])),
+                     engine.to_dev(B), out=S, info=info)
+    got = engine.unpack_sym(S.cpu().numpy(), 36)
+    assert not info.any()
+    assert max(rel(got[i], g["S"][i]) for i in range(keep)) <= 1e-12
