@@ -19,6 +19,8 @@
 // the solver path take the structured kernels of condense_struct.cu /
 // condense_fused.cu; this dense engine serves the config-5 microbench and
 // user-supplied blocks without the MCS structure.)
+#include <cstdlib>
+
 #include "elim_v5.cuh"
 
 namespace mcs {
@@ -217,6 +219,10 @@ static int persistent_grid(Kern k, int threads, size_t smem, int64_t n) {
   return static_cast<int>(n < g ? n : g);
 }
 
+template <int NS, int NC>
+int launch_spd_schur_w2(const double* A, const double* B, double* S, int* info, int64_t batch,
+                        cudaStream_t st);   // micro.cu
+
 }  // namespace mcs
 
 using namespace mcs;
@@ -225,7 +231,12 @@ MCS_API int mcs_spd_schur_batched(int n, int m, int64_t batch, const double* A_p
                                   const double* B, double* S_packed, int* info, void* stream) {
   if (batch <= 0) return 0;
   auto st = static_cast<cudaStream_t>(stream);
-  if (n == 60 && m == 36) return launch_spd_schur_v5<60, 36, 4, 5>(A_packed_lower, B, S_packed, info, batch, st);
+  // default: the two-warp engine of micro.cu; MCS_MICRO=5: the v5 engine
+  static const int which = getenv("MCS_MICRO") ? atoi(getenv("MCS_MICRO")) : 2;
+  if (n == 60 && m == 36) {
+    if (which == 5) return launch_spd_schur_v5<60, 36, 4, 5>(A_packed_lower, B, S_packed, info, batch, st);
+    return launch_spd_schur_w2<60, 36>(A_packed_lower, B, S_packed, info, batch, st);
+  }
   return -1000;  // unsupported shape (compiled instantiations only)
 }
 
