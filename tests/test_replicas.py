@@ -48,7 +48,7 @@ def test_reference_arm_torchrun_two_ranks():
     cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node=2",
            "--master-addr", "127.0.0.1", "--master-port", str(_free_port()), "bench.py",
            "--impl", "reference", "--gpus", "2", "--cfg", "1", "--steps", "1", "--warmup", "3",
-           "--ref-sample-per-core", "1"]
+           "--ref-elements", "16"]
     p = subprocess.run(cmd, cwd=ROOT, capture_output=True, text=True, timeout=600)
     assert p.returncode == 0, p.stderr[-2000:]
     lines = [ln for ln in p.stdout.splitlines() if ln.startswith("{")]
