@@ -212,10 +212,10 @@ def test_gpu_fused_matches_oracle(cuda, cfg, n, k):
         S_ref, _ = O.condense_element(*ob[:5])
         assert rel(S_got[t], S_ref) <= 1e-12, ("S_T", t)
         Soo, X, Sd_ref = O.double_schur_element(S_ref, k)
-        assert rel(E[t, :ni * nc].reshape(ni, nc), X) <= 1e-10, ("X", t)
+        assert rel(E[t, :ni * nc].reshape(ni, nc), X) <= 1e-12, ("X", t)
         Sinv = engine.unpack_sym(E[t, ni * nc:ni * nc + ni * (ni + 1) // 2], ni)
-        assert rel(Sinv, np.linalg.inv(Soo)) <= 1e-10, ("Soo^-1", t)
-        assert rel(Sd_got[t], Sd_ref) <= 1e-10, ("Sd", t)
+        assert rel(Sinv, np.linalg.inv(Soo)) <= 1e-12, ("Soo^-1", t)
+        assert rel(Sd_got[t], Sd_ref) <= 1e-12, ("Sd", t)
 
 
 @pytest.mark.gpu
@@ -262,10 +262,10 @@ def test_gpu_double_schur_kernel_matches_oracle(cuda, k):
     Sd_got = engine.unpack_sym(Sd.cpu().numpy(), nc)
     for t in range(nt):
         Soo, X, Sd_ref = O.double_schur_element(S_all[t], k)
-        assert rel(E[t, :ni * nc].reshape(ni, nc), X) <= 1e-10
+        assert rel(E[t, :ni * nc].reshape(ni, nc), X) <= 1e-12
         Sinv = engine.unpack_sym(E[t, ni * nc:ni * nc + ni * (ni + 1) // 2], ni)
-        assert rel(Sinv, np.linalg.inv(Soo)) <= 1e-10
-        assert rel(Sd_got[t], Sd_ref) <= 1e-10
+        assert rel(Sinv, np.linalg.inv(Soo)) <= 1e-12
+        assert rel(Sd_got[t], Sd_ref) <= 1e-12
 
 
 @pytest.mark.gpu
