@@ -11,6 +11,8 @@
 // Outputs:
 //   ext record  [X (n_int x ncpl, row-major) | S_oo^-1 (lower packed)]  (even stride)
 //   Sd_T        lower packed (even stride)
+#include <cstdlib>
+
 #include "elim_v5.cuh"
 
 namespace mcs {
@@ -126,7 +128,16 @@ MCS_API int mcs_double_schur(int k, int64_t nt, const double* S_packed, double* 
     case 3: return launch_double_schur_v5<3, 2, 6>(S_packed, ext, Sd_packed, info, nt, st);
     case 4: return launch_double_schur_v5<4, 4, 4>(S_packed, ext, Sd_packed, info, nt, st);
     case 5: return launch_double_schur_v5<5, 4, 4>(S_packed, ext, Sd_packed, info, nt, st);
-    case 6: return launch_double_schur_v5<6, 8, 2>(S_packed, ext, Sd_packed, info, nt, st);
+    case 6: {
+      // MCS_DS6 = 0..3 selects the (warps, CTAs/SM) variant (A/B measurements)
+      static const int v = getenv("MCS_DS6") ? atoi(getenv("MCS_DS6")) : 0;
+      switch (v) {
+        case 1: return launch_double_schur_v5<6, 2, 6>(S_packed, ext, Sd_packed, info, nt, st);
+        case 2: return launch_double_schur_v5<6, 4, 4>(S_packed, ext, Sd_packed, info, nt, st);
+        case 3: return launch_double_schur_v5<6, 4, 6>(S_packed, ext, Sd_packed, info, nt, st);
+        default: return launch_double_schur_v5<6, 8, 2>(S_packed, ext, Sd_packed, info, nt, st);
+      }
+    }
   }
   return -1000;
 }

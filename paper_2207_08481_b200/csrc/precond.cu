@@ -9,6 +9,8 @@
 //  A10 CSR SpMV y = alpha*A x + beta*y for E_c and its explicitly stored
 //      transpose (preconditioners.py:316-317); a sub-warp per row with a
 //      fixed-order shuffle reduction (deterministic).
+#include <cstdlib>
+
 #include "common.cuh"
 
 namespace mcs {
@@ -103,6 +105,35 @@ __global__ void __launch_bounds__(64)
   }
 }
 
+// Thread per (facet, block row): a CTA of B warps covers 32 facets, warp w
+// computes row w of every facet's x[blk] = Binv r[blk].  Nine times the
+// threads of the facet-per-thread kernel (each with 9 + 9 + 9 independent
+// loads); the shared packed entries, indices and gathered r come from L1/L2.
+// Kept as an A/B variant (MCS_JAC_VARIANT=2): slower than one thread per
+// facet at cfg2 (14.3 vs 10.2 us event time).
+template <int B>
+__global__ void __launch_bounds__(32 * B)
+    jacobi_rows_kernel(const double* __restrict__ binv, const int* __restrict__ bidx, int nblk,
+                       const double* r, double* __restrict__ x, double scale_inv) {
+  const int row = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int f = blockIdx.x * 32 + lane;
+  const int ff = f < nblk ? f : nblk - 1;
+  double a[B];
+  int id[B];
+#pragma unroll
+  for (int j = 0; j < B; ++j) {
+    a[j] = __ldg(binv + (int64_t)(row >= j ? pk(row, j) : pk(j, row)) * nblk + ff);
+    id[j] = __ldg(bidx + (int64_t)j * nblk + ff);
+  }
+  pdl_wait();   // the block inverses and indices are in flight; r may now be read
+  pdl_trigger();
+  if (f >= nblk) return;
+  double s = 0.0;
+#pragma unroll
+  for (int j = 0; j < B; ++j) s = fma(a[j], id[j] >= 0 ? r[id[j]] : 0.0, s);
+  if (id[row] >= 0) x[id[row]] = s * scale_inv;
+}
+
 template <int LANES>
 __global__ void csr_spmv_kernel(int nrows, const int* __restrict__ ptr, const int* __restrict__ col,
                                 const double* __restrict__ val, const double* x,
@@ -145,6 +176,20 @@ MCS_API int mcs_jacobi_apply(int k, int nblk, const double* binv, const int* bid
                              const double* r, double* x, double scale_inv, void* stream) {
   if (nblk <= 0) return 0;
   auto st = static_cast<cudaStream_t>(stream);
+  // default: thread per facet.  MCS_JAC_VARIANT=2: thread per (facet, row),
+  // measured slower at cfg2 (14.3 vs 10.2 us, profiles/r02/jacobi_variants.txt)
+  static const int variant = getenv("MCS_JAC_VARIANT") ? atoi(getenv("MCS_JAC_VARIANT")) : 1;
+  if (variant == 2) {
+    const int gr = (nblk + 31) / 32;
+    switch (k) {
+      case 2: return launch_pdl_g(PDL_PREC, jacobi_rows_kernel<5>, gr, 32 * 5, 0, st, binv, bidx, nblk, r, x, scale_inv);
+      case 3: return launch_pdl_g(PDL_PREC, jacobi_rows_kernel<7>, gr, 32 * 7, 0, st, binv, bidx, nblk, r, x, scale_inv);
+      case 4: return launch_pdl_g(PDL_PREC, jacobi_rows_kernel<9>, gr, 32 * 9, 0, st, binv, bidx, nblk, r, x, scale_inv);
+      case 5: return launch_pdl_g(PDL_PREC, jacobi_rows_kernel<11>, gr, 32 * 11, 0, st, binv, bidx, nblk, r, x, scale_inv);
+      case 6: return launch_pdl_g(PDL_PREC, jacobi_rows_kernel<13>, gr, 32 * 13, 0, st, binv, bidx, nblk, r, x, scale_inv);
+      default: return -1000;
+    }
+  }
   const int grid = (nblk + 63) / 64;
   switch (k) {
     case 2: return launch_pdl_g(PDL_PREC, jacobi_apply_kernel<5>, grid, 64, 0, st, binv, bidx, nblk, r, x, scale_inv);
