@@ -216,6 +216,10 @@ int mcs_cg_update_gated(int64_t n, double* x, double* r, const double* p, const 
 int mcs_xpby(int64_t n, const double* z, double* p, const double* sc, int num, int den,
              void* stream);
 int mcs_axpby(int64_t n, double a, const double* x, double b, double* y, void* stream);
+/* y = x / d elementwise (PressureMassPrecond.apply, preconditioners.py:400-401) */
+int mcs_vdiv(int64_t n, const double* x, const double* d, double* y, void* stream);
+/* y[0..n) = 0 as a memset node (accumulation targets of the atomic scatters) */
+int mcs_zero(int64_t n, double* y, void* stream);
 
 /* ---- A13 PCG loop as one CUDA graph (csrc/pcg_loop.cu) ------------------
  * Replaces the host iteration loop of krylov.py:103-137 (one Python

@@ -75,6 +75,8 @@ SIGNATURES = {
     "mcs_cg_update_gated": [_l, _p, _p, _p, _p, _p, _i, _i, _i, _i, _i, _i, _i, _p, _p, _p],
     "mcs_xpby": [_l, _p, _p, _p, _i, _i, _p],
     "mcs_axpby": [_l, _d, _p, _d, _p, _p],
+    "mcs_vdiv": [_l, _p, _p, _p, _p],
+    "mcs_zero": [_l, _p, _p],
     # pcg_loop.cu
     "mcs_pcg_loop_build": [_p, _p, _p, _i, _i, _i, _i, _i, _i, _i, _p],
     "mcs_pcg_loop_launch": [_p, _p, _i, _p],
@@ -131,3 +133,39 @@ def call(name, *args):
         raise McsError(f"{name} failed with CUDA error {-rc}"
                        if rc > -1000 else f"{name}: unsupported arguments ({rc})")
     return rc
+
+
+# ---- NVTX ranges per kernel group: one range per public call
+# (condensation, operator applies, preconditioner stages, Krylov solves) so
+# Nsight timelines / `ncu --nvtx --nvtx-include` can select a group.
+# MCS_NVTX=0 turns them off.  Inside a CUDA-graph replay no Python runs, so
+# the ranges cost nothing on the captured PCG loop.
+_NVTX = os.environ.get("MCS_NVTX", "1") != "0"
+
+
+class nvtx:
+    """Context manager / decorator: an NVTX range named `mcs:<name>`."""
+
+    def __init__(self, name):
+        self.name = "mcs:" + name
+
+    def __enter__(self):
+        if _NVTX:
+            import torch
+            torch.cuda.nvtx.range_push(self.name)
+        return self
+
+    def __exit__(self, *exc):
+        if _NVTX:
+            import torch
+            torch.cuda.nvtx.range_pop()
+        return False
+
+    def __call__(self, fn):
+        import functools
+
+        @functools.wraps(fn)
+        def wrapped(*a, **kw):
+            with self:
+                return fn(*a, **kw)
+        return wrapped

@@ -173,6 +173,7 @@ class CondensedSystem:
             raise ValueError(f"expected a vector over all {self.fes.n_vv} (V, Vhat) dofs")
         return x, on_host
 
+    @_abi.nvtx("apply_S_factorized")
     def apply_S_factorized(self, x_full, stream=None):
         """S @ x over all (V, Vhat) dofs through the exact triangular
         factorisation (reference `condensation.py:104-122`), on the GPU
@@ -187,6 +188,7 @@ class CondensedSystem:
                   _abi.ptr(x), _abi.ptr(y), _abi.stream(stream))
         return y.cpu().numpy() if on_host else y
 
+    @_abi.nvtx("harmonic_extend")
     def harmonic_extend(self, x_full, stream=None):
         """Energy-minimal completion of the interior bubble dofs, out_o =
         -X x_c per element (reference `condensation.py:93-102`), on the GPU."""
@@ -228,6 +230,7 @@ class CondensedSystem:
             self._recovery = list(R.cpu().numpy())
         return self._recovery
 
+    @_abi.nvtx("recover_stress")
     def recover_stress(self, x_full, stream=None):
         """Element-wise (sigma, omega) from a velocity vector over all (V, Vhat)
         dofs (reference `condensation.py:64-74`), on the GPU
@@ -273,6 +276,7 @@ def _fused_tables(k, refs):
 STRUCT_TOL = 1e-10
 
 
+@_abi.nvtx("condense")
 def condense_sigma_omega(fes, nu: float, body_force=None, blocks=None,
                          stream=None) -> CondensedSystem:
     """Eliminate (sigma, omega) element-wise on the GPU (reference
@@ -321,6 +325,7 @@ def condense_sigma_omega(fes, nu: float, body_force=None, blocks=None,
     return sys_
 
 
+@_abi.nvtx("double_schur")
 def double_schur(sys: CondensedSystem, stream=None) -> CondensedSystem:
     """Eliminate interior bubbles per element on the GPU (reference
     `condensation.py:191-239`); mutates and returns `sys`."""

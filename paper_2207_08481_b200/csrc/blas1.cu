@@ -123,6 +123,16 @@ __global__ void axpby_kernel(int64_t n, double a, const double* __restrict__ x, 
     y[i] = b == 0.0 ? a * x[i] : fma(a, x[i], b * y[i]);
 }
 
+// y = x / d (elementwise, IEEE division: the reference's r / diag)
+__global__ void vdiv_kernel(int64_t n, const double* __restrict__ x, const double* __restrict__ d,
+                            double* __restrict__ y) {
+  pdl_wait();
+  pdl_trigger();
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x)
+    y[i] = x[i] / d[i];
+}
+
 static int grid_for(int64_t n);
 
 }  // namespace mcs
@@ -191,4 +201,16 @@ MCS_API int mcs_axpby(int64_t n, double a, const double* x, double b, double* y,
   if (n <= 0) return 0;
   auto st = static_cast<cudaStream_t>(stream);
   return launch_pdl_g(PDL_BLAS, axpby_kernel, grid_for(n), 256, 0, st, n, a, x, b, y);
+}
+
+MCS_API int mcs_vdiv(int64_t n, const double* x, const double* d, double* y, void* stream) {
+  if (n <= 0) return 0;
+  auto st = static_cast<cudaStream_t>(stream);
+  return launch_pdl_g(PDL_BLAS, vdiv_kernel, grid_for(n), 256, 0, st, n, x, d, y);
+}
+
+// zero n doubles with a memset node (no kernel launch)
+MCS_API int mcs_zero(int64_t n, double* y, void* stream) {
+  if (n <= 0) return 0;
+  return err_code(cudaMemsetAsync(y, 0, (size_t)n * sizeof(double), static_cast<cudaStream_t>(stream)));
 }

@@ -175,6 +175,7 @@ _NO_LOOP = __import__("os").environ.get("MCS_NO_LOOP", "0") == "1"
 _LOOP_CAP = 4096   # steps of device-side (p'Ap, rr) history
 
 
+@_abi.nvtx("cg")
 def cg(apply_A, b, apply_M=None, rtol=1e-8, maxit=1000, stream=None, use_graph=True):
     """Preconditioned CG.  `apply_A` / `apply_M` are device operators
     (objects with `.apply(v, out=)`, or callables on CUDA tensors).  `b` may
@@ -288,6 +289,7 @@ def _op(op, v, out, host_callables=False):
 _GS_STATS = {"steps": 0, "second_pass": 0}
 
 
+@_abi.nvtx("gmres")
 def gmres(apply_A, b, apply_M=None, rtol=1e-6, maxit=500, project=None, x0=None):
     """Full (non-restarted) right-preconditioned GMRES (reference
     `krylov.py:25-100`) with the Krylov basis in HBM.
@@ -330,15 +332,19 @@ def gmres(apply_A, b, apply_M=None, rtol=1e-6, maxit=500, project=None, x0=None)
         return finish(x0d)
     cap = min(maxit + 1, 64)
     V = torch.empty((cap, n), dtype=torch.float64, device="cuda")
-    V[0].copy_(r0).mul_(1.0 / beta)
+    _abi.call("mcs_axpby", n, 1.0 / beta, _abi.ptr(r0), 0.0, _abi.ptr(V[0]), _abi.stream(None))
     H = np.zeros((maxit + 1, maxit))
     cs, sn = np.zeros(maxit), np.zeros(maxit)
     g = np.zeros(maxit + 1)
     g[0] = beta
     partial = torch.empty(_abi.call("mcs_mdot_len") * (maxit + 1), dtype=torch.float64,
                           device="cuda")
-    h1 = torch.empty(maxit + 1, dtype=torch.float64, device="cuda")
-    h2 = torch.empty(maxit + 1, dtype=torch.float64, device="cuda")
+    # the per-step read-back (||w|| before / after each pass, gate, both h
+    # columns): two D2H copies into one pinned buffer, no gather kernel
+    hh = torch.empty(2 * (maxit + 1), dtype=torch.float64, device="cuda")
+    h1, h2 = hh[:maxit + 1], hh[maxit + 1:]
+    nsc = ws.TMP3 - ws.TMP + 1
+    back_h = torch.empty(nsc + 2 * (maxit + 1), dtype=torch.float64).pin_memory()
     z, w = empty(n), empty(n)
     j = 0
     while j < maxit:
@@ -367,10 +373,14 @@ def gmres(apply_A, b, apply_M=None, rtol=1e-6, maxit=500, project=None, x0=None)
         _abi.call("mcs_gemv_acc_gated", m, n, n, _abi.ptr(V), _abi.ptr(h2), -1.0, 1.0,
                   _abi.ptr(w), gate, _abi.stream(None))
         ws.dot(w, w, ws.TMP3)
-        back = torch.cat((ws.sc[ws.TMP:ws.TMP3 + 1], h1[:m], h2[:m])).cpu().numpy()
+        back_h[:nsc].copy_(ws.sc[ws.TMP:ws.TMP3 + 1], non_blocking=True)
+        back_h[nsc:nsc + m].copy_(h1[:m], non_blocking=True)
+        back_h[nsc + m:nsc + 2 * m].copy_(h2[:m], non_blocking=True)
+        torch.cuda.current_stream().synchronize()
+        back = back_h.numpy()
         wnorm, hnext = float(np.sqrt(back[0])), float(np.sqrt(back[ws.TMP2 - ws.TMP]))
-        o = ws.TMP3 - ws.TMP + 1
-        hcol = back[o:o + m]
+        o = nsc
+        hcol = back[o:o + m].copy()
         _GS_STATS["steps"] += 1
         second = not hnext > 0.7071067811865476 * wnorm
         if second != (back[ws.GS_GATE - ws.TMP] == 0.0):
@@ -404,7 +414,8 @@ def gmres(apply_A, b, apply_M=None, rtol=1e-6, maxit=500, project=None, x0=None)
                                  device="cuda")
                 Vn[:V.shape[0]].copy_(V)
                 V = Vn
-            V[j + 1].copy_(w).mul_(1.0 / hsub)
+            _abi.call("mcs_axpby", n, 1.0 / hsub, _abi.ptr(w), 0.0, _abi.ptr(V[j + 1]),
+                      _abi.stream(None))           # V[j+1] = w / h_{j+1,j}, one kernel
         j += 1
         if res <= rtol or happy:
             report.converged = True

@@ -84,6 +84,7 @@ class _ElemOperator:
         self.nt = M_dev.shape[0]
         self.shape = (n, n)
 
+    @_abi.nvtx("apply_elem")
     def apply(self, x, out=None, stream=None):
         xd, host = as_device(x)
         y = out if out is not None else empty(self.n)
@@ -154,7 +155,7 @@ class BOperator:
     def apply_T(self, p, out=None, stream=None):
         pd, host = as_device(p)
         y = out if out is not None else empty(self.n_v)
-        y.zero_()
+        _abi.call("mcs_zero", y.numel(), _abi.ptr(y), _abi.stream(stream))   # memset node
         _abi.call("mcs_apply_BT", self.nq, self.nu, self.nloc, self.nt, _abi.ptr(self.Bpu),
                   _abi.ptr(self.codes), _abi.ptr(pd), _abi.ptr(y), _abi.stream(stream))
         return y.cpu().numpy() if host else y

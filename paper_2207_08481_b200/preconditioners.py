@@ -297,6 +297,7 @@ class FacetBlockSmoother:
         if len(bad):
             raise RuntimeError(f"smoother block {int(bad[0])} not SPD")
 
+    @_abi.nvtx("facet_jacobi")
     def jacobi_apply(self, r, out=None, scale_inv=1.0, stream=None):
         rd, host = as_device(r)
         x = out if out is not None else empty(rd.numel())
@@ -392,6 +393,7 @@ class AspPreconditioner:
             axpby(1.0 / lam, y, 0.0, x)
         return 1.1 * lam
 
+    @_abi.nvtx("coarse_correction")
     def coarse_correction(self, r, x, beta):
         """x = beta*x + E C^-1 E^T r."""
         self.Et.mv(r, self._u)
@@ -462,6 +464,7 @@ class ExtendedAsp:
         self.acc, self.wc = empty(self.nc), empty(self.nc)
         self.zc = empty(self.nc)
 
+    @_abi.nvtx("extended_asp")
     def apply(self, r_free, out=None, stream=None):
         s = self.sys
         rd, host = as_device(r_free)
@@ -505,7 +508,8 @@ class PressureMassPrecond:
     def apply(self, r, out=None, stream=None):
         rd, host = as_device(r)
         out = out if out is not None else empty(len(self.diag))
-        __import__("torch").div(rd, self.diag_dev, out=out)
+        _abi.call("mcs_vdiv", len(self.diag), _abi.ptr(rd), _abi.ptr(self.diag_dev),
+                  _abi.ptr(out), _abi.stream(stream))
         return out.cpu().numpy() if host else out
 
     def mass_matrix(self):
