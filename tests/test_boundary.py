@@ -307,3 +307,40 @@ def test_solve_stokes_elliptic_returns_solve_result(cuda):
     assert rel(np.asarray(r.x_free), g["cg_additive_x"]) <= 1e-7
     with pytest.raises(NotImplementedError):            # the reference default smoother
         D.solve_stokes(prob, prob.k, prob.nu, D.SolverOptions(mode="elliptic"))
+
+
+@pytest.mark.skipif(not os.path.isdir(REF_SRC), reason="reference not present (GPU box)")
+def test_integration_install_and_reference_problem_objects():
+    """integration.install swaps the reference driver's entry points for the
+    GPU ones (and uninstall restores them); the GPU host setup accepts the
+    reference's own Problem / Mesh / BoundaryRegions objects and produces the
+    same dof maps, geometry and free masks as from this package's mesh."""
+    import importlib
+    import sys
+    sys.path.insert(0, REF_SRC)
+    try:
+        rdrv = importlib.import_module("mcstokes.driver")
+        rmesh = importlib.import_module("mcstokes.mesh")
+    finally:
+        sys.path.remove(REF_SRC)
+    from paper_2207_08481_b200 import integration
+    orig = rdrv.solve_stokes
+    integration.install(rdrv)
+    try:
+        assert rdrv.solve_stokes is D.solve_stokes
+        assert rdrv.velocity_preconditioner is D.velocity_preconditioner
+        assert rdrv.SolverOptions is D.SolverOptions
+    finally:
+        integration.uninstall(rdrv)
+    assert rdrv.solve_stokes is orig
+    prob = baseline_config(2, 3)
+    m = rmesh.from_arrays(prob.mesh.vertices, prob.mesh.triangles)
+    regions = rmesh.classify_boundary(m, dirichlet=lambda x: x[0] < 1 - 1e-12,
+                                      neumann=lambda x: x[0] >= 1 - 1e-12)
+    ours = FeSystem(prob.mesh, prob.regions, prob.k)
+    theirs = FeSystem(m, regions, prob.k)           # the GPU host setup on reference objects
+    for a in ("vv_free", "vv_interior", "vv_values", "J", "detJ", "Jinv"):
+        assert np.array_equal(getattr(ours, a), getattr(theirs, a)), a
+    for a in ("dof_v", "dof_vhat", "dof_vbar", "dof_q"):
+        assert np.array_equal(getattr(ours, a).loc2glob, getattr(theirs, a).loc2glob), a
+    assert np.array_equal(ours.dof_v.signs, theirs.dof_v.signs)
