@@ -57,6 +57,12 @@ int mcs_condense_struct(int k, int64_t nt, const double* srecords, double* S_pac
  *      element, Y in shared memory; the compact record never reaches HBM. */
 int mcs_condense_gen(int k, int64_t nt, const double* W, int nwgt, const double* tables,
                      double* S_packed, int* info, void* stream);
+/* k = 5, 6: mcs_condense_gen plus the double Schur outputs in the same kernel
+ *      (replaces condensation.py:159-177 AND :207-226 per element): ext and
+ *      Sd_packed as mcs_double_schur; info bit 0: singular stress block,
+ *      bit 1: S_oo not SPD. */
+int mcs_condense_gen_ds(int k, int64_t nt, const double* W, int nwgt, const double* tables,
+                        double* S_packed, double* ext, double* Sd_packed, int* info, void* stream);
 
 /* ---- fused element pipeline for k <= 4 (replaces assembly.py:49-91 +
  *      condensation.py:159-177 + condensation.py:207-226 per element): one

@@ -29,6 +29,7 @@ SIGNATURES = {
     "mcs_srec_len": [_i],
     "mcs_condense_struct": [_i, _l, _p, _p, _p, _p],
     "mcs_condense_gen": [_i, _l, _p, _i, _p, _p, _p, _p],
+    "mcs_condense_gen_ds": [_i, _l, _p, _i, _p, _p, _p, _p, _p, _p],
     # stokes.cu
     "mcs_apply_B": [_i, _i, _i, _l, _p, _p, _p, _p, _p],
     "mcs_apply_BT": [_i, _i, _i, _l, _p, _p, _p, _p, _p],

@@ -274,6 +274,12 @@ def _fused_tables(k, refs):
         _FUSED[k] = engine.to_dev(engine.fused_tables(refs)[0])
     return _FUSED[k]
 STRUCT_TOL = 1e-10
+# k = 5, 6: the double Schur as a separate warp-per-element kernel (default,
+# 8.9 + 5.1 ms at cfg3) or as the last phase of the condensation kernel
+# (MCS_GEN_DS=1, bitwise identical, measured 14.9 ms: its serial Cholesky
+# phase idles three of the CTA's four warps next to the DMMA streams of the
+# co-resident CTAs)
+_GEN_DS = __import__("os").environ.get("MCS_GEN_DS", "0") == "1"
 
 
 @_abi.nvtx("condense")
@@ -310,7 +316,13 @@ def condense_sigma_omega(fes, nu: float, body_force=None, blocks=None,
                                                      stream=stream)
         pending = (ext, Sd, info)
         loads = load_vectors(fes, refs, body_force)
-    else:                                         # k = 5, 6: no record in HBM either
+    elif _GEN_DS:   # k = 5, 6, MCS_GEN_DS=1: condensation + double Schur in one kernel
+        W = engine.to_dev(element_weights(fes, nu))
+        S_dev, ext, Sd, info = engine.condense_gen_ds(k, nt, W, _fused_tables(k, refs),
+                                                      stream=stream)
+        pending = (ext, Sd, info)
+        loads = load_vectors(fes, refs, body_force)
+    else:       # k = 5, 6: generation-fused condensation; double_schur() runs next
         W = engine.to_dev(element_weights(fes, nu))
         S_dev, info = engine.condense_gen(k, nt, W, _fused_tables(k, refs), stream=stream)
         loads = load_vectors(fes, refs, body_force)

@@ -33,7 +33,9 @@
 //   B  thread per row of Bsig: Y row = (B_m F_m | L_b^-1 b_bubble);
 //   C  S_T = adiv + Y Y^T on the FP64 tensor cores (DMMA m8n8k4, 8x8 output
 //      tiles of the lower triangle spread over the warps), written packed.
-#include "common.cuh"
+#include <cstdlib>
+
+#include "ds_warp.cuh"
 
 namespace mcs {
 
@@ -300,10 +302,11 @@ __device__ __forceinline__ int gen_row_woff(int i) {
 }
 }  // namespace cs
 
-template <int K, int W, int MINB>
+template <int K, int W, int MINB, bool DS>
 __global__ void __launch_bounds__(32 * W, MINB)
     condense_gen_kernel(const double* __restrict__ Wg, int nwgt, const double* __restrict__ tab,
-                        double* __restrict__ ST, int* __restrict__ info, int64_t nt) {
+                        double* __restrict__ ST, double* __restrict__ ext,
+                        double* __restrict__ Sd, int* __restrict__ info, int64_t nt) {
   using Z = Sizes<K>;
   using R = SRec<K>;
   using TB = FTab<K>;
@@ -479,6 +482,34 @@ __global__ void __launch_bounds__(32 * W, MINB)
       }
     }
     __syncthreads();
+    if constexpr (DS) {
+      // ---- D: the double Schur of this element (condensation.py:207-226),
+      // fused: S_T is read back from global memory just written by this CTA
+      // (L2; plain loads, not the non-coherent path), the four warps split the
+      // work (ds_warp.cuh), Y's shared memory holds L, L^-1 and W.
+      using DG = dsw::Geo<K>;
+      static_assert(even(DG::L_LEN) + DG::LI_LEN + DG::W_LEN + DG::NI <= G::NR * YST,
+                    "double-Schur buffers fit in Y");
+      double* Ls = Y;
+      double* LIs = Ls + even(DG::L_LEN);
+      double* Wd = LIs + DG::LI_LEN;
+      double* rdd = Wd + DG::W_LEN;
+      const double* Sp = Se;
+      auto Sg = [&](int a, int b) { return Sp[a >= b ? pk(a, b) : pk(b, a)]; };
+      if (warp == 0) {
+        if (!dsw::chol_soo<K>(Sg, Ls, rdd) && lane == 0) atomicOr(&bad, 2);
+      } else {
+        dsw::stage_soc<K>(Sg, Wd, tid - 32, T - 32);
+      }
+      __syncthreads();
+      if (warp == 0) dsw::linv<K>(Ls, rdd, LIs);
+      __syncthreads();
+      for (int J = warp; J < DG::NCB; J += W) dsw::w_block<K>(LIs, Wd, J);
+      __syncthreads();
+      using EL = ExtLayout<K>;
+      dsw::out_tiles<K>(Sg, LIs, Wd, ext + e * EL::len, Sd + e * EL::sd_len, warp, W);
+      __syncthreads();
+    }
     if (tid == 0 && info) info[e] = bad;
   }
 }
@@ -510,11 +541,12 @@ static int launch_condense_struct(const double* recs, double* ST, int* info, int
   return launch_status();
 }
 
-template <int K, int W, int MINB>
+template <int K, int W, int MINB, bool DS = false>
 static int launch_condense_gen(const double* Wg, int nwgt, const double* tab, double* ST, int* info,
-                               int64_t nt, cudaStream_t st) {
+                               int64_t nt, cudaStream_t st, double* ext = nullptr,
+                               double* Sd = nullptr) {
   using G = cs::GeoGen<K, W>;
-  auto kern = condense_gen_kernel<K, W, MINB>;
+  auto kern = condense_gen_kernel<K, W, MINB, DS>;
   const size_t smem = G::SMEM * sizeof(double);
   cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   int per_sm = 0;
@@ -523,7 +555,7 @@ static int launch_condense_gen(const double* Wg, int nwgt, const double* tab, do
     per_sm = 1;
   const int64_t cap = static_cast<int64_t>(per_sm) * cs_num_sms();
   const int grid = static_cast<int>(nt < cap ? nt : cap);
-  kern<<<grid, 32 * W, smem, st>>>(Wg, nwgt, tab, ST, info, nt);
+  kern<<<grid, 32 * W, smem, st>>>(Wg, nwgt, tab, ST, ext, Sd, info, nt);
   return launch_status();
 }
 
@@ -542,6 +574,23 @@ MCS_API int mcs_condense_gen(int k, int64_t nt, const double* W, int nwgt, const
     case 4: return launch_condense_gen<4, 4, 4>(W, nwgt, tables, S_packed, info, nt, st);
     case 5: return launch_condense_gen<5, 4, 4>(W, nwgt, tables, S_packed, info, nt, st);
     case 6: return launch_condense_gen<6, 4, 4>(W, nwgt, tables, S_packed, info, nt, st);
+  }
+  return -1000;
+}
+
+MCS_API int mcs_condense_gen_ds(int k, int64_t nt, const double* W, int nwgt, const double* tables,
+                                double* S_packed, double* ext, double* Sd_packed, int* info,
+                                void* stream) {
+  if (nt <= 0) return 0;
+  if (nwgt < 30) return -1000;
+  auto st = static_cast<cudaStream_t>(stream);
+  switch (k) {
+    case 5: return launch_condense_gen<5, 4, 4, true>(W, nwgt, tables, S_packed, info, nt, st, ext, Sd_packed);
+    case 6: {
+      static const int v = getenv("MCS_GENDS6") ? atoi(getenv("MCS_GENDS6")) : 4;
+      if (v == 3) return launch_condense_gen<6, 4, 3, true>(W, nwgt, tables, S_packed, info, nt, st, ext, Sd_packed);
+      return launch_condense_gen<6, 4, 4, true>(W, nwgt, tables, S_packed, info, nt, st, ext, Sd_packed);
+    }
   }
   return -1000;
 }

@@ -13,6 +13,7 @@
 //   Sd_T        lower packed (even stride)
 #include <cstdlib>
 
+#include "ds_warp.cuh"
 #include "elim_v5.cuh"
 
 namespace mcs {
@@ -76,6 +77,83 @@ __global__ void __launch_bounds__(32 * W, MINB)
   }
 }
 
+// ---- warp per element (default for every k): the reference's own sequence
+// (condensation.py:207-226) on registers, shared memory and the FP64 tensor
+// cores, no inter-warp barrier:
+//   S_oo = L L^T   lane-per-row Cholesky with shuffles for the pivots (rows
+//                  32.. of k = 6 in shared memory, updated by lanes 0..2);
+//   L^-1           lane-per-column forward substitution, blocked by 8 rows
+//                  (an 8-wide independent update, then an 8-step chain);
+//   W = L^-1 S_oc, X = L^-T W, S_oo^-1 = L^-T L^-1, Sd_T = S_cc - W^T W
+//                  m8n8k4 DMMA over 8x8 output tiles (k steps of 4 rows).
+// S_T is read from global memory (it was written by the condensation kernel
+// just before, so mostly from L2); per warp shared memory holds L, then W,
+// and L^-1.  (The v5 CTA engine above is kept as MCS_DS=5 for A/B.)
+// standalone layout (one warp per element): L, then W over it | L^-1 | rd
+template <int K>
+struct DswLayout {
+  using G = dsw::Geo<K>;
+  static constexpr int o_L = 0;
+  static constexpr int LW = G::L_LEN > G::W_LEN ? G::L_LEN : G::W_LEN;
+  static constexpr int o_LI = LW;
+  static constexpr int o_rd = o_LI + G::LI_LEN;
+  static constexpr int PER_WARP = even(o_rd + G::NI);
+};
+
+template <int K, int WPB>
+__global__ void __launch_bounds__(32 * WPB)
+    double_schur_warp(const double* __restrict__ ST, double* __restrict__ ext,
+                      double* __restrict__ Sd, int* __restrict__ info, int64_t nt) {
+  using G = dsw::Geo<K>;
+  using Y = DswLayout<K>;
+  using L = ExtLayout<K>;
+  extern __shared__ __align__(128) double smem[];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  double* base = smem + warp * Y::PER_WARP;
+  double* Ls = base + Y::o_L;
+  double* Wd = base + Y::o_L;      // W replaces L once L^-1 exists
+  double* LI = base + Y::o_LI;
+  double* rd = base + Y::o_rd;
+  const int64_t nw = (int64_t)gridDim.x * WPB;
+#pragma unroll 1
+  for (int64_t e = (int64_t)blockIdx.x * WPB + warp; e < nt; e += nw) {
+    const double* S = ST + e * L::st_len;
+    auto Sg = [&](int a, int b) { return __ldg(S + (a >= b ? pk(a, b) : pk(b, a))); };
+    // pull the next element's S_T into L2 while this one is eliminated
+    if (e + nw < nt) {
+      const char* nx = reinterpret_cast<const char*>(ST + (e + nw) * L::st_len);
+      for (int off = lane * 128; off < L::st_len * 8; off += 32 * 128)
+        asm volatile("prefetch.global.L2 [%0];" ::"l"(nx + off));
+    }
+    const bool ok = dsw::chol_soo<K>(Sg, Ls, rd);
+    __syncwarp();
+    dsw::linv<K>(Ls, rd, LI);
+    __syncwarp();
+    dsw::stage_soc<K>(Sg, Wd, lane, 32);
+    __syncwarp();
+#pragma unroll 1
+    for (int J = 0; J < G::NCB; ++J) dsw::w_block<K>(LI, Wd, J);
+    dsw::out_tiles<K>(Sg, LI, Wd, ext + e * L::len, Sd + e * L::sd_len, 0, 1);
+    if (lane == 0 && info) info[e] = ok ? 0 : 1;
+    __syncwarp();
+  }
+}
+
+template <int K, int WPB>
+static int launch_double_schur_warp(const double* ST, double* ext, double* Sd, int* info,
+                                    int64_t nt, cudaStream_t st) {
+  auto kern = double_schur_warp<K, WPB>;
+  const size_t smem = (size_t)WPB * DswLayout<K>::PER_WARP * sizeof(double);
+  cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  int per_sm = 0;
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, 32 * WPB, smem) != cudaSuccess ||
+      per_sm < 1)
+    per_sm = 1;
+  const int64_t want = (nt + WPB - 1) / WPB, cap = (int64_t)per_sm * sm_count();
+  kern<<<(int)(want < cap ? want : cap), 32 * WPB, smem, st>>>(ST, ext, Sd, info, nt);
+  return launch_status();
+}
+
 template <int K, int W, int MINB>
 static int launch_double_schur_v5(const double* ST, double* ext, double* Sd, int* info, int64_t nt,
                                   cudaStream_t st) {
@@ -123,6 +201,18 @@ MCS_API int mcs_double_schur(int k, int64_t nt, const double* S_packed, double* 
                              int* info, void* stream) {
   if (nt <= 0) return 0;
   auto st = static_cast<cudaStream_t>(stream);
+  // default: the warp-per-element kernel; MCS_DS=5: the v5 CTA engine
+  static const int ds = getenv("MCS_DS") ? atoi(getenv("MCS_DS")) : 1;
+  if (ds != 5) {
+    switch (k) {
+      case 2: return launch_double_schur_warp<2, 4>(S_packed, ext, Sd_packed, info, nt, st);
+      case 3: return launch_double_schur_warp<3, 4>(S_packed, ext, Sd_packed, info, nt, st);
+      case 4: return launch_double_schur_warp<4, 4>(S_packed, ext, Sd_packed, info, nt, st);
+      case 5: return launch_double_schur_warp<5, 1>(S_packed, ext, Sd_packed, info, nt, st);
+      case 6: return launch_double_schur_warp<6, 1>(S_packed, ext, Sd_packed, info, nt, st);
+    }
+    return -1000;
+  }
   switch (k) {
     case 2: return launch_double_schur_v5<2, 2, 8>(S_packed, ext, Sd_packed, info, nt, st);
     case 3: return launch_double_schur_v5<3, 2, 6>(S_packed, ext, Sd_packed, info, nt, st);

@@ -203,6 +203,24 @@ def recover_stress(k: int, nt: int, W_dev, tables_dev, codes_dev, x_dev, sig=Non
     return sig, om, info
 
 
+def condense_gen_ds(k: int, nt: int, W_dev, tables_dev, stream=None):
+    """k = 5, 6: S_T from the geometry weights AND the double Schur outputs
+    (ext = [X | S_oo^-1], Sd_T) in one kernel (csrc/condense_struct.cu
+    condense_gen_kernel<..., DS = true> + csrc/ds_warp.cuh).  info bit 0:
+    singular stress block, bit 1: S_oo not SPD."""
+    torch = _t()
+    if _abi.call("mcs_fused_table_len", k) != fused_table_layout(k)["len"]:
+        raise _abi.McsError("fused table layout mismatch between Python and libmcsgpu")
+    dev = W_dev.device
+    ST = torch.empty((nt, st_stride(k)), dtype=torch.float64, device=dev)
+    ext = torch.empty((nt, _abi.call("mcs_ext_stride", k)), dtype=torch.float64, device=dev)
+    Sd = torch.empty((nt, _abi.call("mcs_sd_stride", k)), dtype=torch.float64, device=dev)
+    info = torch.empty(nt, dtype=torch.int32, device=dev)
+    _abi.call("mcs_condense_gen_ds", k, nt, _abi.ptr(W_dev), W_dev.shape[1], _abi.ptr(tables_dev),
+              _abi.ptr(ST), _abi.ptr(ext), _abi.ptr(Sd), _abi.ptr(info), _abi.stream(stream))
+    return ST, ext, Sd, info
+
+
 def condense_gen(k: int, nt: int, W_dev, tables_dev, ST=None, info=None, stream=None):
     """S_T from the geometry weights for any k (csrc/condense_struct.cu
     condense_gen_kernel: Bsig regenerated from the fused tables, no record
