@@ -163,6 +163,67 @@ def as_written(cfg=2):
     print(path, os.path.getsize(path) / 1e6, "MB", tm, flush=True)
 
 
+def stokes_written(cfg=2, comps=("additive",)):
+    """Stokes (saddle) mode at the BASELINE size through the reference as
+    written (driver.py:147-161: K = [[S, B^T], [B, 0]] on free dofs,
+    SaddlePreconditioner(velocity_preconditioner, PressureMassPrecond),
+    krylov.gmres), smoother "jacobi", rtol 1e-8.  Vectors: norms + a seeded
+    sample (the full K has 1.26 M unknowns at cfg2)."""
+    import scipy.sparse as sp
+    R = _ref()
+    pc = R["pc"]
+    orig = pc.build_embedding
+    cache = {}
+
+    def build_embedding_memo(fes):
+        if id(fes) not in cache:
+            cache[id(fes)] = orig(fes)
+        return cache[id(fes)]
+
+    pc.build_embedding = build_embedding_memo
+    tm = {}
+    prob, fes = _fes(R, cfg)
+    t0 = time.perf_counter()
+    sys_ = R["condensation"].condense_sigma_omega(fes, prob.nu, prob.body_force)
+    R["condensation"].double_schur(sys_)
+    tm["condense"] = time.perf_counter() - t0
+    free = fes.vv_free
+    S_free = sys_.S[free][:, free].tocsr()
+    B_free = sys_.B[:, free].tocsr()
+    K = sp.bmat([[S_free, B_free.T], [B_free, None]], format="csr")
+    rhs_u, rhs_p = R["driver"].condensed_rhs(fes, sys_)
+    rhs = np.concatenate([rhs_u, rhs_p])
+    mp = pc.PressureMassPrecond.build(fes, prob.nu)
+    idx = sample_index(K.shape[0])
+    out = dict(cfg=cfg, n=fes.mesh.num_triangles, k=prob.k, nu=prob.nu, sample_idx=idx,
+               rhs_norm=np.linalg.norm(rhs), rhs_sample=rhs[idx])
+    v = probe_vector(K.shape[0], seed=21)
+    Kv = K @ v
+    out["probe_Kv_norm"], out["probe_Kv_sample"] = np.linalg.norm(Kv), Kv[idx]
+    for comp in comps:
+        opts = R["driver"].SolverOptions(mode="stokes", target="Sd", smoother="jacobi",
+                                         composition=comp, rtol=1e-8, maxit=1000)
+        t0 = time.perf_counter()
+        vel = R["driver"].velocity_preconditioner(fes, sys_, prob.nu, opts)
+        saddle = pc.SaddlePreconditioner(vel, mp, B_free)
+        tm[f"setup_{comp}"] = time.perf_counter() - t0
+        Pv = saddle.apply(v)
+        out[f"probe_P_{comp}_norm"], out[f"probe_P_{comp}_sample"] = np.linalg.norm(Pv), Pv[idx]
+        t0 = time.perf_counter()
+        x, rep = R["krylov"].gmres(lambda u: K @ u, rhs, saddle.apply, rtol=1e-8, maxit=1000)
+        tm[f"gmres_{comp}"] = time.perf_counter() - t0
+        out[f"gmres_{comp}_iters"] = rep.iterations
+        out[f"gmres_{comp}_res"] = np.array(rep.residuals)
+        out[f"gmres_{comp}_converged"] = rep.converged
+        out[f"gmres_{comp}_x_norm"] = np.linalg.norm(x)
+        out[f"gmres_{comp}_x_sample"] = x[idx]
+        print(comp, rep.iterations, tm, flush=True)
+    out["timings_json"] = repr(tm)
+    path = os.environ.get("MCS_GOLDEN_OUT") or os.path.join(OUT, f"stokes_cfg{cfg}_full.npz")
+    np.savez_compressed(path, **out)
+    print(path, os.path.getsize(path) / 1e6, "MB", tm, flush=True)
+
+
 # ------------------------------------------------------------------ config 3
 
 _G = {}
@@ -398,3 +459,5 @@ if __name__ == "__main__":
         lean(2)
     if "written3" in sys.argv:       # cross-check at small cfg3 meshes
         as_written(3)
+    if "stokes2" in sys.argv:        # Stokes mode (GMRES) at the full cfg2
+        stokes_written(2)

@@ -96,3 +96,36 @@ def test_full_size_pcg_matches_reference(cuda, cfg, comp):
     ref = g[f"cg_{comp}_res"]
     m = min(len(ref), len(rep.residuals))
     np.testing.assert_allclose(rep.residuals[:m], ref[:m], rtol=1e-6, atol=1e-12)
+
+
+def test_full_size_stokes_gmres_matches_reference(cuda):
+    """Stokes (saddle) mode at the full cfg2 size (1.26 M unknowns): GMRES
+    iterations +-1 against the reference as written
+    (`stokes_cfg2_full.npz`, oracle/make_golden_full.py stokes2), K v to
+    1e-10, the saddle preconditioner to 1e-10, x to 1e-6 (the tolerance of
+    tests/test_stokes.py), residual history to 1e-4."""
+    name = "stokes_cfg2_full"
+    if not _have(name):
+        pytest.skip(f"{name}.npz not generated")
+    from paper_2207_08481_b200 import preconditioners as pc
+    from paper_2207_08481_b200.driver import SolverOptions, condensed_rhs, velocity_preconditioner
+    from paper_2207_08481_b200.krylov import gmres
+    from paper_2207_08481_b200.operators import SaddleOperator
+    g = golden(name)
+    prob, fes, sys_ = _system(2)
+    K = SaddleOperator(sys_)
+    rhs = np.concatenate(condensed_rhs(fes, sys_))
+    _check_vec(rhs, g, "rhs", 1e-12)
+    v = np.random.default_rng(21).standard_normal(K.n)
+    _check_vec(K(v), g, "probe_Kv", 1e-10)
+    vel = velocity_preconditioner(fes, sys_, prob.nu,
+                                  SolverOptions(smoother="jacobi", composition="additive"))
+    P = pc.SaddlePreconditioner(vel, pc.PressureMassPrecond.build(fes, prob.nu), K.B)
+    _check_vec(P(v), g, "probe_P_additive", 1e-10)
+    x, rep = gmres(K, rhs, P, rtol=1e-8, maxit=1000)
+    ref_it = int(g["gmres_additive_iters"])
+    assert rep.converged and abs(rep.iterations - ref_it) <= 1, (rep.iterations, ref_it)
+    _check_vec(x, g, "gmres_additive_x", 1e-6)
+    ref = g["gmres_additive_res"]
+    m = min(len(ref), len(rep.residuals))
+    np.testing.assert_allclose(rep.residuals[:m], ref[:m], rtol=1e-4, atol=1e-12)
