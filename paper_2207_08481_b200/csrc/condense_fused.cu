@@ -141,6 +141,36 @@ __device__ __forceinline__ bool chol_rows(double (&a)[N], double (&l)[N], double
   return ok;
 }
 
+// Column `col` of L^-1 for the n x n lower L in shared memory (row stride
+// ls, 1/diag in rd): forward substitution blocked by 8 rows -- the rows of
+// earlier blocks enter as 8 independent accumulations, only the 8 rows of a
+// diagonal block form a dependent chain (an n-step chain otherwise).
+template <int N>
+__device__ __forceinline__ void linv_col(const double* Ls, int ls, const double* rd, int col,
+                                         double (&x)[N]) {
+#pragma unroll
+  for (int jb = 0; jb < N; jb += 8) {
+    double acc[8];
+#pragma unroll
+    for (int u = 0; u < 8; ++u) acc[u] = (jb + u == col) ? 1.0 : 0.0;
+#pragma unroll
+    for (int q = 0; q < jb; ++q)
+#pragma unroll
+      for (int u = 0; u < 8; ++u)
+        if (jb + u < N) acc[u] = fma(-Ls[(jb + u) * ls + q], x[q], acc[u]);
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {
+      const int j = jb + u;
+      if (j < N) {
+        double v = acc[u];
+#pragma unroll
+        for (int q = jb; q < j; ++q) v = fma(-Ls[j * ls + q], x[q], v);
+        x[j] = v * rd[j];
+      }
+    }
+  }
+}
+
 }  // namespace fz
 
 template <int K, int WPB, int MINB>
@@ -277,15 +307,9 @@ __global__ void __launch_bounds__(32 * WPB, MINB)
       Fm[5] = f21;
     }
     __syncwarp();
-    if (lane < nb) {   // column `lane` of L_b^-1 (forward substitution)
+    if (lane < nb) {   // column `lane` of L_b^-1 (blocked forward substitution)
       double x[nb];
-#pragma unroll
-      for (int j = 0; j < nb; ++j) {
-        double acc = (j == lane) ? 1.0 : 0.0;
-#pragma unroll
-        for (int q = 0; q < j; ++q) acc = fma(-Ls[j * nb + q], x[q], acc);
-        x[j] = acc * Rd[j];
-      }
+      fz::linv_col<nb>(Ls, nb, Rd, lane, x);
 #pragma unroll
       for (int j = 0; j < nb; ++j) Li[j * nb + lane] = x[j];
     }
@@ -435,16 +459,11 @@ __global__ void __launch_bounds__(32 * WPB, MINB)
       if (j >= NI || c >= NI) LIs[q] = 0.0;
     }
     __syncwarp();
-    if (lane < NI) {   // column `lane` of L^-1
+    if (lane < NI) {   // column `lane` of L^-1 (blocked forward substitution)
       double x[NI];
+      fz::linv_col<NI>(Loo, NI, Rdo, lane, x);
 #pragma unroll
-      for (int j = 0; j < NI; ++j) {
-        double acc = (j == lane) ? 1.0 : 0.0;
-#pragma unroll
-        for (int q = 0; q < j; ++q) acc = fma(-Loo[j * NI + q], x[q], acc);
-        x[j] = acc * Rdo[j];
-        LIs[j * LST + lane] = x[j];
-      }
+      for (int j = 0; j < NI; ++j) LIs[j * LST + lane] = x[j];
     }
     __syncwarp();
     {   // S_oc (row j = interior dof NEM + j, column c = coupling dof), zero padded, over Loo
