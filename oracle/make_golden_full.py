@@ -219,7 +219,8 @@ def stokes_written(cfg=2, comps=("additive",)):
         out[f"gmres_{comp}_x_sample"] = x[idx]
         print(comp, rep.iterations, tm, flush=True)
     out["timings_json"] = repr(tm)
-    path = os.environ.get("MCS_GOLDEN_OUT") or os.path.join(OUT, f"stokes_cfg{cfg}_full.npz")
+    tag = "" if comps == ("additive",) else "_" + "_".join(comps)
+    path = os.environ.get("MCS_GOLDEN_OUT") or os.path.join(OUT, f"stokes_cfg{cfg}{tag}_full.npz")
     np.savez_compressed(path, **out)
     print(path, os.path.getsize(path) / 1e6, "MB", tm, flush=True)
 
@@ -461,3 +462,5 @@ if __name__ == "__main__":
         as_written(3)
     if "stokes2" in sys.argv:        # Stokes mode (GMRES) at the full cfg2
         stokes_written(2)
+    if "stokes2m" in sys.argv:       # the same, multiplicative composition
+        stokes_written(2, comps=("multiplicative",))

@@ -34,7 +34,8 @@ struct Geo {
   static constexpr int st_(int n) { return (n % 16 == 4 || n % 16 == 12) ? n : st_(n + 1); }
   static constexpr int WST = st_(8 * NCB);
   static constexpr int LST = st_(8 * NIT);
-  static constexpr int L_LEN = NI * NI, LI_LEN = NIR * LST, W_LEN = NIR * WST;
+  static constexpr int NWR = 4 * NIK;                      // rows of W the k steps read
+  static constexpr int L_LEN = NI * NI, LI_LEN = NIR * LST, W_LEN = NWR * WST;
   static constexpr int NTX = NIT * NCB, NTS = NIT * (NIT + 1) / 2, NTD = NCB * (NCB + 1) / 2;
   static constexpr int NTILES = NTX + NTS + NTD;           // output tiles of out_tiles
   static_assert(NX <= 8 && NC <= 64, "lane-per-row factor: at most 8 extra rows");
@@ -188,7 +189,7 @@ __device__ __forceinline__ void stage_soc(SG Sg, double* Wd, int tid, int nthr) 
   constexpr int NI = G::NI, NC = G::NC, NEM = G::NEM, WST = G::WST, NIR = G::NIR;
   // (loads batched 16 deep: each is an L2 round trip)
 #pragma unroll 16
-  for (int q = tid; q < NIR * WST; q += nthr) {
+  for (int q = tid; q < G::NWR * WST; q += nthr) {
     const int j = q / WST, c = q % WST;
     Wd[q] = (j < NI && c < NC) ? Sg(NEM + j, cpl_local<K>(c)) : 0.0;
   }
@@ -212,7 +213,7 @@ __device__ __forceinline__ void w_block(const double* LI, double* Wd, int J) {
   __syncwarp();                                // every lane has read column block J
 #pragma unroll
   for (int I = 0; I < G::NIT; ++I)
-    if (8 * I + g < NIR)
+    if (8 * I + g < G::NWR)                    // rows >= 4 NIK are zero and never read
       *reinterpret_cast<double2*>(Wd + (8 * I + g) * WST + 8 * J + 2 * t) =
           make_double2(cacc[I][0], cacc[I][1]);
   __syncwarp();

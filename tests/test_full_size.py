@@ -98,13 +98,14 @@ def test_full_size_pcg_matches_reference(cuda, cfg, comp):
     np.testing.assert_allclose(rep.residuals[:m], ref[:m], rtol=1e-6, atol=1e-12)
 
 
-def test_full_size_stokes_gmres_matches_reference(cuda):
+@pytest.mark.parametrize("name,comp", [("stokes_cfg2_full", "additive"),
+                                       ("stokes_cfg2_multiplicative_full", "multiplicative")])
+def test_full_size_stokes_gmres_matches_reference(cuda, name, comp):
     """Stokes (saddle) mode at the full cfg2 size (1.26 M unknowns): GMRES
     iterations +-1 against the reference as written
     (`stokes_cfg2_full.npz`, oracle/make_golden_full.py stokes2), K v to
     1e-10, the saddle preconditioner to 1e-10, x to 1e-6 (the tolerance of
     tests/test_stokes.py), residual history to 1e-4."""
-    name = "stokes_cfg2_full"
     if not _have(name):
         pytest.skip(f"{name}.npz not generated")
     from paper_2207_08481_b200 import preconditioners as pc
@@ -119,13 +120,13 @@ def test_full_size_stokes_gmres_matches_reference(cuda):
     v = np.random.default_rng(21).standard_normal(K.n)
     _check_vec(K(v), g, "probe_Kv", 1e-10)
     vel = velocity_preconditioner(fes, sys_, prob.nu,
-                                  SolverOptions(smoother="jacobi", composition="additive"))
+                                  SolverOptions(smoother="jacobi", composition=comp))
     P = pc.SaddlePreconditioner(vel, pc.PressureMassPrecond.build(fes, prob.nu), K.B)
-    _check_vec(P(v), g, "probe_P_additive", 1e-10)
+    _check_vec(P(v), g, f"probe_P_{comp}", 1e-10)
     x, rep = gmres(K, rhs, P, rtol=1e-8, maxit=1000)
-    ref_it = int(g["gmres_additive_iters"])
+    ref_it = int(g[f"gmres_{comp}_iters"])
     assert rep.converged and abs(rep.iterations - ref_it) <= 1, (rep.iterations, ref_it)
-    _check_vec(x, g, "gmres_additive_x", 1e-6)
-    ref = g["gmres_additive_res"]
+    _check_vec(x, g, f"gmres_{comp}_x", 1e-6)
+    ref = g[f"gmres_{comp}_res"]
     m = min(len(ref), len(rep.residuals))
     np.testing.assert_allclose(rep.residuals[:m], ref[:m], rtol=1e-4, atol=1e-12)
