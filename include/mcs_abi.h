@@ -203,6 +203,16 @@ int mcs_mdot_gated(int m, int64_t n, int64_t ld, const double* V, const double* 
 int mcs_gemv_acc_gated(int m, int64_t n, int64_t ld, const double* V, const double* h,
                        double alpha, double beta, double* w, const double* gate, void* stream);
 int mcs_gs_gate(double* sc, int before, int after, int gate, void* stream);
+/* One basis read for the second Gram-Schmidt pass (replaces, per GMRES step,
+ * the gemv w -= V h1, the dot ||w||^2, mcs_gs_gate and the gated mdot):
+ * w <- w - V h1 in place, h2 = V^T w (0 when the gate skips the second pass),
+ * sc[after] = ||w||^2, sc[gate] as mcs_gs_gate.  ph2: [m][mcs_gs_fused_blocks()],
+ * pnrm: [mcs_gs_fused_blocks()].  Returns -1000 when m exceeds the shared-
+ * memory tile (m > 990): the caller then uses the unfused kernels. */
+int mcs_gs_fused_blocks(void);
+int mcs_gs_fused(int m, int64_t n, int64_t ld, const double* V, double* w, const double* h1,
+                 double* ph2, double* pnrm, double* h2, double* sc, int before, int after,
+                 int gate, void* stream);
 
 /* ---- PCG vector algebra (replaces krylov.py:103-137 NumPy ops); deterministic
  *      reductions into device scalars sc[]. */

@@ -39,6 +39,8 @@ SIGNATURES = {
     "mcs_mdot_gated": [_i, _l, _l, _p, _p, _p, _p, _p, _p],
     "mcs_gemv_acc_gated": [_i, _l, _l, _p, _p, _d, _d, _p, _p, _p],
     "mcs_gs_gate": [_p, _i, _i, _i, _p],
+    "mcs_gs_fused_blocks": [],
+    "mcs_gs_fused": [_i, _l, _l, _p, _p, _p, _p, _p, _p, _p, _i, _i, _i, _p],
     # postcheck.cu
     "mcs_post_checks": [_l, _i, _i, _p, _p, _p, _p, _p, _p, _i, _i, _i, _p, _p, _p, _p, _p, _p,
                         _p, _i, _p],

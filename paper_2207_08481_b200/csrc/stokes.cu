@@ -119,6 +119,105 @@ __global__ void gs_gate_kernel(double* sc, int before, int after, int g) {
   sc[g] = (sqrt(sc[after]) > 0.7071067811865476 * sqrt(sc[before])) ? 1.0 : 0.0;
 }
 
+// ---- fused classical Gram-Schmidt pass (krylov.py gmres): given the first
+// pass's h1 = V^T w, one read of the basis V produces
+//   w' = w - V h1               (the first pass's update, in place),
+//   h2 partials = V^T w' and ||w'||^2 partials
+// per CTA column range; gs_final sums them in fixed order, evaluates the DGKS
+// gate and leaves h2 (zero when the gate skips the second pass).  Each CTA
+// stages a tile of SUB basis columns x m rows in shared memory, so every V
+// entry leaves HBM once for both products (three basis reads per step
+// instead of four).  Deterministic: fixed column ranges, fixed row order,
+// fixed reduction trees.
+constexpr int GS_THREADS = 256, GS_SMEM = 64 * 1024;
+
+__global__ void __launch_bounds__(GS_THREADS)
+    gs_fused_kernel(int m, int64_t n, int64_t ld, int sub, const double* __restrict__ V,
+                    double* __restrict__ w, const double* __restrict__ h1,
+                    double* __restrict__ ph2, double* __restrict__ pnrm) {
+  extern __shared__ double tile[];            // [m][sub], then R x sub partials, sub w'
+  const int tid = threadIdx.x;
+  const int R = GS_THREADS / sub;              // row groups of pass a
+  double* part = tile + m * sub;
+  double* wp = part + R * sub;
+  const int64_t span = (n + gridDim.x - 1) / gridDim.x;
+  const int64_t lo = (int64_t)blockIdx.x * span, hi = lo + span < n ? lo + span : n;
+  double h2acc[4] = {0.0, 0.0, 0.0, 0.0};      // rows tid + 256 q (m <= 1024)
+  double nrm = 0.0;
+  const int c = tid % sub, r = tid / sub;
+  for (int64_t c0 = lo; c0 < hi; c0 += sub) {
+    const int cw = (int)(hi - c0 < sub ? hi - c0 : sub);
+    for (int q = tid; q < m * sub; q += GS_THREADS) {
+      const int i = q / sub, cc = q % sub;
+      tile[q] = cc < cw ? V[i * ld + c0 + cc] : 0.0;
+    }
+    __syncthreads();
+    // pass a: column c, rows r, r + R, ... (in order), then the R partials in order
+    double s = 0.0;
+    for (int i = r; i < m; i += R) s = fma(__ldg(h1 + i), tile[i * sub + c], s);
+    part[r * sub + c] = s;
+    __syncthreads();
+    if (tid < sub) {
+      double t = 0.0;
+      for (int q = 0; q < R; ++q) t += part[q * sub + tid];
+      double v = 0.0;
+      if (tid < cw) {
+        v = w[c0 + tid] - t;
+        w[c0 + tid] = v;
+      }
+      wp[tid] = v;
+      nrm = fma(v, v, nrm);
+    }
+    __syncthreads();
+    // pass b: row i, the sub columns in order
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      const int i = tid + GS_THREADS * q;
+      if (i < m) {
+        double a = h2acc[q];
+        for (int cc = 0; cc < sub; ++cc) a = fma(tile[i * sub + cc], wp[cc], a);
+        h2acc[q] = a;
+      }
+    }
+    __syncthreads();
+  }
+#pragma unroll
+  for (int q = 0; q < 4; ++q) {
+    const int i = tid + GS_THREADS * q;
+    if (i < m) ph2[(int64_t)i * gridDim.x + blockIdx.x] = h2acc[q];
+  }
+  // ||w'||^2 of this CTA: the sub column threads in order
+  __syncthreads();
+  if (tid < sub) part[tid] = nrm;
+  __syncthreads();
+  if (tid == 0) {
+    double t = 0.0;
+    for (int q = 0; q < sub; ++q) t += part[q];
+    pnrm[blockIdx.x] = t;
+  }
+}
+
+// h2[i] = sum_cta ph2[i][cta] (in order); sc[after] = sum_cta pnrm; the DGKS
+// gate sc[g] as gs_gate_kernel; h2 = 0 when the gate skips the second pass.
+__global__ void gs_final_kernel(int m, int nblk, const double* __restrict__ ph2,
+                                const double* __restrict__ pnrm, double* __restrict__ h2,
+                                double* sc, int before, int after, int g) {
+  __shared__ double gate;
+  if (threadIdx.x == 0) {
+    double t = 0.0;
+    for (int b = 0; b < nblk; ++b) t += pnrm[b];
+    sc[after] = t;
+    gate = (sqrt(t) > 0.7071067811865476 * sqrt(sc[before])) ? 1.0 : 0.0;
+    sc[g] = gate;
+  }
+  __syncthreads();
+  for (int i = threadIdx.x; i < m; i += blockDim.x) {
+    double s = 0.0;
+    for (int b = 0; b < nblk; ++b) s += ph2[(int64_t)i * nblk + b];
+    h2[i] = gate != 0.0 ? 0.0 : s;
+  }
+}
+
 static int sk_grid(int64_t n) {
   const int64_t g = (n + SK_THREADS - 1) / SK_THREADS;
   return (int)(g < 8 * 148 ? (g < 1 ? 1 : g) : 8 * 148);
@@ -180,5 +279,37 @@ MCS_API int mcs_gemv_acc(int m, int64_t n, int64_t ld, const double* V, const do
 
 MCS_API int mcs_gs_gate(double* sc, int before, int after, int gate, void* stream) {
   gs_gate_kernel<<<1, 1, 0, static_cast<cudaStream_t>(stream)>>>(sc, before, after, gate);
+  return launch_status();
+}
+
+// sub-tile width for m basis vectors (64 KB of shared memory per CTA); 0 =
+// the fused pass is not available (m > 1024: use the unfused kernels)
+static int gs_sub(int m) {
+  const int need = m + 2;                     // tile rows + partial / w' slack
+  if (m > 1024) return 0;
+  for (int sub = 32; sub >= 8; sub /= 2)
+    if ((int64_t)need * sub * 8 + (GS_THREADS / sub) * sub * 8 <= GS_SMEM) return sub;
+  return 0;
+}
+
+MCS_API int mcs_gs_fused_blocks(void) { return 2 * 148; }
+
+MCS_API int mcs_gs_fused(int m, int64_t n, int64_t ld, const double* V, double* w, const double* h1,
+                         double* ph2, double* pnrm, double* h2, double* sc, int before, int after,
+                         int gate, void* stream) {
+  const int sub = gs_sub(m);
+  if (sub == 0 || m <= 0) return -1000;
+  auto st = static_cast<cudaStream_t>(stream);
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(gs_fused_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, GS_SMEM);
+    attr = true;
+  }
+  const int nblk = mcs_gs_fused_blocks();
+  const size_t smem = ((size_t)m * sub + (GS_THREADS / sub) * sub + sub) * sizeof(double);
+  gs_fused_kernel<<<nblk, GS_THREADS, smem, st>>>(m, n, ld, sub, V, w, h1, ph2, pnrm);
+  int rc = launch_status();
+  if (rc) return rc;
+  gs_final_kernel<<<1, 256, 0, st>>>(m, nblk, ph2, pnrm, h2, sc, before, after, gate);
   return launch_status();
 }

@@ -285,6 +285,12 @@ def _op(op, v, out, host_callables=False):
     return _apply(op, v, out, host_callables)
 
 
+# MCS_GS_FUSED=1: the fused second-pass kernel (one basis read for w - V h1,
+# V^T w' and ||w'||; three basis reads per step instead of four).  Measured
+# slower at cfg2 (727 vs 365 ms for 246 steps, profiles/r02/gmres_gs_fused.txt):
+# each CTA's tile sweep serialises load -> products -> barriers, and the
+# plain multi-dot / GEMV kernels already run near the HBM rate.
+_GS_FUSED = __import__("os").environ.get("MCS_GS_FUSED", "0") == "1"
 # Gram-Schmidt accounting of `gmres` (diagnostics: tools/gmres_prof.py)
 _GS_STATS = {"steps": 0, "second_pass": 0}
 
@@ -341,6 +347,10 @@ def gmres(apply_A, b, apply_M=None, rtol=1e-6, maxit=500, project=None, x0=None)
                           device="cuda")
     # the per-step read-back (||w|| before / after each pass, gate, both h
     # columns): two D2H copies into one pinned buffer, no gather kernel
+    # fused second-pass products (one basis read for w - V h1, V^T w' and ||w'||)
+    nblk = _abi.call("mcs_gs_fused_blocks")
+    ph2 = torch.empty((maxit + 1) * nblk, dtype=torch.float64, device="cuda")
+    pnrm = torch.empty(nblk, dtype=torch.float64, device="cuda")
     hh = torch.empty(2 * (maxit + 1), dtype=torch.float64, device="cuda")
     h1, h2 = hh[:maxit + 1], hh[maxit + 1:]
     nsc = ws.TMP3 - ws.TMP + 1
@@ -361,15 +371,24 @@ def gmres(apply_A, b, apply_M=None, rtol=1e-6, maxit=500, project=None, x0=None)
         ws.dot(w, w, ws.TMP)
         _abi.call("mcs_mdot", m, n, n, _abi.ptr(V), _abi.ptr(w), _abi.ptr(partial),
                   _abi.ptr(h1), _abi.stream(None))
-        _abi.call("mcs_gemv_acc", m, n, n, _abi.ptr(V), _abi.ptr(h1), -1.0, 1.0,
-                  _abi.ptr(w), _abi.stream(None))
-        ws.dot(w, w, ws.TMP2)
         # the DGKS decision on the device: the second pass is launched always
         # and skipped by its kernels when the first one kept enough of ||w||
         gate = ws.sc.data_ptr() + 8 * ws.GS_GATE
-        _abi.call("mcs_gs_gate", _abi.ptr(ws.sc), ws.TMP, ws.TMP2, ws.GS_GATE, _abi.stream(None))
-        _abi.call("mcs_mdot_gated", m, n, n, _abi.ptr(V), _abi.ptr(w), _abi.ptr(partial),
-                  _abi.ptr(h2), gate, _abi.stream(None))
+        rc = -1000
+        if _GS_FUSED:   # w -= V h1, h2 = V^T w, ||w||^2 and the gate from one basis read
+            rc = _abi.lib().mcs_gs_fused(
+                m, n, n, _abi.ptr(V), _abi.ptr(w), _abi.ptr(h1), _abi.ptr(ph2), _abi.ptr(pnrm),
+                _abi.ptr(h2), _abi.ptr(ws.sc), ws.TMP, ws.TMP2, ws.GS_GATE, _abi.stream(None))
+            if rc not in (0, -1000):
+                raise _abi.McsError(f"mcs_gs_fused failed with CUDA error {-rc}")
+        if rc != 0:     # the default; also m beyond the fused kernel's shared-memory tile
+            _abi.call("mcs_gemv_acc", m, n, n, _abi.ptr(V), _abi.ptr(h1), -1.0, 1.0,
+                      _abi.ptr(w), _abi.stream(None))
+            ws.dot(w, w, ws.TMP2)
+            _abi.call("mcs_gs_gate", _abi.ptr(ws.sc), ws.TMP, ws.TMP2, ws.GS_GATE,
+                      _abi.stream(None))
+            _abi.call("mcs_mdot_gated", m, n, n, _abi.ptr(V), _abi.ptr(w), _abi.ptr(partial),
+                      _abi.ptr(h2), gate, _abi.stream(None))
         _abi.call("mcs_gemv_acc_gated", m, n, n, _abi.ptr(V), _abi.ptr(h2), -1.0, 1.0,
                   _abi.ptr(w), gate, _abi.stream(None))
         ws.dot(w, w, ws.TMP3)
