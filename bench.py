@@ -146,8 +146,11 @@ def ncu_traffic(prefix):
     with `prefix`, from the newest committed `ncu --set full` summary
     (profiles/ncu_kernels_*.json) that has it."""
     import glob
-    for path in sorted(glob.glob(os.path.join(ROOT, "profiles", "ncu_kernels_*.json")),
-                       key=os.path.getmtime, reverse=True):
+    paths = glob.glob(os.path.join(ROOT, "profiles", "ncu_kernels_*.json")) + \
+        glob.glob(os.path.join(ROOT, "profiles", "r*", "ncu_kernels_*.json"))
+    # newest round first (the round directory / file suffix), then mtime
+    for path in sorted(paths, key=lambda p_: (os.path.basename(os.path.dirname(p_)), p_),
+                       reverse=True):
         try:
             with open(path) as fh:
                 d = json.load(fh)

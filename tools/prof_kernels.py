@@ -38,3 +38,10 @@ if what in ("all", "cfg"):
     x, rep = cg(SOperator(sys_), condensed_rhs(fes, sys_)[0], M, rtol=1e-8, maxit=3)
     torch.cuda.synchronize()
     print("iters", rep.iterations)
+if what in ("all", "ds"):
+    # cfg3 (k = 6): generation-fused condensation + the warp-per-element double Schur
+    prob = baseline_config(3, int(os.environ.get("PROF_N3", "128")))
+    fes = FeSystem(prob.mesh, prob.regions, prob.k)
+    sys_ = double_schur(condense_sigma_omega(fes, prob.nu, prob.body_force))
+    torch.cuda.synchronize()
+    print("cfg3 elements", prob.mesh.num_triangles)
