@@ -51,6 +51,65 @@ namespace fz {
 
 constexpr int W_MSIG = 0, W_ADIV = 27, NWS = 36;   // weight slots (refblocks.py), 30.. = 0
 
+// Row classification of Bsig and the per-tile formats of the lane-ordered
+// shared-memory tables (a separate struct: Geo uses these in its own
+// constant expressions).
+template <int K>
+struct Rows {
+  using Z = Sizes<K>;
+  static constexpr int NEM = Z::n_em, nu = Z::nu, nloc = Z::nloc;
+  // Bsig row i: 0 facet (bus volume + edge term of edge i/(k+1)), 1 interior
+  // bubble (volume only), 2 Vhat (bhs of edge (i-nu)/k), 3 padding
+  __host__ __device__ static constexpr int row_type(int i) {
+    return i < NEM ? 0 : (i < nu ? 1 : (i < nloc ? 2 : 3));
+  }
+  // weight slot of row i's three edge weights (refblocks.py W_BUSE / W_BHS)
+  __host__ __device__ static constexpr int row_woff(int i) {
+    return i < NEM ? 9 + 3 * (i / (K + 1)) : ((i >= nu && i < nloc) ? 18 + 3 * ((i - nu) / K) : 30);
+  }
+  // Row types present in the 8-row tile I (bit 0 facet, 1 interior, 2 Vhat).
+  __host__ __device__ static constexpr int tile_types(int I) {
+    int m = 0;
+    for (int rr = 0; rr < 8; ++rr) {
+      const int ty = row_type(8 * I + rr);
+      if (ty < 3) m |= 1 << ty;
+    }
+    return m;
+  }
+  // Per-CTA shared-memory tables of Bsig, stored IN THE ORDER THE LANES READ
+  // THEM (lane (g, t) of tile I owns row 8I + g): every lane generates exactly
+  // the entries its Y registers need, so Bsig is never staged.
+  //
+  // Low blocks (dof 3m + a = Dubiner function m x generator a): the edge
+  // terms act on generator a only, T_a[i][3m + a'] = delta_aa' Ehat[i][m]
+  // (engine.fused_tables checks it), hence per (row, m = 4 kc + t) the four
+  // values (base_0, base_1, base_2, Ehat) and
+  //   y_s = sum_a base_a F_m[a][s] + Ehat * G_s,  G_s = sum_a w_a F_m[a][s]
+  // (G per element and edge group, precomputed once per element).
+  // Format of tile I: 4 = (b0, b1 | b2, Ehat) as two conflict-free 16-byte
+  // planes, 3 = interior rows only (b0, b1, b2), 1 = Vhat rows only (Ehat).
+  __host__ __device__ static constexpr int fmt_low(int I) {
+    const int m = tile_types(I);
+    return m == 2 ? 3 : (m == 4 ? 1 : 4);
+  }
+  // Bubble columns (A operand of the bubble DMMA, column nl + 4 ks + t): 4 =
+  // (base, T0 | T1, T2), 1 = interior rows only (base), 3 = Vhat only (T0, T1, T2).
+  __host__ __device__ static constexpr int fmt_bub(int I) {
+    const int m = tile_types(I);
+    return m == 2 ? 1 : (m == 4 ? 3 : 4);
+  }
+  __host__ __device__ static constexpr int lo_off(int I, int nlow) {
+    int o = 0;
+    for (int q = 0; q < I; ++q) o += 32 * nlow * fmt_low(q);
+    return o;
+  }
+  __host__ __device__ static constexpr int bu_off(int I, int nks) {
+    int o = 0;
+    for (int q = 0; q < I; ++q) o += 32 * nks * fmt_bub(q);
+    return o;
+  }
+};
+
 template <int K>
 struct Geo {
   using Z = Sizes<K>;
@@ -78,7 +137,7 @@ struct Geo {
   static constexpr int o_S = o_F + even(6 * ml);      // packed S_T
   static constexpr int o_U = o_S + st_len;            // phase-dependent union
   static constexpr int UA = 2 * nb * nb + even(nb);   // Ls | Li | 1/diag
-  static constexpr int UB = 8 * ns;                   // one 8-row tile of B
+  static constexpr int UB = even(6 * ml * 2);         // G[edge group][m][s] (phase B)
   static constexpr int NIT = (NI + 7) / 8;            // 8-row tiles of L^-1 / X
   static constexpr int LST = 20;                      // L^-1 row stride (== 4 mod 16)
   static constexpr int NIR = 8 * NIT > 4 * NIK ? 8 * NIT : 4 * NIK;   // padded rows
@@ -91,26 +150,20 @@ struct Geo {
   static_assert(nb <= 32 && ml <= 32 && NI <= 32 && NC <= 32, "lane-per-row factorisations");
   static_assert(8 * NCB <= WST, "W columns");
   static_assert(8 * NIT <= LST && 4 * NIK <= LST, "L^-1 columns");
-  // Bsig row i: 0 facet (bus volume + edge term of edge i/(k+1)), 1 interior
-  // bubble (volume only), 2 Vhat (bhs of edge (i-nu)/k), 3 padding
-  __host__ __device__ static constexpr int row_type(int i) {
-    return i < NEM ? 0 : (i < nu ? 1 : (i < nloc ? 2 : 3));
-  }
-  // weight slot of row i's three edge weights (refblocks.py W_BUSE / W_BHS)
-  __host__ __device__ static constexpr int row_woff(int i) {
-    return i < NEM ? 9 + 3 * (i / (K + 1)) : ((i >= nu && i < nloc) ? 18 + 3 * ((i - nu) / K) : 30);
-  }
-  // compact shared-memory copy of the Bsig tables: facet rows (base, T0, T1,
-  // T2) per entry, interior rows base only, Vhat rows (T0, T1, T2)
-  __host__ __device__ static constexpr int row_off(int i) {
-    return i < NEM ? 4 * ns * i
-                   : (i < nu ? 4 * ns * NEM + ns * (i - NEM)
-                             : 4 * ns * NEM + ns * (nu - NEM) + 3 * ns * (i - nu));
-  }
-  static constexpr int TAB_B = even(4 * ns * NEM + ns * (nu - NEM) + 3 * ns * (nloc - nu));
-  static constexpr int TAB_MB = TAB_B;                       // MbRef [6][nb][nb]
+  static_assert(6 * ml * 2 <= nb * nb, "G fits over Ls");
+  using RW = Rows<K>;
+  __host__ __device__ static constexpr int row_type(int i) { return RW::row_type(i); }
+  __host__ __device__ static constexpr int row_woff(int i) { return RW::row_woff(i); }
+  __host__ __device__ static constexpr int fmt_low(int I) { return RW::fmt_low(I); }
+  __host__ __device__ static constexpr int fmt_bub(int I) { return RW::fmt_bub(I); }
+  __host__ __device__ static constexpr int lo_off(int I) { return RW::lo_off(I, NLOW); }
+  __host__ __device__ static constexpr int bu_off(int I) { return RW::bu_off(I, NKS); }
+  static constexpr int TAB_LO = 0;
+  static constexpr int TAB_BU = TAB_LO + RW::lo_off(NRB, NLOW);
+  static constexpr int TAB_MB = TAB_BU + RW::bu_off(NRB, NKS);        // MbRef [6][nb][nb]
   static constexpr int TAB_A = TAB_MB + even(6 * nb * nb);   // ARef [6][ml][9]
   static constexpr int TAB_SMEM = TAB_A + even(6 * 9 * ml);
+  static constexpr int NG = 6 * ml * 2;                      // G[edge group][m][s], in U during phase B
   // bubble column of DMMA n-tile bt, output column n (-1: none)
   __host__ __device__ static constexpr int jmap(int bt, int n) {
     if (MIX && bt == 0) return (n >= 2 * r && n - 2 * r < nb) ? n - 2 * r : -1;
@@ -191,21 +244,57 @@ __global__ void __launch_bounds__(32 * WPB, MINB)
   double* sw = smem + G::TAB_SMEM + warp * G::PER_WARP;
   for (int q = threadIdx.x; q < 6 * nb * nb; q += 32 * WPB) stab[G::TAB_MB + q] = tab[T::o_Mb + q];
   for (int q = threadIdx.x; q < 6 * 9 * ml; q += 32 * WPB) stab[G::TAB_A + q] = tab[T::o_A + q];
-  for (int q = threadIdx.x; q < nloc * ns; q += 32 * WPB) {
-    const int i = q / ns, c = q % ns, ty = G::row_type(i);
-    const double* src = tab + T::o_G4 + 4 * q;
-    double* dst = stab + G::row_off(i);
-    if (ty == 0) {
-      dst[4 * c] = src[0];
-      dst[4 * c + 1] = src[1];
-      dst[4 * c + 2] = src[2];
-      dst[4 * c + 3] = src[3];
-    } else if (ty == 1) {
-      dst[c] = src[0];
+  // lane-ordered Bsig tables (layout: fz::Geo)
+  for (int q = threadIdx.x; q < 32 * G::NLOW * NRB; q += 32 * WPB) {
+    const int ln = q & 31, kc = (q >> 5) % G::NLOW, I = (q >> 5) / G::NLOW;
+    const int i = 8 * I + (ln >> 2), m = 4 * kc + (ln & 3);
+    double b0 = 0.0, b1 = 0.0, b2 = 0.0, eh = 0.0;
+    if (i < nloc && m < ml) {
+      const double* src = tab + T::o_G4 + 4 * (i * ns + 3 * m);
+      b0 = src[0];
+      b1 = src[4];
+      b2 = src[8];
+      eh = src[1];   // T_0 of column 3m (= T_1 of 3m + 1 = T_2 of 3m + 2)
+    }
+    double* dst = stab + G::TAB_LO + G::lo_off(I);
+    const int fmt = G::fmt_low(I);
+    if (fmt == 4) {
+      dst[(2 * kc) * 64 + 2 * ln] = b0;
+      dst[(2 * kc) * 64 + 2 * ln + 1] = b1;
+      dst[(2 * kc + 1) * 64 + 2 * ln] = b2;
+      dst[(2 * kc + 1) * 64 + 2 * ln + 1] = eh;
+    } else if (fmt == 3) {
+      dst[(3 * kc) * 32 + ln] = b0;
+      dst[(3 * kc + 1) * 32 + ln] = b1;
+      dst[(3 * kc + 2) * 32 + ln] = b2;
     } else {
-      dst[3 * c] = src[1];
-      dst[3 * c + 1] = src[2];
-      dst[3 * c + 2] = src[3];
+      dst[kc * 32 + ln] = eh;
+    }
+  }
+  for (int q = threadIdx.x; q < 32 * G::NKS * NRB; q += 32 * WPB) {
+    const int ln = q & 31, ks = (q >> 5) % G::NKS, I = (q >> 5) / G::NKS;
+    const int i = 8 * I + (ln >> 2), c = 4 * ks + (ln & 3);
+    double v0 = 0.0, v1 = 0.0, v2 = 0.0, v3 = 0.0;
+    if (i < nloc && c < nb) {
+      const double* src = tab + T::o_G4 + 4 * (i * ns + nl + c);
+      v0 = src[0];
+      v1 = src[1];
+      v2 = src[2];
+      v3 = src[3];
+    }
+    double* dst = stab + G::TAB_BU + G::bu_off(I);
+    const int fmt = G::fmt_bub(I);
+    if (fmt == 4) {
+      dst[(2 * ks) * 64 + 2 * ln] = v0;
+      dst[(2 * ks) * 64 + 2 * ln + 1] = v1;
+      dst[(2 * ks + 1) * 64 + 2 * ln] = v2;
+      dst[(2 * ks + 1) * 64 + 2 * ln + 1] = v3;
+    } else if (fmt == 3) {
+      dst[(3 * ks) * 32 + ln] = v1;
+      dst[(3 * ks + 1) * 32 + ln] = v2;
+      dst[(3 * ks + 2) * 32 + ln] = v3;
+    } else {
+      dst[ks * 32 + ln] = v0;
     }
   }
   __syncthreads();
@@ -326,72 +415,100 @@ __global__ void __launch_bounds__(32 * WPB, MINB)
       }
     }
     __syncwarp();
+    // G[grp][m][s] = sum_a w[9 + 3 grp + a] F_m[a][s]: the edge weights of
+    // the three bus edges (grp 0..2) and the three bhs edges (3..5) folded
+    // into F (over Ls, which is dead once L_b^-1 is formed)
+    double* Gs = U;
+    for (int q = lane; q < G::NG; q += 32) {
+      const int sI = q & 1, m = (q >> 1) % ml, grp = (q >> 1) / ml;
+      const double* w = wts + 9 + 3 * grp;
+      const double* Fm = Fs + 6 * m + sI;
+      Gs[q] = fma(w[0], Fm[0], fma(w[1], Fm[2], w[2] * Fm[4]));
+    }
+    __syncwarp();
 
     FZ_T(0);
-    // ---------------- B: Y in registers, one 8-row tile of B at a time
+    // ---------------- B: Y in registers, every lane generating exactly the
+    // Bsig entries its registers need from the lane-ordered tables
     double2 Yf[NRB][NKC];
-    double* Bt = U;
 #pragma unroll
-    for (int I = 0; I < NRB; ++I) {
-      // rows of one type per instruction (compile-time after unrolling),
-      // lanes along the row: coalesced table reads, warp-uniform weights
+    for (int kc = 0; kc < G::NLOW; ++kc) {
+      const int m = 4 * kc + t;
+      const int mm = m < ml ? m : ml - 1;       // padding lanes: zero table entries
+      const double2 F0 = *reinterpret_cast<const double2*>(Fs + 6 * mm);
+      const double2 F1 = *reinterpret_cast<const double2*>(Fs + 6 * mm + 2);
+      const double2 F2 = *reinterpret_cast<const double2*>(Fs + 6 * mm + 4);
 #pragma unroll
-      for (int rr = 0; rr < 8; ++rr) {
-        const int i = 8 * I + rr;
-        const int ty = G::row_type(i);
-        const int wo = G::row_woff(i);
-        const double w0 = wts[wo], w1 = wts[wo + 1], w2 = wts[wo + 2];
-        const double* p = stab + G::row_off(i);
-#pragma unroll
-        for (int c0 = 0; c0 < ns; c0 += 32) {
-          const int c = c0 + lane;
-          if (c0 + 32 <= ns || c < ns) {
-            double v = 0.0;
-            if (ty == 0) {            // facet row: base + edge term
-              const double2 v01 = *reinterpret_cast<const double2*>(p + 4 * c);
-              const double2 v23 = *reinterpret_cast<const double2*>(p + 4 * c + 2);
-              v = fma(w0, v01.y, v01.x);
-              v = fma(w1, v23.x, v);
-              v = fma(w2, v23.y, v);
-            } else if (ty == 1) {     // interior bubble row: J-invariant volume part
-              v = p[c];
-            } else if (ty == 2) {     // Vhat row: bhs of its edge
-              v = fma(w2, p[3 * c + 2], fma(w1, p[3 * c + 1], w0 * p[3 * c]));
-            }
-            Bt[rr * ns + c] = v;
+      for (int I = 0; I < NRB; ++I) {
+        const double* tl = stab + G::TAB_LO + G::lo_off(I);
+        const int fmt = G::fmt_low(I);
+        double y0 = 0.0, y1 = 0.0, eh4 = 0.0;
+        if (fmt != 1) {
+          double b0, b1, b2;
+          if (fmt == 4) {
+            const double2 p = *reinterpret_cast<const double2*>(tl + (2 * kc) * 64 + 2 * lane);
+            const double2 q = *reinterpret_cast<const double2*>(tl + (2 * kc + 1) * 64 + 2 * lane);
+            b0 = p.x;
+            b1 = p.y;
+            b2 = q.x;
+            eh4 = q.y;
+          } else {
+            b0 = tl[(3 * kc) * 32 + lane];
+            b1 = tl[(3 * kc + 1) * 32 + lane];
+            b2 = tl[(3 * kc + 2) * 32 + lane];
           }
+          y0 = fma(b0, F0.x, fma(b1, F1.x, b2 * F2.x));
+          y1 = fma(b0, F0.y, fma(b1, F1.y, b2 * F2.y));
         }
-      }
-      __syncwarp();
-      const double* brow = Bt + g * ns;
-#pragma unroll
-      for (int kc = 0; kc < G::NLOW; ++kc) {
-        const int m = 4 * kc + t;
-        const int mm = m < ml ? m : ml - 1;
-        const double b0 = brow[3 * mm], b1 = brow[3 * mm + 1], b2 = brow[3 * mm + 2];
-        const double* Fm = Fs + 6 * mm;
-        double y0 = fma(b0, Fm[0], fma(b1, Fm[2], b2 * Fm[4]));
-        double y1 = fma(b0, Fm[1], fma(b1, Fm[3], b2 * Fm[5]));
-        if (m >= ml) y0 = y1 = 0.0;
+        if (fmt != 3) {
+          const double eh = fmt == 4 ? eh4 : tl[kc * 32 + lane];
+          const int wo = G::row_woff(8 * I + g);
+          const int grp = wo < 30 ? (wo - 9) / 3 : 0;      // interior / padding rows: Ehat = 0
+          const double2 Gm = *reinterpret_cast<const double2*>(Gs + 2 * (grp * ml + mm));
+          y0 = fma(eh, Gm.x, y0);
+          y1 = fma(eh, Gm.y, y1);
+        }
         Yf[I][kc] = make_double2(y0, y1);
       }
+    }
+#pragma unroll
+    for (int I = 0; I < NRB; ++I) {
 #pragma unroll
       for (int kc = G::NLOW; kc < NKC; ++kc) Yf[I][kc] = make_double2(0.0, 0.0);
+      const double* tb = stab + G::TAB_BU + G::bu_off(I);
+      const int fmt = G::fmt_bub(I);
+      double w0 = 0.0, w1 = 0.0, w2 = 0.0;
+      if (fmt != 1) {
+        const int wo = G::row_woff(8 * I + g);
+        w0 = wts[wo];
+        w1 = wts[wo + 1];
+        w2 = wts[wo + 2];
+      }
+      double a[G::NKS];
+#pragma unroll
+      for (int ks = 0; ks < G::NKS; ++ks) {
+        if (fmt == 4) {
+          const double2 p = *reinterpret_cast<const double2*>(tb + (2 * ks) * 64 + 2 * lane);
+          const double2 q = *reinterpret_cast<const double2*>(tb + (2 * ks + 1) * 64 + 2 * lane);
+          a[ks] = fma(w2, q.y, fma(w1, q.x, fma(w0, p.y, p.x)));
+        } else if (fmt == 3) {
+          a[ks] = fma(w2, tb[(3 * ks + 2) * 32 + lane],
+                      fma(w1, tb[(3 * ks + 1) * 32 + lane], w0 * tb[(3 * ks) * 32 + lane]));
+        } else {
+          a[ks] = tb[ks * 32 + lane];
+        }
+      }
 #pragma unroll
       for (int bt = 0; bt < G::NBT; ++bt) {
         double c0 = 0.0, c1 = 0.0;
 #pragma unroll
-        for (int ks = 0; ks < G::NKS; ++ks) {
-          const int q = 4 * ks + t;
-          const double a = q < nb ? brow[nl + q] : 0.0;
-          dmma884(c0, c1, a, LiR[bt][ks]);
-        }
+        for (int ks = 0; ks < G::NKS; ++ks) dmma884(c0, c1, a[ks], LiR[bt][ks]);
         const int kc = G::NLF + bt;
         Yf[I][kc].x += c0;
         Yf[I][kc].y += c1;
       }
-      __syncwarp();
     }
+    __syncwarp();
 
     FZ_T(1);
     // ---------------- C: S_T = adiv + Y Y^T (DMMA), packed into shared memory
@@ -559,6 +676,10 @@ __global__ void __launch_bounds__(32 * WPB, MINB)
   }
 }
 
+#ifndef MCS_FZ_WPB4
+#define MCS_FZ_WPB4 12   // warps per CTA at k = 4 (tools/fused_prof.py sweeps it)
+#endif
+
 template <int K, int WPB, int MINB>
 static int launch_condense_fused(int64_t nt, const double* W, int nwgt, const double* tab,
                                  double* ST, double* ext, double* Sd, int* info,
@@ -604,7 +725,7 @@ MCS_API int mcs_condense_fused(int k, int64_t nt, const double* W, int nwgt, con
     // one CTA per SM: the compact tables once per CTA, one element per warp
     case 2: return launch_condense_fused<2, 16, 1>(nt, W, nwgt, tables, S_packed, ext, Sd_packed, info, st);
     case 3: return launch_condense_fused<3, 12, 1>(nt, W, nwgt, tables, S_packed, ext, Sd_packed, info, st);
-    case 4: return launch_condense_fused<4, 12, 1>(nt, W, nwgt, tables, S_packed, ext, Sd_packed, info, st);
+    case 4: return launch_condense_fused<4, MCS_FZ_WPB4, 1>(nt, W, nwgt, tables, S_packed, ext, Sd_packed, info, st);
   }
   return -1000;
 }

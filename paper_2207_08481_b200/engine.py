@@ -158,6 +158,15 @@ def fused_tables(refs: BlockRefs):
         woff[rows] = W_BUSE + 3 * e
         woff[nu + e * k:nu + (e + 1) * k] = W_BHS + 3 * e
     assert n_em == 3 * (k + 1) and nloc == nu + 3 * k
+    # low dof 3m + a' is Dubiner function m times generator a', so the edge
+    # terms act on generator a only: T_a[i][3m + a'] = delta_aa' Ehat[i][m].
+    # The fused kernel stores one Ehat per (row, m) and relies on it.
+    Tl = T[:, :, :nl].reshape(3, NR, ml, 3)
+    for a in range(3):
+        for b in range(3):
+            dev = np.abs(Tl[a, :, :, b] - (Tl[0, :, :, 0] if a == b else 0.0)).max()
+            if dev > 1e-13 * max(scale, 1.0):
+                raise ValueError("edge tables do not have the generator-diagonal structure")
     tab[L["G4"]:L["G4"] + 4 * NR * ns] = np.stack([base, T[0], T[1], T[2]], -1).ravel()
     tab[L["adiv"]:L["adiv"] + nu * nu] = refs.adiv.ravel()
     tab[L["Mb"]:L["Mb"] + 6 * nb * nb] = refs.msig[:, nl:, nl:].ravel()

@@ -16,11 +16,12 @@ from paper_2207_08481_b200 import _abi, engine, refblocks  # noqa: E402
 from paper_2207_08481_b200.dofmap import FeSystem  # noqa: E402
 from paper_2207_08481_b200.problems import baseline_config  # noqa: E402
 
-so = os.path.join(ROOT, "tools", "_fused_prof.so")
+WPB = int(os.environ.get("WPB", "12"))
+so = os.path.join(ROOT, "tools", f"_fused_prof_{WPB}.so")
 csrc = os.path.join(ROOT, "paper_2207_08481_b200", "csrc")
 if not os.path.exists(so):
     subprocess.check_call(["nvcc", "-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-std=c++17",
-                           "-Xcompiler", "-fPIC", "-shared", "-DMCS_FUSED_PROF", "-I", csrc, "-I",
+                           "-Xcompiler", "-fPIC", "-shared", "-DMCS_FUSED_PROF", f"-DMCS_FZ_WPB4={WPB}", "-I", csrc, "-I",
                            os.path.join(ROOT, "include"), "--expt-relaxed-constexpr",
                            os.path.join(csrc, "condense_fused.cu"), "-o", so])
 lib = ctypes.CDLL(so)
@@ -39,6 +40,13 @@ args = (k, nt, W.data_ptr(), W.shape[1], tab.data_ptr(), ST.data_ptr(), ext.data
         Sd.data_ptr(), info.data_ptr(), torch.cuda.current_stream().cuda_stream)
 lib.mcs_condense_fused(*args)
 torch.cuda.synchronize()
+ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+ev0.record()
+for _ in range(10):
+    lib.mcs_condense_fused(*args)
+ev1.record()
+torch.cuda.synchronize()
+print(f"WPB {WPB}: {ev0.elapsed_time(ev1) / 10:.4f} ms per launch (with clock accounting)")
 sym = ctypes.c_ulonglong * 8
 buf = sym()
 cudart = ctypes.CDLL("libcudart.so") if False else None
@@ -46,7 +54,7 @@ cudart = ctypes.CDLL("libcudart.so") if False else None
 getter = getattr(lib, "fz_prof_read", None)
 getter.argtypes = [P]
 getter(ctypes.addressof(buf))
-v = np.array(buf[:4], dtype=float)
+v = np.array(buf[:4], dtype=float) / 11
 names = ["A factors", "B Bsig+Y", "C S_T (DMMA)", "D double Schur"]
 tot = v.sum()
 for nm, x in zip(names, v):
