@@ -13,6 +13,7 @@
 //   Sd_T        lower packed (even stride)
 #include <cstdlib>
 
+#include "ds_reg.cuh"
 #include "ds_warp.cuh"
 #include "elim_v5.cuh"
 
@@ -100,7 +101,7 @@ struct DswLayout {
   static constexpr int PER_WARP = even(o_rd + G::NI);
 };
 
-template <int K, int WPB>
+template <int K, int WPB, int YM>
 __global__ void __launch_bounds__(32 * WPB)
     double_schur_warp(const double* __restrict__ ST, double* __restrict__ ext,
                       double* __restrict__ Sd, int* __restrict__ info, int64_t nt) {
@@ -132,18 +133,72 @@ __global__ void __launch_bounds__(32 * WPB)
     dsw::stage_soc<K>(Sg, Wd, lane, 32);
     __syncwarp();
 #pragma unroll 1
-    for (int J = 0; J < G::NCB; ++J) dsw::w_block<K>(LI, Wd, J);
-    dsw::out_tiles<K>(Sg, LI, Wd, ext + e * L::len, Sd + e * L::sd_len, 0, 1);
+    for (int J = 0; J < G::NCB; ++J) dsw::w_block<K, YM>(LI, Wd, J);
+    dsw::out_tiles<K, decltype(Sg), YM>(Sg, LI, Wd, ext + e * L::len, Sd + e * L::sd_len, 0, 1);
     if (lane == 0 && info) info[e] = ok ? 0 : 1;
     __syncwarp();
   }
 }
 
+template <int K, int WPB, int YM>
+static int launch_dsw(const double* ST, double* ext, double* Sd, int* info,
+                      int64_t nt, cudaStream_t st) {
+  auto kern = double_schur_warp<K, WPB, YM>;
+  const size_t smem = (size_t)WPB * DswLayout<K>::PER_WARP * sizeof(double);
+  cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  int per_sm = 0;
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, 32 * WPB, smem) != cudaSuccess ||
+      per_sm < 1)
+    per_sm = 1;
+  const int64_t want = (nt + WPB - 1) / WPB, cap = (int64_t)per_sm * sm_count();
+  kern<<<(int)(want < cap ? want : cap), 32 * WPB, smem, st>>>(ST, ext, Sd, info, nt);
+  return launch_status();
+}
+
 template <int K, int WPB>
 static int launch_double_schur_warp(const double* ST, double* ext, double* Sd, int* info,
                                     int64_t nt, cudaStream_t st) {
-  auto kern = double_schur_warp<K, WPB>;
-  const size_t smem = (size_t)WPB * DswLayout<K>::PER_WARP * sizeof(double);
+  // MCS_DS_YIELD: throttle mask (1 after every W column block, 2 after every
+  // output tile, 4 after every 4th output tile); A/B measurements
+  static const int ym = getenv("MCS_DS_YIELD") ? atoi(getenv("MCS_DS_YIELD")) : 0;
+  switch (ym) {
+    case 1: return launch_dsw<K, WPB, 1>(ST, ext, Sd, info, nt, st);
+    case 2: return launch_dsw<K, WPB, 2>(ST, ext, Sd, info, nt, st);
+    case 3: return launch_dsw<K, WPB, 3>(ST, ext, Sd, info, nt, st);
+    case 4: return launch_dsw<K, WPB, 4>(ST, ext, Sd, info, nt, st);
+    case 5: return launch_dsw<K, WPB, 5>(ST, ext, Sd, info, nt, st);
+  }
+  return launch_dsw<K, WPB, 0>(ST, ext, Sd, info, nt, st);
+}
+
+// ---- register-resident warp-per-element kernel (ds_reg.cuh)
+template <int K, int WPB, int MINB>
+__global__ void __launch_bounds__(32 * WPB, MINB)
+    double_schur_reg(const double* __restrict__ ST, double* __restrict__ ext,
+                     double* __restrict__ Sd, int* __restrict__ info, int64_t nt) {
+  using G = dsr::Geo<K>;
+  using L = ExtLayout<K>;
+  extern __shared__ __align__(128) double smem[];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  double* T = smem + warp * G::PER_WARP;
+  const int64_t nw = (int64_t)gridDim.x * WPB;
+#pragma unroll 1
+  for (int64_t e = (int64_t)blockIdx.x * WPB + warp; e < nt; e += nw) {
+    if (e + nw < nt) {                     // the next element's S_T into L2
+      const char* nx = reinterpret_cast<const char*>(ST + (e + nw) * L::st_len);
+      for (int off = lane * 128; off < L::st_len * 8; off += 32 * 128)
+        asm volatile("prefetch.global.L2 [%0];" ::"l"(nx + off));
+    }
+    const bool ok = dsr::element<K>(ST + e * L::st_len, T, ext + e * L::len, Sd + e * L::sd_len);
+    if (lane == 0 && info) info[e] = ok ? 0 : 1;
+  }
+}
+
+template <int K, int WPB, int MINB>
+static int launch_double_schur_reg(const double* ST, double* ext, double* Sd, int* info,
+                                   int64_t nt, cudaStream_t st) {
+  auto kern = double_schur_reg<K, WPB, MINB>;
+  const size_t smem = (size_t)WPB * dsr::Geo<K>::PER_WARP * sizeof(double);
   cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   int per_sm = 0;
   if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, 32 * WPB, smem) != cudaSuccess ||
@@ -201,8 +256,23 @@ MCS_API int mcs_double_schur(int k, int64_t nt, const double* S_packed, double* 
                              int* info, void* stream) {
   if (nt <= 0) return 0;
   auto st = static_cast<cudaStream_t>(stream);
-  // default: the warp-per-element kernel; MCS_DS=5: the v5 CTA engine
-  static const int ds = getenv("MCS_DS") ? atoi(getenv("MCS_DS")) : 1;
+  // default: the register-resident warp-per-element kernel (ds_reg.cuh);
+  // MCS_DS=1: the shared-memory warp kernel (ds_warp.cuh), MCS_DS=5: the v5 CTA engine
+  static const int ds = getenv("MCS_DS") ? atoi(getenv("MCS_DS")) : 2;
+  if (ds == 2) {                            // register-resident kernel (ds_reg.cuh)
+    static const int occ = getenv("MCS_DSR_OCC") ? atoi(getenv("MCS_DSR_OCC")) : 0;
+    switch (k) {
+      case 2: return launch_double_schur_reg<2, 4, 1>(S_packed, ext, Sd_packed, info, nt, st);
+      case 3: return launch_double_schur_reg<3, 4, 1>(S_packed, ext, Sd_packed, info, nt, st);
+      case 4: return launch_double_schur_reg<4, 4, 1>(S_packed, ext, Sd_packed, info, nt, st);
+      case 5: return launch_double_schur_reg<5, 4, 1>(S_packed, ext, Sd_packed, info, nt, st);
+      case 6:
+        if (occ == 3) return launch_double_schur_reg<6, 4, 3>(S_packed, ext, Sd_packed, info, nt, st);
+        if (occ == 4) return launch_double_schur_reg<6, 4, 4>(S_packed, ext, Sd_packed, info, nt, st);
+        return launch_double_schur_reg<6, 4, 2>(S_packed, ext, Sd_packed, info, nt, st);
+    }
+    return -1000;
+  }
   if (ds != 5) {
     switch (k) {
       case 2: return launch_double_schur_warp<2, 4>(S_packed, ext, Sd_packed, info, nt, st);

@@ -1,0 +1,243 @@
+// Register-resident double Schur complement, one warp per element (SURVEY
+// §8a row A4; the reference's sequence condensation.py:207-226 on the
+// element-local S_T):
+//   S_oo = L L^T,  X = S_oo^-1 S_oc,  S_oo^-1,  Sd_T = S_cc - S_co X.
+//
+// Every matrix is cut into 8x8 tiles held in the DMMA "row layout" (lane
+// (g, t) owns entries [g][2t], [g][2t+1]), which is at once the m8n8k4
+// accumulator layout and a valid operand layout of C += X Y^T (two m8n8k4
+// steps over the k slots 2t and 2t+1).  With S_co (coupling x interior) and
+// an identity block as right-hand sides, ONE right-looking sweep over the
+// pivot tiles j of S_oo produces, in registers,
+//   W^T  = S_co L^-T        (bt[c][j],  NCB x NP tiles)
+//   L^-T = I    L^-T        (it[J][I],  I >= J)
+// and then
+//   Sd_T   = S_cc - W^T W          (X Y^T of bt rows)
+//   X      = L^-T W     = it bt^T  (row tile I, sum over I' >= I)
+//   S_oo^-1 = L^-T L^-1 = it it^T.
+// Per step j: the 8x8 diagonal tile is factorised with shuffles (chol8m,
+// which returns M_j^-1), the panel L_ij = A_ij M_j^-T and every trailing
+// update are DMMA pairs on register operands.  The trailing part of S_oo
+// lives in per-lane private shared-memory slots (lane l only ever touches
+// bytes [16 l, 16 l + 16) of a tile, so no warp synchronisation is needed);
+// nothing else leaves the registers: no W / L^-1 staging, no operand
+// reloads, ~770 DMMAs and ~3k instructions per element at k = 6 against
+// 864 DMMAs and 12.4k instructions for the shared-memory kernel of
+// ds_warp.cuh.
+#pragma once
+#include "common.cuh"
+
+namespace mcs {
+namespace dsr {
+
+template <int K>
+struct Geo {
+  using Z = Sizes<K>;
+  static constexpr int NI = Z::n_int, NC = Z::ncpl, NEM = Z::n_em;
+  static constexpr int NP = (NI + 7) / 8;                  // pivot tiles of S_oo
+  static constexpr int NCB = (NC + 7) / 8;                 // row tiles of S_co / Sd
+  static constexpr int NT = NP * (NP + 1) / 2;             // lower tiles of S_oo
+  static constexpr int PER_WARP = NT * 64;                 // doubles of shared memory per warp
+  __host__ __device__ static constexpr int q(int i, int j) { return i * (i + 1) / 2 + j; }
+};
+
+__device__ __forceinline__ void mma_xyt(double2& c, double2 x, double2 y) {
+  dmma884(c.x, c.y, x.x, y.x);
+  dmma884(c.x, c.y, x.y, y.y);
+}
+__device__ __forceinline__ double2 neg2(double2 v) { return make_double2(-v.x, -v.y); }
+
+// Cholesky M M^T = Y of one SPD 8x8 tile in the row layout (lower triangle
+// significant) and M^-1, also in the row layout, by forward elimination of
+// the identity alongside.  The elimination chain needs only 1/d per pivot;
+// the scaling d^-1/2 feeds the M^-1 recurrence off the critical path.
+// bad: first non-positive pivot (1-based, offset by base), 0 if none yet.
+__device__ __forceinline__ double2 chol8m(double y0, double y1, int& bad, int base) {
+  const int lane = threadIdx.x & 31, g = lane >> 2, t = lane & 3;
+  double x0 = (g == 2 * t) ? 1.0 : 0.0, x1 = (g == 2 * t + 1) ? 1.0 : 0.0;
+#pragma unroll
+  for (int p = 0; p < 8; ++p) {
+    const int sp = p >> 1;
+    const double yp = (p & 1) ? y1 : y0;                   // Y[g][p] in lanes t == sp
+    const double d = __shfl_sync(0xffffffffu, yp, 4 * p + sp);
+    const double yg = __shfl_sync(0xffffffffu, yp, 4 * g + sp);
+    const double yc0 = __shfl_sync(0xffffffffu, yp, 8 * t + sp);
+    const double yc1 = __shfl_sync(0xffffffffu, yp, 8 * t + 4 + sp);
+    if (!(d > 0.0) && bad == 0) bad = base + p + 1;
+    const double w = yg * rcp64(d);
+    y0 = fma(-w, yc0, y0);
+    y1 = fma(-w, yc1, y1);
+    const double sc = rsqrt_nr(d);
+    const double mg = yg * sc;                             // M[g][p]
+    const double xp0 = __shfl_sync(0xffffffffu, x0, 4 * p + t) * sc;
+    const double xp1 = __shfl_sync(0xffffffffu, x1, 4 * p + t) * sc;
+    if (g == p) {
+      x0 = xp0;
+      x1 = xp1;
+    } else if (g > p) {
+      x0 = fma(-mg, xp0, x0);
+      x1 = fma(-mg, xp1, x1);
+    }
+  }
+  return make_double2(x0, x1);
+}
+
+// One element.  S: packed lower S_T; T: this warp's NT private tile slots.
+// Returns false if S_oo is not positive definite.
+template <int K>
+__device__ __forceinline__ bool element(const double* __restrict__ S, double* __restrict__ T,
+                                        double* __restrict__ xo, double* __restrict__ so) {
+  using G = Geo<K>;
+  using L = ExtLayout<K>;
+  constexpr int NI = G::NI, NC = G::NC, NEM = G::NEM, NP = G::NP, NCB = G::NCB;
+  const int lane = threadIdx.x & 31, g = lane >> 2, t = lane & 3;
+  double* Tl = T + 2 * lane;
+  auto sym = [&](int a, int b) { return __ldg(S + (a >= b ? pk(a, b) : pk(b, a))); };
+
+  // ---- loads: S_co tiles into registers, S_oo lower tiles into the slots
+  double2 bt[NCB][NP];
+#pragma unroll
+  for (int c = 0; c < NCB; ++c) {
+    const int row = 8 * c + g, a = cpl_local<K>(row);
+#pragma unroll
+    for (int i = 0; i < NP; ++i) {
+      const int col = 8 * i + 2 * t;
+      double2 v = make_double2(0.0, 0.0);
+      if (row < NC) {
+        if (col < NI) v.x = sym(a, NEM + col);
+        if (col + 1 < NI) v.y = sym(a, NEM + col + 1);
+      }
+      bt[c][i] = v;
+    }
+  }
+#pragma unroll
+  for (int i = 0; i < NP; ++i)
+#pragma unroll
+    for (int j = 0; j <= i; ++j) {
+      const int r = 8 * i + g, c0 = 8 * j + 2 * t;
+      double2 v;
+      v.x = (r < NI && c0 < NI) ? sym(NEM + r, NEM + c0) : (r == c0 ? 1.0 : 0.0);
+      v.y = (r < NI && c0 + 1 < NI) ? sym(NEM + r, NEM + c0 + 1) : (r == c0 + 1 ? 1.0 : 0.0);
+      *reinterpret_cast<double2*>(Tl + G::q(i, j) * 64) = v;
+    }
+
+  double2 it[NP][NP];
+#pragma unroll
+  for (int a = 0; a < NP; ++a)
+#pragma unroll
+    for (int b = 0; b < NP; ++b) it[a][b] = make_double2(0.0, 0.0);
+  const double2 eye = make_double2(g == 2 * t ? 1.0 : 0.0, g == 2 * t + 1 ? 1.0 : 0.0);
+  int bad = 0;
+
+  // ---- the sweep over the pivot tiles
+#pragma unroll
+  for (int j = 0; j < NP; ++j) {
+    const double2 dj = *reinterpret_cast<const double2*>(Tl + G::q(j, j) * 64);
+    const double2 mi = chol8m(dj.x, dj.y, bad, 8 * j);     // M_j^-1
+    // panel L_ij = A_ij M_j^-T (kept negated for the updates)
+    double2 l[NP], ln[NP];
+#pragma unroll
+    for (int i = j + 1; i < NP; ++i) {
+      double2 o = make_double2(0.0, 0.0);
+      mma_xyt(o, *reinterpret_cast<const double2*>(Tl + G::q(i, j) * 64), mi);
+      l[i] = o;
+      ln[i] = neg2(o);
+    }
+    // the next diagonal tile first: its factorisation heads the critical path
+    if (j + 1 < NP) {
+      double2 c = *reinterpret_cast<const double2*>(Tl + G::q(j + 1, j + 1) * 64);
+      mma_xyt(c, ln[j + 1], l[j + 1]);
+      *reinterpret_cast<double2*>(Tl + G::q(j + 1, j + 1) * 64) = c;
+    }
+    // right-hand sides: W^T_cj = B_cj M_j^-T, (L^-T)_Jj likewise (J <= j)
+#pragma unroll
+    for (int c = 0; c < NCB; ++c) {
+      double2 o = make_double2(0.0, 0.0);
+      mma_xyt(o, bt[c][j], mi);
+      bt[c][j] = o;
+    }
+#pragma unroll
+    for (int J = 0; J <= j; ++J) {
+      double2 o = make_double2(0.0, 0.0);
+      mma_xyt(o, J == j ? eye : it[J][j], mi);
+      it[J][j] = o;
+    }
+    // trailing updates with column j
+#pragma unroll
+    for (int i = j + 1; i < NP; ++i) {
+#pragma unroll
+      for (int k = j + 1; k <= i; ++k) {
+        if (i == j + 1 && k == j + 1) continue;            // done above
+        double2 c = *reinterpret_cast<const double2*>(Tl + G::q(i, k) * 64);
+        mma_xyt(c, ln[i], l[k]);
+        *reinterpret_cast<double2*>(Tl + G::q(i, k) * 64) = c;
+      }
+#pragma unroll
+      for (int c = 0; c < NCB; ++c) mma_xyt(bt[c][i], bt[c][j], ln[i]);
+#pragma unroll
+      for (int J = 0; J <= j; ++J) mma_xyt(it[J][i], it[J][j], ln[i]);
+    }
+  }
+
+  // ---- Sd_T = S_cc - W^T W (lower tiles), S_cc loaded ahead of each chain
+#pragma unroll
+  for (int c = 0; c < NCB; ++c) {
+    const int row = 8 * c + g, a = cpl_local<K>(row);
+#pragma unroll
+    for (int d = 0; d <= c; ++d) {
+      const int col = 8 * d + 2 * t;
+      double s0 = 0.0, s1 = 0.0;
+      if (row < NC) {
+        if (col <= row) s0 = sym(a, cpl_local<K>(col));
+        if (col + 1 <= row) s1 = sym(a, cpl_local<K>(col + 1));
+      }
+      double2 o = make_double2(0.0, 0.0);
+#pragma unroll
+      for (int j = 0; j < NP; ++j) mma_xyt(o, bt[c][j], bt[d][j]);
+      if (row < NC) {
+        if (col <= row) so[pk(row, col)] = s0 - o.x;
+        if (col + 1 <= row) so[pk(row, col + 1)] = s1 - o.y;
+      }
+    }
+  }
+  // ---- X = L^-T W (row tile I: sum over I' >= I), row-major n_int x ncpl
+#pragma unroll
+  for (int I = 0; I < NP; ++I) {
+    const int row = 8 * I + g;
+#pragma unroll
+    for (int c = 0; c < NCB; ++c) {
+      double2 o = make_double2(0.0, 0.0);
+#pragma unroll
+      for (int Ip = I; Ip < NP; ++Ip) mma_xyt(o, it[I][Ip], bt[c][Ip]);
+      const int col = 8 * c + 2 * t;
+      if (row < NI) {
+        if constexpr (NC % 2 == 0) {
+          if (col < NC) *reinterpret_cast<double2*>(xo + row * NC + col) = o;
+        } else {
+          if (col < NC) xo[row * NC + col] = o.x;
+          if (col + 1 < NC) xo[row * NC + col + 1] = o.y;
+        }
+      }
+    }
+  }
+  // ---- S_oo^-1 = L^-T L^-1 (lower packed)
+#pragma unroll
+  for (int I = 0; I < NP; ++I) {
+    const int row = 8 * I + g;
+#pragma unroll
+    for (int Iq = 0; Iq <= I; ++Iq) {
+      double2 o = make_double2(0.0, 0.0);
+#pragma unroll
+      for (int Ip = I; Ip < NP; ++Ip) mma_xyt(o, it[I][Ip], it[Iq][Ip]);
+      const int col = 8 * Iq + 2 * t;
+      if (row < NI) {
+        if (col <= row) xo[L::x_len + pk(row, col)] = o.x;
+        if (col + 1 <= row) xo[L::x_len + pk(row, col + 1)] = o.y;
+      }
+    }
+  }
+  return __all_sync(0xffffffffu, bad == 0);
+}
+
+}  // namespace dsr
+}  // namespace mcs

@@ -196,7 +196,9 @@ __device__ __forceinline__ void stage_soc(SG Sg, double* Wd, int tid, int nthr) 
 }
 
 // W column block J = L^-1 S_oc[:, block J], in place over the staged S_oc.
-template <int K>
+// YM: FP64-pipe throttle (tools/dmma_prio.cu): __nanosleep(0) after a DMMA
+// burst lets the dependent chains of the co-resident warps through.
+template <int K, int YM = 0>
 __device__ __forceinline__ void w_block(const double* LI, double* Wd, int J) {
   using G = Geo<K>;
   constexpr int WST = G::WST, LST = G::LST, NIR = G::NIR;
@@ -217,11 +219,12 @@ __device__ __forceinline__ void w_block(const double* LI, double* Wd, int J) {
       *reinterpret_cast<double2*>(Wd + (8 * I + g) * WST + 8 * J + 2 * t) =
           make_double2(cacc[I][0], cacc[I][1]);
   __syncwarp();
+  if constexpr (YM & 1) __nanosleep(0);
 }
 
 // Output tiles q = tile0, tile0 + step, ... of [X (NIT x NCB) | S_oo^-1
 // (lower NIT) | Sd_T (lower NCB)] into the ext record xo and Sd_T so.
-template <int K, class SG>
+template <int K, class SG, int YM = 0>
 __device__ __forceinline__ void out_tiles(SG Sg, const double* LI, const double* Wd, double* xo,
                                           double* so, int tile0, int step) {
   using G = Geo<K>;
@@ -230,6 +233,8 @@ __device__ __forceinline__ void out_tiles(SG Sg, const double* LI, const double*
   const int lane = threadIdx.x & 31, g = lane >> 2, t = lane & 3;
 #pragma unroll 1
   for (int q = tile0; q < G::NTILES; q += step) {
+    if constexpr (YM & 2) __nanosleep(0);
+    if constexpr (YM & 4) { if ((q & 3) == 3) __nanosleep(0); }
     if (q < G::NTX) {                          // X = L^-T W
       const int I = q / G::NCB, J = q % G::NCB;
       double c0 = 0.0, c1 = 0.0;

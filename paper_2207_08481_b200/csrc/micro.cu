@@ -27,7 +27,13 @@
 // The next element's packed A (14.6 KB at n = 60) arrives by one 1-D bulk
 // copy (TMA engine) during phase 2 and its B^T is loaded into registers
 // during phase 1, so the HBM traffic overlaps the arithmetic.
+#include <cstdlib>
+
 #include "elim_v5.cuh"
+
+#ifndef MCS_MICRO_YM
+#define MCS_MICRO_YM 0
+#endif
 
 namespace mcs {
 namespace micro {
@@ -215,7 +221,17 @@ __device__ __forceinline__ void unpack_a(const double* __restrict__ P, double* _
 
 // Phase 2 for the column blocks [CB, CE) of one warp.  X: warp 0's W^T_j
 // tiles (double-buffered by j parity) for the cross blocks of warp 1.
-template <int NS, int NC, int CB, int CE>
+// YM: FP64-pipe throttle mask (tools/dmma_prio.cu): a warp that streams DMMAs
+// delays every dependent FP64 op of the co-resident warps by hundreds of
+// cycles; __nanosleep(0) after a burst lets their chains through.
+// bit 0: after every trailing-update tile, 1: after every trailing row,
+// 2: after every phase-2 pivot block, 3: after every phase-2 B^T row update.
+template <int YM, int BIT>
+__device__ __forceinline__ void yield_fp64() {
+  if constexpr ((YM >> BIT) & 1) __nanosleep(0);
+}
+
+template <int NS, int NC, int CB, int CE, int YM>
 __device__ __forceinline__ void phase2(const double* T, double* X, double2 (&bt)[CE - CB][Geo<NS, NC>::NP],
                                        double* __restrict__ Se) {
   using G = Geo<NS, NC>;
@@ -252,7 +268,9 @@ __device__ __forceinline__ void phase2(const double* T, double* X, double2 (&bt)
       const double2 l = ld2(T + G::q(i, j) * 64);
 #pragma unroll
       for (int a = 0; a < NW; ++a) mma_xyt(bt[a][i], neg(wt[a]), l);
+      yield_fp64<YM, 3>();
     }
+    yield_fp64<YM, 2>();
     bar(2);
     if constexpr (CROSS) {
 #pragma unroll
@@ -286,7 +304,7 @@ __device__ __forceinline__ void phase2(const double* T, double* X, double2 (&bt)
 // One element, from the point of view of warp WARP (0 or 1).  The two warps
 // run the same barrier sequence; each instantiation only keeps its own B^T
 // column blocks live.
-template <int NS, int NC, int WARP>
+template <int NS, int NC, int WARP, int YM>
 __device__ __forceinline__ void element(const double* __restrict__ A, const double* __restrict__ B,
                                         double* __restrict__ S, int* __restrict__ info,
                                         int64_t batch, int64_t e, double* T, double* X, double* P,
@@ -356,7 +374,9 @@ __device__ __forceinline__ void element(const double* __restrict__ A, const doub
             double2 c = ld2(C);
             mma_xyt(c, li, ld2(T + G::q(k, j) * 64));
             st2(C, c);
+            yield_fp64<YM, 0>();
           }
+          yield_fp64<YM, 1>();
         }
       }
       bar(1);
@@ -366,7 +386,7 @@ __device__ __forceinline__ void element(const double* __restrict__ A, const doub
   // ---- phase 2: W^T = B^T L^-T, S = W^T W (registers)
   double* Se = S + e * (int64_t)(NC * (NC + 1) / 2);
   if constexpr (CE > CB)
-    phase2<NS, NC, CB, CE>(T, X, bt, Se);
+    phase2<NS, NC, CB, CE, YM>(T, X, bt, Se);
   else
     for (int j = 0; j < NP; ++j) bar(2);
   MP(WARP, 4);
@@ -375,7 +395,7 @@ __device__ __forceinline__ void element(const double* __restrict__ A, const doub
   MP(WARP, 5);
 }
 
-template <int NS, int NC>
+template <int NS, int NC, int YM>
 __global__ void __launch_bounds__(64, 6)
     spd_schur_w2(const double* __restrict__ A, const double* __restrict__ B,
                  double* __restrict__ S, int* __restrict__ info, int64_t batch) {
@@ -403,19 +423,19 @@ __global__ void __launch_bounds__(64, 6)
   const bool w0 = threadIdx.x < 32;
   for (; e < batch; e += gridDim.x, phase ^= 1) {
     if (w0)
-      element<NS, NC, 0>(A, B, S, info, batch, e, T, X, P, mbar, phase, ones, &bad);
+      element<NS, NC, 0, YM>(A, B, S, info, batch, e, T, X, P, mbar, phase, ones, &bad);
     else
-      element<NS, NC, 1>(A, B, S, info, batch, e, T, X, P, mbar, phase, ones, &bad);
+      element<NS, NC, 1, YM>(A, B, S, info, batch, e, T, X, P, mbar, phase, ones, &bad);
   }
 }
 
 }  // namespace micro
 
-template <int NS, int NC>
-int launch_spd_schur_w2(const double* A, const double* B, double* S, int* info, int64_t batch,
-                        cudaStream_t st) {
+template <int NS, int NC, int YM>
+static int launch_w2(const double* A, const double* B, double* S, int* info, int64_t batch,
+                     cudaStream_t st) {
   using G = micro::Geo<NS, NC>;
-  auto kern = micro::spd_schur_w2<NS, NC>;
+  auto kern = micro::spd_schur_w2<NS, NC, YM>;
   const size_t smem = G::SMEM;
   cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   int per_sm = 0;
@@ -425,6 +445,24 @@ int launch_spd_schur_w2(const double* A, const double* B, double* S, int* info, 
   const int64_t g = (int64_t)per_sm * sm_count();
   kern<<<(int)(batch < g ? batch : g), 64, smem, st>>>(A, B, S, info, batch);
   return launch_status();
+}
+
+template <int NS, int NC>
+int launch_spd_schur_w2(const double* A, const double* B, double* S, int* info, int64_t batch,
+                        cudaStream_t st) {
+  // MCS_MICRO_YIELD = throttle mask (A/B measurements; default MCS_MICRO_YM)
+  static const int ym = getenv("MCS_MICRO_YIELD") ? atoi(getenv("MCS_MICRO_YIELD")) : MCS_MICRO_YM;
+  switch (ym) {
+    case 1: return launch_w2<NS, NC, 1>(A, B, S, info, batch, st);
+    case 2: return launch_w2<NS, NC, 2>(A, B, S, info, batch, st);
+    case 4: return launch_w2<NS, NC, 4>(A, B, S, info, batch, st);
+    case 8: return launch_w2<NS, NC, 8>(A, B, S, info, batch, st);
+    case 5: return launch_w2<NS, NC, 5>(A, B, S, info, batch, st);
+    case 6: return launch_w2<NS, NC, 6>(A, B, S, info, batch, st);
+    case 9: return launch_w2<NS, NC, 9>(A, B, S, info, batch, st);
+    case 10: return launch_w2<NS, NC, 10>(A, B, S, info, batch, st);
+  }
+  return launch_w2<NS, NC, 0>(A, B, S, info, batch, st);
 }
 
 template int launch_spd_schur_w2<60, 36>(const double*, const double*, double*, int*, int64_t,
