@@ -25,6 +25,7 @@
 // columns, produced by a DMMA of the bubble part of B with L_b^-T whose
 // accumulator layout IS the operand layout.
 #include "common.cuh"
+#include "ds_reg.cuh"
 
 namespace mcs {
 
@@ -127,9 +128,6 @@ struct Geo {
   static constexpr int NKC = NLF + MIX + NBP;         // 8-column chunks of Y
   static constexpr int NKS = (nb + 3) / 4;            // k-steps of the bubble DMMA
   static constexpr int NR = T::NR, NRB = NR / 8;
-  static constexpr int NIK = (NI + 3) / 4;            // k-steps of Sd = S_cc - W^T W
-  static constexpr int NCB = (NC + 7) / 8;            // Sd tile rows
-  static constexpr int WST = 36;                      // W row stride (== 4 mod 16: conflict-free)
   static constexpr int st_len = ExtLayout<K>::st_len;
   // per-warp shared memory (doubles)
   static constexpr int o_w = 0;
@@ -138,18 +136,10 @@ struct Geo {
   static constexpr int o_U = o_S + st_len;            // phase-dependent union
   static constexpr int UA = 2 * nb * nb + even(nb);   // Ls | Li | 1/diag
   static constexpr int UB = even(6 * ml * 2);         // G[edge group][m][s] (phase B)
-  static constexpr int NIT = (NI + 7) / 8;            // 8-row tiles of L^-1 / X
-  static constexpr int LST = 20;                      // L^-1 row stride (== 4 mod 16)
-  static constexpr int NIR = 8 * NIT > 4 * NIK ? 8 * NIT : 4 * NIK;   // padded rows
-  static constexpr int o_Da = 0;                     // Loo, then S_oc, then W (in place)
-  static constexpr int o_LI = (NI * NI > NIR * WST ? NI * NI : NIR * WST);
-  static constexpr int o_Rd = o_LI + NIR * LST;
-  static constexpr int UD = o_Rd + even(NI);
+  static constexpr int UD = dsr::Geo<K>::PER_WARP;    // phase D: private tile slots of S_oo
   static constexpr int UMAX = UA > UB ? (UA > UD ? UA : UD) : (UB > UD ? UB : UD);
   static constexpr int PER_WARP = o_U + even(UMAX);
-  static_assert(nb <= 32 && ml <= 32 && NI <= 32 && NC <= 32, "lane-per-row factorisations");
-  static_assert(8 * NCB <= WST, "W columns");
-  static_assert(8 * NIT <= LST && 4 * NIK <= LST, "L^-1 columns");
+  static_assert(nb <= 32 && ml <= 32, "lane-per-row factorisations");
   static_assert(6 * ml * 2 <= nb * nb, "G fits over Ls");
   using RW = Rows<K>;
   __host__ __device__ static constexpr int row_type(int i) { return RW::row_type(i); }
@@ -237,7 +227,6 @@ __global__ void __launch_bounds__(32 * WPB, MINB)
   using L = ExtLayout<K>;
   constexpr int ml = G::ml, nb = G::nb, nl = G::nl, ns = G::ns, nu = G::nu, nloc = G::nloc;
   constexpr int NI = G::NI, NC = G::NC, NEM = G::NEM, NRB = G::NRB, NKC = G::NKC;
-  constexpr int WST = G::WST;
   extern __shared__ __align__(16) double smem[];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, g = lane >> 2, t = lane & 3;
   double* stab = smem;                                   // compact Bsig tables (per CTA)
@@ -549,126 +538,13 @@ __global__ void __launch_bounds__(32 * WPB, MINB)
     }
 
     FZ_T(2);
-    // ---------------- D: double Schur on the element-local S_T
-    //   S_oo = L L^T (lane-per-row Cholesky), L^-1 (lane-per-column forward
-    //   substitution), then four small GEMMs on the tensor cores:
-    //   W = L^-1 S_oc, X = L^-T W, S_oo^-1 = L^-T L^-1, Sd_T = S_cc - W^T W.
-    auto S = [&](int a, int b) { return a >= b ? Spk[pk(a, b)] : Spk[pk(b, a)]; };
-    constexpr int LST = G::LST, NIR = G::NIR;
-    double* Loo = U + G::o_Da;
-    double* Soc = U + G::o_Da;            // after L^-1 is formed
-    double* LIs = U + G::o_LI;
-    double* Wd = U + G::o_Da;             // W overwrites S_oc column block by column block
-    double* Rdo = U + G::o_Rd;
+    // ---------------- D: double Schur on the element-local S_T, register
+    // resident (ds_reg.cuh): one sweep over the 8x8 pivot tiles of S_oo with
+    // S_co and an identity block as right-hand sides, then Sd_T, X and
+    // S_oo^-1 as X Y^T products of register tiles
     {
-      const int i = lane < NI ? lane : 0;
-      double a[NI], l[NI];
-#pragma unroll
-      for (int c = 0; c < NI; ++c) a[c] = S(NEM + i, NEM + c);
-      if (!fz::chol_rows<NI>(a, l, Rdo)) bad |= 2;
-      if (lane < NI) {
-#pragma unroll
-        for (int c = 0; c < NI; ++c) Loo[lane * NI + c] = l[c];
-      }
-    }
-    for (int q = lane; q < NIR * LST; q += 32) {   // zero padding of L^-1
-      const int j = q / LST, c = q % LST;
-      if (j >= NI || c >= NI) LIs[q] = 0.0;
-    }
-    __syncwarp();
-    if (lane < NI) {   // column `lane` of L^-1 (blocked forward substitution)
-      double x[NI];
-      fz::linv_col<NI>(Loo, NI, Rdo, lane, x);
-#pragma unroll
-      for (int j = 0; j < NI; ++j) LIs[j * LST + lane] = x[j];
-    }
-    __syncwarp();
-    {   // S_oc (row j = interior dof NEM + j, column c = coupling dof), zero padded, over Loo
-      const int lc = cpl_local<K>(lane);
-#pragma unroll
-      for (int j = 0; j < NIR; ++j) {
-        const int a = NEM + j;
-        double v = 0.0;
-        if (j < NI && lane < NC) v = Spk[lc < a ? pk(a, lc) : pk(lc, a)];
-        Soc[j * WST + lane] = v;
-        if (lane < WST - 32) Soc[j * WST + 32 + lane] = 0.0;
-      }
-    }
-    __syncwarp();
-    // W = L^-1 S_oc  (NIT x NCB tiles); a column block of W replaces the
-    // column block of S_oc it was computed from
-#pragma unroll
-    for (int J = 0; J < G::NCB; ++J) {
-      double c[G::NIT][2];
-#pragma unroll
-      for (int I = 0; I < G::NIT; ++I) {
-        c[I][0] = c[I][1] = 0.0;
-#pragma unroll
-        for (int ks = 0; ks < G::NIK; ++ks)
-          dmma884(c[I][0], c[I][1], LIs[(8 * I + g) * LST + 4 * ks + t],
-                  Soc[(4 * ks + t) * WST + 8 * J + g]);
-      }
-      __syncwarp();
-#pragma unroll
-      for (int I = 0; I < G::NIT; ++I)
-        if (8 * I + g < NIR)
-          *reinterpret_cast<double2*>(Wd + (8 * I + g) * WST + 8 * J + 2 * t) =
-              make_double2(c[I][0], c[I][1]);
-      __syncwarp();
-    }
-    __syncwarp();
-    double* xo = ext + e * L::len;
-    // X = L^-T W
-#pragma unroll
-    for (int I = 0; I < G::NIT; ++I) {
-#pragma unroll
-      for (int J = 0; J < G::NCB; ++J) {
-        double c0 = 0.0, c1 = 0.0;
-#pragma unroll
-        for (int ks = 0; ks < G::NIK; ++ks)
-          dmma884(c0, c1, LIs[(4 * ks + t) * LST + 8 * I + g], Wd[(4 * ks + t) * WST + 8 * J + g]);
-        const int i = 8 * I + g, c = 8 * J + 2 * t;
-        if (i < NI) {
-          if (c < NC) xo[i * NC + c] = c0;
-          if (c + 1 < NC) xo[i * NC + c + 1] = c1;
-        }
-      }
-    }
-    // S_oo^-1 = L^-T L^-1 (lower packed)
-#pragma unroll
-    for (int I = 0; I < G::NIT; ++I) {
-#pragma unroll
-      for (int J = 0; J <= I; ++J) {
-        double c0 = 0.0, c1 = 0.0;
-#pragma unroll
-        for (int ks = 0; ks < G::NIK; ++ks)
-          dmma884(c0, c1, LIs[(4 * ks + t) * LST + 8 * I + g], LIs[(4 * ks + t) * LST + 8 * J + g]);
-        const int i = 8 * I + g, j = 8 * J + 2 * t;
-        if (i < NI) {
-          if (j <= i) xo[L::x_len + pk(i, j)] = c0;
-          if (j + 1 <= i) xo[L::x_len + pk(i, j + 1)] = c1;
-        }
-      }
-    }
-    // Sd_T = S_cc - W^T W on the tensor cores (lower 8x8 tiles)
-    double* so = Sd + e * L::sd_len;
-#pragma unroll
-    for (int I = 0; I < G::NCB; ++I) {
-#pragma unroll
-      for (int J = 0; J <= I; ++J) {
-        double c0 = 0.0, c1 = 0.0;
-#pragma unroll
-        for (int ks = 0; ks < G::NIK; ++ks) {
-          const double* wr = Wd + (4 * ks + t) * WST;
-          dmma884(c0, c1, wr[8 * I + g], wr[8 * J + g]);
-        }
-        const int a = 8 * I + g, b = 8 * J + 2 * t;
-        if (a < NC) {
-          const int la = cpl_local<K>(a);
-          if (b <= a) so[pk(a, b)] = S(la, cpl_local<K>(b)) - c0;
-          if (b + 1 <= a) so[pk(a, b + 1)] = S(la, cpl_local<K>(b + 1)) - c1;
-        }
-      }
+      auto S = [&](int a, int b) { return a >= b ? Spk[pk(a, b)] : Spk[pk(b, a)]; };
+      if (!dsr::element<K>(S, U, ext + e * L::len, Sd + e * L::sd_len)) bad |= 2;
     }
     FZ_T(3);
     if (lane == 0 && info) info[e] = bad;

@@ -189,7 +189,9 @@ __global__ void __launch_bounds__(32 * WPB, MINB)
       for (int off = lane * 128; off < L::st_len * 8; off += 32 * 128)
         asm volatile("prefetch.global.L2 [%0];" ::"l"(nx + off));
     }
-    const bool ok = dsr::element<K>(ST + e * L::st_len, T, ext + e * L::len, Sd + e * L::sd_len);
+    const double* S = ST + e * L::st_len;
+    auto sym = [&](int a, int b) { return __ldg(S + (a >= b ? pk(a, b) : pk(b, a))); };
+    const bool ok = dsr::element<K>(sym, T, ext + e * L::len, Sd + e * L::sd_len);
     if (lane == 0 && info) info[e] = ok ? 0 : 1;
   }
 }

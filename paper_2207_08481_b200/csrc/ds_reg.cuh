@@ -82,18 +82,17 @@ __device__ __forceinline__ double2 chol8m(double y0, double y1, int& bad, int ba
   return make_double2(x0, x1);
 }
 
-// One element.  S: packed lower S_T; T: this warp's NT private tile slots.
+// One element.  sym(a, b): entry (a, b) of the symmetric S_T (global or
+// shared memory); T: this warp's NT private tile slots (16-byte aligned).
 // Returns false if S_oo is not positive definite.
-template <int K>
-__device__ __forceinline__ bool element(const double* __restrict__ S, double* __restrict__ T,
+template <int K, class SYM>
+__device__ __forceinline__ bool element(SYM sym, double* __restrict__ T,
                                         double* __restrict__ xo, double* __restrict__ so) {
   using G = Geo<K>;
   using L = ExtLayout<K>;
   constexpr int NI = G::NI, NC = G::NC, NEM = G::NEM, NP = G::NP, NCB = G::NCB;
   const int lane = threadIdx.x & 31, g = lane >> 2, t = lane & 3;
   double* Tl = T + 2 * lane;
-  auto sym = [&](int a, int b) { return __ldg(S + (a >= b ? pk(a, b) : pk(b, a))); };
-
   // ---- loads: S_co tiles into registers, S_oo lower tiles into the slots
   double2 bt[NCB][NP];
 #pragma unroll
