@@ -1,6 +1,10 @@
-// Fused element pipeline for degrees k <= 4: geometry weights -> element
-// blocks -> sigma/omega condensation -> double Schur, ONE WARP PER ELEMENT
-// (SURVEY §8a rows A1 + A3 + A4, §8f-1).
+// Fused element pipeline: geometry weights -> element blocks -> sigma/omega
+// condensation -> double Schur, ONE WARP PER ELEMENT (SURVEY §8a rows
+// A1 + A3 + A4, §8f-1).  k <= 4: Y whole in registers, one pass.  k = 5, 6:
+// Y is produced CPP column chunks at a time (passes), the partial S_T sums
+// live in the warp's packed shared-memory copy between passes, the
+// lane-ordered Bsig tables are read from a global (L2-resident) buffer with
+// coalesced loads instead of a per-CTA shared-memory copy.
 //
 // Algebra (csrc/condense_struct.cu): with the block
 // structure of the MCS element spaces
@@ -129,16 +133,24 @@ struct Geo {
   static constexpr int NKS = (nb + 3) / 4;            // k-steps of the bubble DMMA
   static constexpr int NR = T::NR, NRB = NR / 8;
   static constexpr int st_len = ExtLayout<K>::st_len;
+  // k >= 5 (BIG): Y in passes of CPP chunks, tables in global memory, the
+  // phase-A factors alias the packed S_T (dead until the first pass ends),
+  // G has its own slot (it lives across the passes)
+  static constexpr bool BIG = K >= 5;
+  static constexpr int CPP = BIG ? 3 : NKC;
+  static constexpr int NPASS = (NKC + CPP - 1) / CPP;
+  static constexpr int NG = 6 * ml * 2;               // G[edge group][m][s]
   // per-warp shared memory (doubles)
   static constexpr int o_w = 0;
   static constexpr int o_F = NWS;                     // F_m, 6 per block
-  static constexpr int o_S = o_F + even(6 * ml);      // packed S_T
-  static constexpr int o_U = o_S + st_len;            // phase-dependent union
+  static constexpr int o_G = o_F + even(6 * ml);      // G (BIG only)
+  static constexpr int o_S = o_G + (BIG ? even(NG) : 0);   // packed S_T
   static constexpr int UA = 2 * nb * nb + even(nb);   // Ls | Li | 1/diag
   static constexpr int UB = even(6 * ml * 2);         // G[edge group][m][s] (phase B)
+  static constexpr int o_U = BIG ? o_S : o_S + st_len;     // phase-dependent union
   static constexpr int UD = dsr::Geo<K>::PER_WARP;    // phase D: private tile slots of S_oo
   static constexpr int UMAX = UA > UB ? (UA > UD ? UA : UD) : (UB > UD ? UB : UD);
-  static constexpr int PER_WARP = o_U + even(UMAX);
+  static constexpr int PER_WARP = BIG ? o_S + (st_len > even(UA) ? st_len : even(UA)) : o_U + even(UMAX);
   static_assert(nb <= 32 && ml <= 32, "lane-per-row factorisations");
   static_assert(6 * ml * 2 <= nb * nb, "G fits over Ls");
   using RW = Rows<K>;
@@ -153,7 +165,6 @@ struct Geo {
   static constexpr int TAB_MB = TAB_BU + RW::bu_off(NRB, NKS);        // MbRef [6][nb][nb]
   static constexpr int TAB_A = TAB_MB + even(6 * nb * nb);   // ARef [6][ml][9]
   static constexpr int TAB_SMEM = TAB_A + even(6 * 9 * ml);
-  static constexpr int NG = 6 * ml * 2;                      // G[edge group][m][s], in U during phase B
   // bubble column of DMMA n-tile bt, output column n (-1: none)
   __host__ __device__ static constexpr int jmap(int bt, int n) {
     if (MIX && bt == 0) return (n >= 2 * r && n - 2 * r < nb) ? n - 2 * r : -1;
@@ -216,25 +227,17 @@ __device__ __forceinline__ void linv_col(const double* Ls, int ls, const double*
 
 }  // namespace fz
 
-template <int K, int WPB, int MINB>
-__global__ void __launch_bounds__(32 * WPB, MINB)
-    condense_fused_kernel(const double* __restrict__ Wg, int nwgt, const double* __restrict__ tab,
-                          double* __restrict__ ST,
-                          double* __restrict__ ext, double* __restrict__ Sd,
-                          int* __restrict__ info, int64_t nt) {
+// Lane-ordered Bsig tables (layout: fz::Rows / fz::Geo) plus the MbRef and
+// ARef segments, from the FTab tables.  Threads tid, tid + nthr, ...
+template <int K>
+__device__ __forceinline__ void build_lane_tables(const double* __restrict__ tab,
+                                                  double* __restrict__ stab, int tid, int nthr) {
   using G = fz::Geo<K>;
   using T = FTab<K>;
-  using L = ExtLayout<K>;
-  constexpr int ml = G::ml, nb = G::nb, nl = G::nl, ns = G::ns, nu = G::nu, nloc = G::nloc;
-  constexpr int NI = G::NI, NC = G::NC, NEM = G::NEM, NRB = G::NRB, NKC = G::NKC;
-  extern __shared__ __align__(16) double smem[];
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, g = lane >> 2, t = lane & 3;
-  double* stab = smem;                                   // compact Bsig tables (per CTA)
-  double* sw = smem + G::TAB_SMEM + warp * G::PER_WARP;
-  for (int q = threadIdx.x; q < 6 * nb * nb; q += 32 * WPB) stab[G::TAB_MB + q] = tab[T::o_Mb + q];
-  for (int q = threadIdx.x; q < 6 * 9 * ml; q += 32 * WPB) stab[G::TAB_A + q] = tab[T::o_A + q];
-  // lane-ordered Bsig tables (layout: fz::Geo)
-  for (int q = threadIdx.x; q < 32 * G::NLOW * NRB; q += 32 * WPB) {
+  constexpr int ml = G::ml, nb = G::nb, nl = G::nl, ns = G::ns, nloc = G::nloc, NRB = G::NRB;
+  for (int q = tid; q < 6 * nb * nb; q += nthr) stab[G::TAB_MB + q] = tab[T::o_Mb + q];
+  for (int q = tid; q < 6 * 9 * ml; q += nthr) stab[G::TAB_A + q] = tab[T::o_A + q];
+  for (int q = tid; q < 32 * G::NLOW * NRB; q += nthr) {
     const int ln = q & 31, kc = (q >> 5) % G::NLOW, I = (q >> 5) / G::NLOW;
     const int i = 8 * I + (ln >> 2), m = 4 * kc + (ln & 3);
     double b0 = 0.0, b1 = 0.0, b2 = 0.0, eh = 0.0;
@@ -260,7 +263,7 @@ __global__ void __launch_bounds__(32 * WPB, MINB)
       dst[kc * 32 + ln] = eh;
     }
   }
-  for (int q = threadIdx.x; q < 32 * G::NKS * NRB; q += 32 * WPB) {
+  for (int q = tid; q < 32 * G::NKS * NRB; q += nthr) {
     const int ln = q & 31, ks = (q >> 5) % G::NKS, I = (q >> 5) / G::NKS;
     const int i = 8 * I + (ln >> 2), c = 4 * ks + (ln & 3);
     double v0 = 0.0, v1 = 0.0, v2 = 0.0, v3 = 0.0;
@@ -286,14 +289,51 @@ __global__ void __launch_bounds__(32 * WPB, MINB)
       dst[ks * 32 + ln] = v0;
     }
   }
-  __syncthreads();
+}
+
+// k >= 5: the tables once per call into a global buffer (stays in L2)
+template <int K>
+__global__ void fused_lane_tables_kernel(const double* __restrict__ tab, double* __restrict__ gtab) {
+  build_lane_tables<K>(tab, gtab, blockIdx.x * blockDim.x + threadIdx.x, gridDim.x * blockDim.x);
+}
+
+template <int N>
+struct IC {
+  static constexpr int value = N;
+};
+
+// DS: the double Schur as phase D (ext, Sd written); otherwise S_T only.
+template <int K, int WPB, int MINB, bool DS>
+__global__ void __launch_bounds__(32 * WPB, MINB)
+    condense_fused_kernel(const double* __restrict__ Wg, int nwgt, const double* __restrict__ tab,
+                          const double* __restrict__ gtab, double* __restrict__ ST,
+                          double* __restrict__ ext, double* __restrict__ Sd,
+                          int* __restrict__ info, int64_t nt) {
+  using G = fz::Geo<K>;
+  using T = FTab<K>;
+  using L = ExtLayout<K>;
+  constexpr int ml = G::ml, nb = G::nb, nu = G::nu, nloc = G::nloc;
+  constexpr int NRB = G::NRB, NKC = G::NKC, CPP = G::CPP, NPASS = G::NPASS;
+  constexpr bool BIG = G::BIG;
+  extern __shared__ __align__(16) double smem[];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, g = lane >> 2, t = lane & 3;
+  const double* stab;                                    // lane-ordered Bsig tables
+  double* sw;
+  if constexpr (BIG) {
+    stab = gtab;
+    sw = smem + warp * G::PER_WARP;
+  } else {
+    build_lane_tables<K>(tab, smem, threadIdx.x, 32 * WPB);   // compact copy per CTA
+    __syncthreads();
+    stab = smem;
+    sw = smem + G::TAB_SMEM + warp * G::PER_WARP;
+  }
   double* wts = sw + G::o_w;
   double* Fs = sw + G::o_F;
   double* Spk = sw + G::o_S;
   double* U = sw + G::o_U;
 
   if (lane < fz::NWS - 30) wts[30 + lane] = 0.0;        // zero weight slots
-  if (lane == 0) Spk[G::st_len - 1] = 0.0;              // packed padding (never written)
   const int64_t nw = static_cast<int64_t>(gridDim.x) * WPB;
   int64_t e = static_cast<int64_t>(blockIdx.x) * WPB + warp;
   const int nwl = nwgt < 30 ? nwgt : 30;
@@ -345,16 +385,14 @@ __global__ void __launch_bounds__(32 * WPB, MINB)
       const double a00 = A[0], a10 = A[3], a11 = A[4], a20 = A[6], a21 = A[7], a22 = A[8];
       const double d11p = a11 - (a10 * a10) / a00;
       const bool okA = a00 > 0.0 && d11p > 0.0;
-      const double i00 = rsqrt_nr(a00), l00 = a00 * i00;
+      const double i00 = rsqrt_nr(a00);
       const double l10 = a10 * i00, l20 = a20 * i00;
       const double d11 = a11 - l10 * l10;
-      const double i11 = rsqrt_nr(d11), l11 = d11 * i11;
+      const double i11 = rsqrt_nr(d11);
       const double l21 = (a21 - l20 * l10) * i11;
       const double d22 = a22 - l20 * l20 - l21 * l21;
       const double i22 = rsqrt_nr(d22);
       if (!(okA && d22 > 0.0)) bad |= 1;
-      (void)l00;
-      (void)l11;
       const double v0 = s0 * i00;
       const double v1 = (s1 - l10 * v0) * i11;
       const double v2 = (s2 - l20 * v0 - l21 * v1) * i22;
@@ -406,130 +444,166 @@ __global__ void __launch_bounds__(32 * WPB, MINB)
     __syncwarp();
     // G[grp][m][s] = sum_a w[9 + 3 grp + a] F_m[a][s]: the edge weights of
     // the three bus edges (grp 0..2) and the three bhs edges (3..5) folded
-    // into F (over Ls, which is dead once L_b^-1 is formed)
-    double* Gs = U;
+    // into F (k <= 4: over Ls, which is dead once L_b^-1 is formed)
+    double* Gs = BIG ? sw + G::o_G : U;
     for (int q = lane; q < G::NG; q += 32) {
       const int sI = q & 1, m = (q >> 1) % ml, grp = (q >> 1) / ml;
       const double* w = wts + 9 + 3 * grp;
       const double* Fm = Fs + 6 * m + sI;
       Gs[q] = fma(w[0], Fm[0], fma(w[1], Fm[2], w[2] * Fm[4]));
     }
+    if (lane == 0) Spk[G::st_len - 1] = 0.0;              // packed padding (never written)
     __syncwarp();
 
     FZ_T(0);
-    // ---------------- B: Y in registers, every lane generating exactly the
-    // Bsig entries its registers need from the lane-ordered tables
-    double2 Yf[NRB][NKC];
+    const double wad = wts[fz::W_ADIV];
+    // ---------------- passes over the column chunks [k0, k1) of Y
+    auto pass = [&](auto PSc) {
+      constexpr int PS = decltype(PSc)::value;
+      // executed from the last chunks down: the bubble chunks (and with them
+      // the L_b^-T operands) belong to pass 0 only
+      constexpr int k1 = NKC - PS * CPP, k0 = (k1 > CPP) ? k1 - CPP : 0, NCH = k1 - k0;
+      static_assert(!BIG || PS == 0 || k1 <= G::NLF, "bubble chunks in pass 0 only");
+      // ---- B: Y chunks in registers, every lane generating exactly the Bsig
+      // entries its registers need from the lane-ordered tables
+      double2 Yf[NRB][NCH];
 #pragma unroll
-    for (int kc = 0; kc < G::NLOW; ++kc) {
-      const int m = 4 * kc + t;
-      const int mm = m < ml ? m : ml - 1;       // padding lanes: zero table entries
-      const double2 F0 = *reinterpret_cast<const double2*>(Fs + 6 * mm);
-      const double2 F1 = *reinterpret_cast<const double2*>(Fs + 6 * mm + 2);
-      const double2 F2 = *reinterpret_cast<const double2*>(Fs + 6 * mm + 4);
+      for (int kc = k0; kc < k1; ++kc) {
+        if (kc >= G::NLOW) {
+#pragma unroll
+          for (int I = 0; I < NRB; ++I) Yf[I][kc - k0] = make_double2(0.0, 0.0);
+          continue;
+        }
+        const int m = 4 * kc + t;
+        const int mm = m < ml ? m : ml - 1;       // padding lanes: zero table entries
+        const double2 F0 = *reinterpret_cast<const double2*>(Fs + 6 * mm);
+        const double2 F1 = *reinterpret_cast<const double2*>(Fs + 6 * mm + 2);
+        const double2 F2 = *reinterpret_cast<const double2*>(Fs + 6 * mm + 4);
+#pragma unroll
+        for (int I = 0; I < NRB; ++I) {
+          const double* tl = stab + G::TAB_LO + G::lo_off(I);
+          const int fmt = G::fmt_low(I);
+          double y0 = 0.0, y1 = 0.0, eh4 = 0.0;
+          if (fmt != 1) {
+            double b0, b1, b2;
+            if (fmt == 4) {
+              const double2 p = *reinterpret_cast<const double2*>(tl + (2 * kc) * 64 + 2 * lane);
+              const double2 q = *reinterpret_cast<const double2*>(tl + (2 * kc + 1) * 64 + 2 * lane);
+              b0 = p.x;
+              b1 = p.y;
+              b2 = q.x;
+              eh4 = q.y;
+            } else {
+              b0 = tl[(3 * kc) * 32 + lane];
+              b1 = tl[(3 * kc + 1) * 32 + lane];
+              b2 = tl[(3 * kc + 2) * 32 + lane];
+            }
+            y0 = fma(b0, F0.x, fma(b1, F1.x, b2 * F2.x));
+            y1 = fma(b0, F0.y, fma(b1, F1.y, b2 * F2.y));
+          }
+          if (fmt != 3) {
+            const double eh = fmt == 4 ? eh4 : tl[kc * 32 + lane];
+            const int wo = G::row_woff(8 * I + g);
+            const int grp = wo < 30 ? (wo - 9) / 3 : 0;      // interior / padding rows: Ehat = 0
+            const double2 Gm = *reinterpret_cast<const double2*>(Gs + 2 * (grp * ml + mm));
+            y0 = fma(eh, Gm.x, y0);
+            y1 = fma(eh, Gm.y, y1);
+          }
+          Yf[I][kc - k0] = make_double2(y0, y1);
+        }
+      }
+      // bubble n-tiles bt whose chunk NLF + bt lies in this pass
+      constexpr int b0t = (k0 > G::NLF ? k0 - G::NLF : 0);
+      constexpr int b1t = (k1 - G::NLF < G::NBT ? k1 - G::NLF : G::NBT);
+      if constexpr (b1t > b0t) {
+#pragma unroll
+        for (int I = 0; I < NRB; ++I) {
+          const double* tb = stab + G::TAB_BU + G::bu_off(I);
+          const int fmt = G::fmt_bub(I);
+          double w0 = 0.0, w1 = 0.0, w2 = 0.0;
+          if (fmt != 1) {
+            const int wo = G::row_woff(8 * I + g);
+            w0 = wts[wo];
+            w1 = wts[wo + 1];
+            w2 = wts[wo + 2];
+          }
+          double a[G::NKS];
+#pragma unroll
+          for (int ks = 0; ks < G::NKS; ++ks) {
+            if (fmt == 4) {
+              const double2 p = *reinterpret_cast<const double2*>(tb + (2 * ks) * 64 + 2 * lane);
+              const double2 q = *reinterpret_cast<const double2*>(tb + (2 * ks + 1) * 64 + 2 * lane);
+              a[ks] = fma(w2, q.y, fma(w1, q.x, fma(w0, p.y, p.x)));
+            } else if (fmt == 3) {
+              a[ks] = fma(w2, tb[(3 * ks + 2) * 32 + lane],
+                          fma(w1, tb[(3 * ks + 1) * 32 + lane], w0 * tb[(3 * ks) * 32 + lane]));
+            } else {
+              a[ks] = tb[ks * 32 + lane];
+            }
+          }
+#pragma unroll
+          for (int bt = b0t; bt < b1t; ++bt) {
+            double c0 = 0.0, c1 = 0.0;
+#pragma unroll
+            for (int ks = 0; ks < G::NKS; ++ks) dmma884(c0, c1, a[ks], LiR[bt][ks]);
+            const int kc = G::NLF + bt - k0;
+            Yf[I][kc].x += c0;
+            Yf[I][kc].y += c1;
+          }
+        }
+      }
+      if constexpr (PS == 0) {
+        __syncwarp();          // BIG: every lane is done with the factors aliased by Spk
+        FZ_T(1);
+      }
+      // ---- C: S_T (+)= Y Y^T over this pass's chunks (DMMA); the packed
+      // shared-memory copy carries the partial sums between passes (each
+      // lane re-reads exactly the entries it stored)
+      // one tile row I at a time: the I + 1 independent accumulator chains of
+      // the row interleave (k outer, J inner) and share the A operand Y_I
 #pragma unroll
       for (int I = 0; I < NRB; ++I) {
-        const double* tl = stab + G::TAB_LO + G::lo_off(I);
-        const int fmt = G::fmt_low(I);
-        double y0 = 0.0, y1 = 0.0, eh4 = 0.0;
-        if (fmt != 1) {
-          double b0, b1, b2;
-          if (fmt == 4) {
-            const double2 p = *reinterpret_cast<const double2*>(tl + (2 * kc) * 64 + 2 * lane);
-            const double2 q = *reinterpret_cast<const double2*>(tl + (2 * kc + 1) * 64 + 2 * lane);
-            b0 = p.x;
-            b1 = p.y;
-            b2 = q.x;
-            eh4 = q.y;
-          } else {
-            b0 = tl[(3 * kc) * 32 + lane];
-            b1 = tl[(3 * kc + 1) * 32 + lane];
-            b2 = tl[(3 * kc + 2) * 32 + lane];
+        const int i = 8 * I + g;
+        double acc[NRB][2];
+#pragma unroll
+        for (int J = 0; J <= I; ++J) {
+          acc[J][0] = acc[J][1] = 0.0;
+          if constexpr (PS > 0) {
+            const int j = 8 * J + 2 * t;
+            if (i < nloc) {
+              if (j <= i) acc[J][0] = Spk[pk(i, j)];
+              if (j + 1 <= i) acc[J][1] = Spk[pk(i, j + 1)];
+            }
           }
-          y0 = fma(b0, F0.x, fma(b1, F1.x, b2 * F2.x));
-          y1 = fma(b0, F0.y, fma(b1, F1.y, b2 * F2.y));
         }
-        if (fmt != 3) {
-          const double eh = fmt == 4 ? eh4 : tl[kc * 32 + lane];
-          const int wo = G::row_woff(8 * I + g);
-          const int grp = wo < 30 ? (wo - 9) / 3 : 0;      // interior / padding rows: Ehat = 0
-          const double2 Gm = *reinterpret_cast<const double2*>(Gs + 2 * (grp * ml + mm));
-          y0 = fma(eh, Gm.x, y0);
-          y1 = fma(eh, Gm.y, y1);
+#pragma unroll
+        for (int kc = 0; kc < NCH; ++kc) {
+#pragma unroll
+          for (int J = 0; J <= I; ++J) dmma884(acc[J][0], acc[J][1], Yf[I][kc].x, Yf[J][kc].x);
+#pragma unroll
+          for (int J = 0; J <= I; ++J) dmma884(acc[J][0], acc[J][1], Yf[I][kc].y, Yf[J][kc].y);
         }
-        Yf[I][kc] = make_double2(y0, y1);
-      }
-    }
 #pragma unroll
-    for (int I = 0; I < NRB; ++I) {
-#pragma unroll
-      for (int kc = G::NLOW; kc < NKC; ++kc) Yf[I][kc] = make_double2(0.0, 0.0);
-      const double* tb = stab + G::TAB_BU + G::bu_off(I);
-      const int fmt = G::fmt_bub(I);
-      double w0 = 0.0, w1 = 0.0, w2 = 0.0;
-      if (fmt != 1) {
-        const int wo = G::row_woff(8 * I + g);
-        w0 = wts[wo];
-        w1 = wts[wo + 1];
-        w2 = wts[wo + 2];
-      }
-      double a[G::NKS];
-#pragma unroll
-      for (int ks = 0; ks < G::NKS; ++ks) {
-        if (fmt == 4) {
-          const double2 p = *reinterpret_cast<const double2*>(tb + (2 * ks) * 64 + 2 * lane);
-          const double2 q = *reinterpret_cast<const double2*>(tb + (2 * ks + 1) * 64 + 2 * lane);
-          a[ks] = fma(w2, q.y, fma(w1, q.x, fma(w0, p.y, p.x)));
-        } else if (fmt == 3) {
-          a[ks] = fma(w2, tb[(3 * ks + 2) * 32 + lane],
-                      fma(w1, tb[(3 * ks + 1) * 32 + lane], w0 * tb[(3 * ks) * 32 + lane]));
-        } else {
-          a[ks] = tb[ks * 32 + lane];
+        for (int J = 0; J <= I; ++J) {
+          const int j = 8 * J + 2 * t;
+          double c0 = acc[J][0], c1 = acc[J][1];
+          if constexpr (PS == NPASS - 1) {
+            if (i < nu && j < nu) c0 = fma(wad, __ldg(tab + T::o_adiv + i * nu + j), c0);
+            if (i < nu && j + 1 < nu) c1 = fma(wad, __ldg(tab + T::o_adiv + i * nu + j + 1), c1);
+          }
+          if (i < nloc) {
+            if (j <= i) Spk[pk(i, j)] = c0;
+            if (j + 1 <= i) Spk[pk(i, j + 1)] = c1;
+          }
         }
+        asm volatile("" ::: "memory");   // keep the epilogue loads row by row (registers)
       }
-#pragma unroll
-      for (int bt = 0; bt < G::NBT; ++bt) {
-        double c0 = 0.0, c1 = 0.0;
-#pragma unroll
-        for (int ks = 0; ks < G::NKS; ++ks) dmma884(c0, c1, a[ks], LiR[bt][ks]);
-        const int kc = G::NLF + bt;
-        Yf[I][kc].x += c0;
-        Yf[I][kc].y += c1;
-      }
-    }
-    __syncwarp();
-
-    FZ_T(1);
-    // ---------------- C: S_T = adiv + Y Y^T (DMMA), packed into shared memory
-    const double wad = wts[fz::W_ADIV];
-    // one tile row I at a time: the I + 1 independent accumulator chains of
-    // the row interleave (k outer, J inner) and share the A operand Y_I
-#pragma unroll
-    for (int I = 0; I < NRB; ++I) {
-      double acc[NRB][2];
-#pragma unroll
-      for (int J = 0; J <= I; ++J) acc[J][0] = acc[J][1] = 0.0;
-#pragma unroll
-      for (int kc = 0; kc < NKC; ++kc) {
-#pragma unroll
-        for (int J = 0; J <= I; ++J) dmma884(acc[J][0], acc[J][1], Yf[I][kc].x, Yf[J][kc].x);
-#pragma unroll
-        for (int J = 0; J <= I; ++J) dmma884(acc[J][0], acc[J][1], Yf[I][kc].y, Yf[J][kc].y);
-      }
-      const int i = 8 * I + g;
-#pragma unroll
-      for (int J = 0; J <= I; ++J) {
-        const int j = 8 * J + 2 * t;
-        double c0 = acc[J][0], c1 = acc[J][1];
-        if (i < nu && j < nu) c0 = fma(wad, __ldg(tab + T::o_adiv + i * nu + j), c0);
-        if (i < nu && j + 1 < nu) c1 = fma(wad, __ldg(tab + T::o_adiv + i * nu + j + 1), c1);
-        if (i < nloc) {
-          if (j <= i) Spk[pk(i, j)] = c0;
-          if (j + 1 <= i) Spk[pk(i, j + 1)] = c1;
-        }
-      }
-      asm volatile("" ::: "memory");   // keep the epilogue loads row by row (registers)
-    }
+    };
+    pass(IC<0>{});
+    if constexpr (NPASS > 1) pass(IC<1>{});
+    if constexpr (NPASS > 2) pass(IC<2>{});
+    if constexpr (NPASS > 3) pass(IC<3>{});
+    static_assert(NPASS <= 4, "passes");
     __syncwarp();
     {
       const double2* src = reinterpret_cast<const double2*>(Spk);
@@ -542,7 +616,8 @@ __global__ void __launch_bounds__(32 * WPB, MINB)
     // resident (ds_reg.cuh): one sweep over the 8x8 pivot tiles of S_oo with
     // S_co and an identity block as right-hand sides, then Sd_T, X and
     // S_oo^-1 as X Y^T products of register tiles
-    {
+    if constexpr (DS) {
+      static_assert(!BIG, "phase D of the big degrees runs as its own kernel");
       auto S = [&](int a, int b) { return a >= b ? Spk[pk(a, b)] : Spk[pk(b, a)]; };
       if (!dsr::element<K>(S, U, ext + e * L::len, Sd + e * L::sd_len)) bad |= 2;
     }
@@ -556,13 +631,24 @@ __global__ void __launch_bounds__(32 * WPB, MINB)
 #define MCS_FZ_WPB4 12   // warps per CTA at k = 4 (tools/fused_prof.py sweeps it)
 #endif
 
-template <int K, int WPB, int MINB>
+template <int K, int WPB, int MINB, bool DS>
 static int launch_condense_fused(int64_t nt, const double* W, int nwgt, const double* tab,
                                  double* ST, double* ext, double* Sd, int* info,
                                  cudaStream_t st) {
   using G = fz::Geo<K>;
-  auto kern = condense_fused_kernel<K, WPB, MINB>;
-  const size_t smem = (G::TAB_SMEM + static_cast<size_t>(WPB) * G::PER_WARP) * sizeof(double);
+  auto kern = condense_fused_kernel<K, WPB, MINB, DS>;
+  const size_t smem =
+      ((G::BIG ? 0 : G::TAB_SMEM) + static_cast<size_t>(WPB) * G::PER_WARP) * sizeof(double);
+  double* gtab = nullptr;
+  if constexpr (G::BIG) {
+    // lane-ordered tables in a library-owned global buffer, rebuilt on the
+    // caller's stream at every call (concurrent calls with DIFFERENT tables
+    // for the same k on different streams are not supported)
+    static double* buf = nullptr;
+    if (!buf && cudaMalloc(&buf, G::TAB_SMEM * sizeof(double)) != cudaSuccess) return launch_status();
+    gtab = buf;
+    fused_lane_tables_kernel<K><<<16, 256, 0, st>>>(tab, gtab);
+  }
   cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   int per_sm = 0, dev = 0, nsm = 148;
   cudaGetDevice(&dev);
@@ -572,8 +658,18 @@ static int launch_condense_fused(int64_t nt, const double* W, int nwgt, const do
     per_sm = 1;
   const int64_t want = (nt + WPB - 1) / WPB, cap = static_cast<int64_t>(per_sm) * nsm;
   const int grid = static_cast<int>(want < cap ? want : cap);
-  kern<<<grid, 32 * WPB, smem, st>>>(W, nwgt, tab, ST, ext, Sd, info, nt);
+  kern<<<grid, 32 * WPB, smem, st>>>(W, nwgt, tab, gtab, ST, ext, Sd, info, nt);
   return launch_status();
+}
+
+// k = 5, 6 without the double Schur (mcs_condense_gen routes here)
+int launch_condense_fused_big(int k, int64_t nt, const double* W, int nwgt, const double* tab,
+                              double* ST, int* info, cudaStream_t st) {
+  switch (k) {
+    case 5: return launch_condense_fused<5, 4, 2, false>(nt, W, nwgt, tab, ST, nullptr, nullptr, info, st);
+    case 6: return launch_condense_fused<6, 4, 2, false>(nt, W, nwgt, tab, ST, nullptr, nullptr, info, st);
+  }
+  return -1000;
 }
 
 }  // namespace mcs
@@ -599,9 +695,9 @@ MCS_API int mcs_condense_fused(int k, int64_t nt, const double* W, int nwgt, con
   auto st = static_cast<cudaStream_t>(stream);
   switch (k) {
     // one CTA per SM: the compact tables once per CTA, one element per warp
-    case 2: return launch_condense_fused<2, 16, 1>(nt, W, nwgt, tables, S_packed, ext, Sd_packed, info, st);
-    case 3: return launch_condense_fused<3, 12, 1>(nt, W, nwgt, tables, S_packed, ext, Sd_packed, info, st);
-    case 4: return launch_condense_fused<4, MCS_FZ_WPB4, 1>(nt, W, nwgt, tables, S_packed, ext, Sd_packed, info, st);
+    case 2: return launch_condense_fused<2, 16, 1, true>(nt, W, nwgt, tables, S_packed, ext, Sd_packed, info, st);
+    case 3: return launch_condense_fused<3, 12, 1, true>(nt, W, nwgt, tables, S_packed, ext, Sd_packed, info, st);
+    case 4: return launch_condense_fused<4, MCS_FZ_WPB4, 1, true>(nt, W, nwgt, tables, S_packed, ext, Sd_packed, info, st);
   }
   return -1000;
 }

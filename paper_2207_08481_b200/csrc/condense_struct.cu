@@ -563,11 +563,20 @@ static int launch_condense_gen(const double* Wg, int nwgt, const double* tab, do
 
 using namespace mcs;
 
+namespace mcs {
+int launch_condense_fused_big(int k, int64_t nt, const double* W, int nwgt, const double* tab,
+                              double* ST, int* info, cudaStream_t st);
+}
+
 MCS_API int mcs_condense_gen(int k, int64_t nt, const double* W, int nwgt, const double* tables,
                              double* S_packed, int* info, void* stream) {
   if (nt <= 0) return 0;
   if (nwgt < 30) return -1000;
   auto st = static_cast<cudaStream_t>(stream);
+  // k = 5, 6: the warp-per-element fused pipeline in passes (condense_fused.cu);
+  // MCS_GEN=1: the CTA-per-element kernel of this file (A/B measurements)
+  static const int gen = getenv("MCS_GEN") ? atoi(getenv("MCS_GEN")) : 2;
+  if (k >= 5 && gen != 1) return launch_condense_fused_big(k, nt, W, nwgt, tables, S_packed, info, st);
   switch (k) {
     case 2: return launch_condense_gen<2, 4, 4>(W, nwgt, tables, S_packed, info, nt, st);
     case 3: return launch_condense_gen<3, 4, 4>(W, nwgt, tables, S_packed, info, nt, st);
