@@ -171,19 +171,29 @@ static int launch_double_schur_warp(const double* ST, double* ext, double* Sd, i
   return launch_dsw<K, WPB, 0>(ST, ext, Sd, info, nt, st);
 }
 
-// ---- register-resident warp-per-element kernel (ds_reg.cuh)
-template <int K, int WPB, int MINB>
+// ---- register-resident warp-per-element kernel (ds_reg.cuh).  PAIR: one
+// 8-warp CTA per SM, warps w and w + 4 (same SM sub-partition) in lockstep
+// through a named barrier before every pivot tile (dsr::sweep).
+template <int K, int WPB, int MINB, bool PAIR>
 __global__ void __launch_bounds__(32 * WPB, MINB)
     double_schur_reg(const double* __restrict__ ST, double* __restrict__ ext,
                      double* __restrict__ Sd, int* __restrict__ info, int64_t nt) {
   using G = dsr::Geo<K>;
   using L = ExtLayout<K>;
+  static_assert(!PAIR || WPB == 8, "pairs: warps w, w + 4 of an 8-warp CTA");
   extern __shared__ __align__(128) double smem[];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   double* T = smem + warp * G::PER_WARP;
   const int64_t nw = (int64_t)gridDim.x * WPB;
+  // every warp of the CTA runs the same number of rounds (the pair barriers);
+  // a warp past the end repeats the last element into its own scratch-free
+  // outputs (same values, harmless rewrite)
+  const int64_t e0 = (int64_t)blockIdx.x * WPB;
+  const int64_t rounds = e0 < nt ? (nt - e0 + nw - 1) / nw : 0;
 #pragma unroll 1
-  for (int64_t e = (int64_t)blockIdx.x * WPB + warp; e < nt; e += nw) {
+  for (int64_t rd = 0; rd < rounds; ++rd) {
+    const int64_t ew = e0 + warp + rd * nw;
+    const int64_t e = ew < nt ? ew : nt - 1;
     if (e + nw < nt) {                     // the next element's S_T into L2
       const char* nx = reinterpret_cast<const char*>(ST + (e + nw) * L::st_len);
       for (int off = lane * 128; off < L::st_len * 8; off += 32 * 128)
@@ -191,15 +201,19 @@ __global__ void __launch_bounds__(32 * WPB, MINB)
     }
     const double* S = ST + e * L::st_len;
     auto sym = [&](int a, int b) { return __ldg(S + (a >= b ? pk(a, b) : pk(b, a))); };
-    const bool ok = dsr::element<K>(sym, T, ext + e * L::len, Sd + e * L::sd_len);
+    bool ok;
+    if constexpr (PAIR)
+      ok = dsr::element<K>(sym, T, ext + e * L::len, Sd + e * L::sd_len, dsr::PairSync{1 + (warp & 3)});
+    else
+      ok = dsr::element<K>(sym, T, ext + e * L::len, Sd + e * L::sd_len);
     if (lane == 0 && info) info[e] = ok ? 0 : 1;
   }
 }
 
-template <int K, int WPB, int MINB>
+template <int K, int WPB, int MINB, bool PAIR>
 static int launch_double_schur_reg(const double* ST, double* ext, double* Sd, int* info,
                                    int64_t nt, cudaStream_t st) {
-  auto kern = double_schur_reg<K, WPB, MINB>;
+  auto kern = double_schur_reg<K, WPB, MINB, PAIR>;
   const size_t smem = (size_t)WPB * dsr::Geo<K>::PER_WARP * sizeof(double);
   cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   int per_sm = 0;
@@ -262,16 +276,18 @@ MCS_API int mcs_double_schur(int k, int64_t nt, const double* S_packed, double* 
   // MCS_DS=1: the shared-memory warp kernel (ds_warp.cuh), MCS_DS=5: the v5 CTA engine
   static const int ds = getenv("MCS_DS") ? atoi(getenv("MCS_DS")) : 2;
   if (ds == 2) {                            // register-resident kernel (ds_reg.cuh)
-    static const int occ = getenv("MCS_DSR_OCC") ? atoi(getenv("MCS_DSR_OCC")) : 0;
+    // MCS_DSR_PAIR=0: k = 5, 6 without the pair barriers (A/B measurements)
+    static const int pair = getenv("MCS_DSR_PAIR") ? atoi(getenv("MCS_DSR_PAIR")) : 1;
     switch (k) {
-      case 2: return launch_double_schur_reg<2, 4, 1>(S_packed, ext, Sd_packed, info, nt, st);
-      case 3: return launch_double_schur_reg<3, 4, 1>(S_packed, ext, Sd_packed, info, nt, st);
-      case 4: return launch_double_schur_reg<4, 4, 1>(S_packed, ext, Sd_packed, info, nt, st);
-      case 5: return launch_double_schur_reg<5, 4, 1>(S_packed, ext, Sd_packed, info, nt, st);
+      case 2: return launch_double_schur_reg<2, 4, 1, false>(S_packed, ext, Sd_packed, info, nt, st);
+      case 3: return launch_double_schur_reg<3, 4, 1, false>(S_packed, ext, Sd_packed, info, nt, st);
+      case 4: return launch_double_schur_reg<4, 4, 1, false>(S_packed, ext, Sd_packed, info, nt, st);
+      case 5:
+        if (pair) return launch_double_schur_reg<5, 8, 1, true>(S_packed, ext, Sd_packed, info, nt, st);
+        return launch_double_schur_reg<5, 4, 2, false>(S_packed, ext, Sd_packed, info, nt, st);
       case 6:
-        if (occ == 3) return launch_double_schur_reg<6, 4, 3>(S_packed, ext, Sd_packed, info, nt, st);
-        if (occ == 4) return launch_double_schur_reg<6, 4, 4>(S_packed, ext, Sd_packed, info, nt, st);
-        return launch_double_schur_reg<6, 4, 2>(S_packed, ext, Sd_packed, info, nt, st);
+        if (pair) return launch_double_schur_reg<6, 8, 1, true>(S_packed, ext, Sd_packed, info, nt, st);
+        return launch_double_schur_reg<6, 4, 2, false>(S_packed, ext, Sd_packed, info, nt, st);
     }
     return -1000;
   }

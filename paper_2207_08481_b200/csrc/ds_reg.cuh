@@ -45,26 +45,38 @@ __device__ __forceinline__ void mma_xyt(double2& c, double2 x, double2 y) {
   dmma884(c.x, c.y, x.x, y.x);
   dmma884(c.x, c.y, x.y, y.y);
 }
-__device__ __forceinline__ double2 neg2(double2 v) { return make_double2(-v.x, -v.y); }
 
 // Cholesky M M^T = Y of one SPD 8x8 tile in the row layout (lower triangle
 // significant) and M^-1, also in the row layout, by forward elimination of
-// the identity alongside.  The elimination chain needs only 1/d per pivot;
-// the scaling d^-1/2 feeds the M^-1 recurrence off the critical path.
+// the identity alongside.  The elimination needs only 1/d per pivot, and the
+// NEXT pivot d' = Y[p+1][p+1] - Y[p+1][p]^2 / d is formed ahead of the tile
+// update from two extra shuffles (the same fma the update performs, so the
+// value is bitwise the one the update leaves in the tile): the reciprocal
+// chain (fma -> rcp) and the update chain (shuffle -> fma) run side by side
+// instead of end to end.  The scaling d^-1/2 feeds the M^-1 recurrence off
+// the critical path.
 // bad: first non-positive pivot (1-based, offset by base), 0 if none yet.
 __device__ __forceinline__ double2 chol8m(double y0, double y1, int& bad, int base) {
   const int lane = threadIdx.x & 31, g = lane >> 2, t = lane & 3;
   double x0 = (g == 2 * t) ? 1.0 : 0.0, x1 = (g == 2 * t + 1) ? 1.0 : 0.0;
+  double d = __shfl_sync(0xffffffffu, y0, 0);
+  double r = rcp64(d);
 #pragma unroll
   for (int p = 0; p < 8; ++p) {
     const int sp = p >> 1;
     const double yp = (p & 1) ? y1 : y0;                   // Y[g][p] in lanes t == sp
-    const double d = __shfl_sync(0xffffffffu, yp, 4 * p + sp);
     const double yg = __shfl_sync(0xffffffffu, yp, 4 * g + sp);
     const double yc0 = __shfl_sync(0xffffffffu, yp, 8 * t + sp);
     const double yc1 = __shfl_sync(0xffffffffu, yp, 8 * t + 4 + sp);
+    double dn = 1.0, rn = 1.0;
+    if (p < 7) {
+      const double e = __shfl_sync(0xffffffffu, yp, 4 * (p + 1) + sp);
+      const double f = __shfl_sync(0xffffffffu, ((p + 1) & 1) ? y1 : y0, 4 * (p + 1) + ((p + 1) >> 1));
+      dn = fma(-(e * r), e, f);
+      rn = rcp64(dn);
+    }
     if (!(d > 0.0) && bad == 0) bad = base + p + 1;
-    const double w = yg * rcp64(d);
+    const double w = yg * r;
     y0 = fma(-w, yc0, y0);
     y1 = fma(-w, yc1, y1);
     const double sc = rsqrt_nr(d);
@@ -78,16 +90,110 @@ __device__ __forceinline__ double2 chol8m(double y0, double y1, int& bad, int ba
       x0 = fma(-mg, xp0, x0);
       x1 = fma(-mg, xp1, x1);
     }
+    d = dn;
+    r = rn;
   }
   return make_double2(x0, x1);
+}
+
+// no-op step hook of sweep()
+struct NoSync {
+  __device__ __forceinline__ void operator()(int) const {}
+};
+
+// The right-looking sweep over the NP pivot tiles of the SPD matrix A whose
+// lower tiles sit NEGATED in this lane's private slots Tl + q(i, j) * 64
+// (padding: -1 on the diagonal): with -A stored, the panel product yields
+// -L_ij, the only form the updates need, and no operand is ever negated.  bt[c][j]: the NCB x NP right-hand-side tiles, replaced by
+// W^T = B L^-T.  IT: also it[J][I] = (L^-T) tiles (I >= J) from an identity
+// right-hand side.  bad: first non-positive pivot (1-based), 0 if none.
+// named barrier over a pair of warps (ids 1..15; 0 is __syncthreads)
+struct PairSync {
+  int id;
+  __device__ __forceinline__ void operator()(int) const {
+    asm volatile("bar.sync %0, 64;" ::"r"(id) : "memory");
+  }
+};
+
+// sync(j) runs before pivot tile j is factorised: the kernels pair the two
+// warps of an SM sub-partition with a named barrier there, so that their
+// latency-bound factorisations coincide and their DMMA bursts share the
+// FP64 pipe (a warp streaming DMMAs starves a co-resident warp's dependent
+// FP64 chain: tools/dmma_prio.cu; unsynchronised, two warps serialise).
+template <int NP, int NCB, bool IT, class SY = NoSync>
+__device__ __forceinline__ void sweep(double* __restrict__ Tl, double2 (&bt)[NCB][NP],
+                                      double2 (&it)[IT ? NP : 1][IT ? NP : 1], int& bad,
+                                      SY sync = SY()) {
+  const int lane = threadIdx.x & 31, g = lane >> 2, t = lane & 3;
+  auto q = [](int i, int j) { return i * (i + 1) / 2 + j; };
+  if constexpr (IT) {
+#pragma unroll
+    for (int a = 0; a < NP; ++a)
+#pragma unroll
+      for (int b = 0; b < NP; ++b) it[a][b] = make_double2(0.0, 0.0);
+  }
+  const double2 eye = make_double2(g == 2 * t ? 1.0 : 0.0, g == 2 * t + 1 ? 1.0 : 0.0);
+#pragma unroll
+  for (int j = 0; j < NP; ++j) {
+    sync(j);
+    const double2 dj = *reinterpret_cast<const double2*>(Tl + q(j, j) * 64);
+    const double2 mi = chol8m(-dj.x, -dj.y, bad, 8 * j);   // M_j^-1
+    // panel: -L_ij = (-A_ij) M_j^-T
+    double2 ln[NP];
+#pragma unroll
+    for (int i = j + 1; i < NP; ++i) {
+      double2 o = make_double2(0.0, 0.0);
+      mma_xyt(o, *reinterpret_cast<const double2*>(Tl + q(i, j) * 64), mi);
+      ln[i] = o;
+    }
+    // the next diagonal tile first: its factorisation heads the critical path
+    if (j + 1 < NP) {
+      double2 c = *reinterpret_cast<const double2*>(Tl + q(j + 1, j + 1) * 64);
+      mma_xyt(c, ln[j + 1], ln[j + 1]);
+      *reinterpret_cast<double2*>(Tl + q(j + 1, j + 1) * 64) = c;
+    }
+    // right-hand sides: W^T_cj = B_cj M_j^-T, (L^-T)_Jj likewise (J <= j)
+#pragma unroll
+    for (int c = 0; c < NCB; ++c) {
+      double2 o = make_double2(0.0, 0.0);
+      mma_xyt(o, bt[c][j], mi);
+      bt[c][j] = o;
+    }
+    if constexpr (IT) {
+#pragma unroll
+      for (int J = 0; J <= j; ++J) {
+        double2 o = make_double2(0.0, 0.0);
+        mma_xyt(o, J == j ? eye : it[J][j], mi);
+        it[J][j] = o;
+      }
+    }
+    // trailing updates with column j: -A_ik += (-L_ij) (-L_kj)^T
+#pragma unroll
+    for (int i = j + 1; i < NP; ++i) {
+#pragma unroll
+      for (int k = j + 1; k <= i; ++k) {
+        if (i == j + 1 && k == j + 1) continue;            // done above
+        double2 c = *reinterpret_cast<const double2*>(Tl + q(i, k) * 64);
+        mma_xyt(c, ln[i], ln[k]);
+        *reinterpret_cast<double2*>(Tl + q(i, k) * 64) = c;
+      }
+#pragma unroll
+      for (int c = 0; c < NCB; ++c) mma_xyt(bt[c][i], bt[c][j], ln[i]);
+      if constexpr (IT) {
+#pragma unroll
+        for (int J = 0; J <= j; ++J) mma_xyt(it[J][i], it[J][j], ln[i]);
+      }
+    }
+  }
 }
 
 // One element.  sym(a, b): entry (a, b) of the symmetric S_T (global or
 // shared memory); T: this warp's NT private tile slots (16-byte aligned).
 // Returns false if S_oo is not positive definite.
-template <int K, class SYM>
+template <int K, class SYM, class SY = NoSync>
 __device__ __forceinline__ bool element(SYM sym, double* __restrict__ T,
-                                        double* __restrict__ xo, double* __restrict__ so) {
+                                        double* __restrict__ xo, double* __restrict__ so,
+                                        SY sync = SY()) {
   using G = Geo<K>;
   using L = ExtLayout<K>;
   constexpr int NI = G::NI, NC = G::NC, NEM = G::NEM, NP = G::NP, NCB = G::NCB;
@@ -115,68 +221,14 @@ __device__ __forceinline__ bool element(SYM sym, double* __restrict__ T,
     for (int j = 0; j <= i; ++j) {
       const int r = 8 * i + g, c0 = 8 * j + 2 * t;
       double2 v;
-      v.x = (r < NI && c0 < NI) ? sym(NEM + r, NEM + c0) : (r == c0 ? 1.0 : 0.0);
-      v.y = (r < NI && c0 + 1 < NI) ? sym(NEM + r, NEM + c0 + 1) : (r == c0 + 1 ? 1.0 : 0.0);
+      v.x = (r < NI && c0 < NI) ? -sym(NEM + r, NEM + c0) : (r == c0 ? -1.0 : 0.0);
+      v.y = (r < NI && c0 + 1 < NI) ? -sym(NEM + r, NEM + c0 + 1) : (r == c0 + 1 ? -1.0 : 0.0);
       *reinterpret_cast<double2*>(Tl + G::q(i, j) * 64) = v;
     }
 
   double2 it[NP][NP];
-#pragma unroll
-  for (int a = 0; a < NP; ++a)
-#pragma unroll
-    for (int b = 0; b < NP; ++b) it[a][b] = make_double2(0.0, 0.0);
-  const double2 eye = make_double2(g == 2 * t ? 1.0 : 0.0, g == 2 * t + 1 ? 1.0 : 0.0);
   int bad = 0;
-
-  // ---- the sweep over the pivot tiles
-#pragma unroll
-  for (int j = 0; j < NP; ++j) {
-    const double2 dj = *reinterpret_cast<const double2*>(Tl + G::q(j, j) * 64);
-    const double2 mi = chol8m(dj.x, dj.y, bad, 8 * j);     // M_j^-1
-    // panel L_ij = A_ij M_j^-T (kept negated for the updates)
-    double2 l[NP], ln[NP];
-#pragma unroll
-    for (int i = j + 1; i < NP; ++i) {
-      double2 o = make_double2(0.0, 0.0);
-      mma_xyt(o, *reinterpret_cast<const double2*>(Tl + G::q(i, j) * 64), mi);
-      l[i] = o;
-      ln[i] = neg2(o);
-    }
-    // the next diagonal tile first: its factorisation heads the critical path
-    if (j + 1 < NP) {
-      double2 c = *reinterpret_cast<const double2*>(Tl + G::q(j + 1, j + 1) * 64);
-      mma_xyt(c, ln[j + 1], l[j + 1]);
-      *reinterpret_cast<double2*>(Tl + G::q(j + 1, j + 1) * 64) = c;
-    }
-    // right-hand sides: W^T_cj = B_cj M_j^-T, (L^-T)_Jj likewise (J <= j)
-#pragma unroll
-    for (int c = 0; c < NCB; ++c) {
-      double2 o = make_double2(0.0, 0.0);
-      mma_xyt(o, bt[c][j], mi);
-      bt[c][j] = o;
-    }
-#pragma unroll
-    for (int J = 0; J <= j; ++J) {
-      double2 o = make_double2(0.0, 0.0);
-      mma_xyt(o, J == j ? eye : it[J][j], mi);
-      it[J][j] = o;
-    }
-    // trailing updates with column j
-#pragma unroll
-    for (int i = j + 1; i < NP; ++i) {
-#pragma unroll
-      for (int k = j + 1; k <= i; ++k) {
-        if (i == j + 1 && k == j + 1) continue;            // done above
-        double2 c = *reinterpret_cast<const double2*>(Tl + G::q(i, k) * 64);
-        mma_xyt(c, ln[i], l[k]);
-        *reinterpret_cast<double2*>(Tl + G::q(i, k) * 64) = c;
-      }
-#pragma unroll
-      for (int c = 0; c < NCB; ++c) mma_xyt(bt[c][i], bt[c][j], ln[i]);
-#pragma unroll
-      for (int J = 0; J <= j; ++J) mma_xyt(it[J][i], it[J][j], ln[i]);
-    }
-  }
+  sweep<NP, NCB, true>(Tl, bt, it, bad, sync);
 
   // ---- Sd_T = S_cc - W^T W (lower tiles), S_cc loaded ahead of each chain
 #pragma unroll

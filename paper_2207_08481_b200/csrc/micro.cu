@@ -29,6 +29,7 @@
 // during phase 1, so the HBM traffic overlaps the arithmetic.
 #include <cstdlib>
 
+#include "ds_reg.cuh"
 #include "elim_v5.cuh"
 
 #ifndef MCS_MICRO_YM
@@ -429,6 +430,90 @@ __global__ void __launch_bounds__(64, 6)
   }
 }
 
+// ---- one warp per element, register resident (the sweep of ds_reg.cuh):
+// B^T lives in registers in the DMMA row layout and becomes W^T = B^T L^-T
+// under the right-looking sweep over the 8x8 pivot tiles of A; the trailing
+// part of A sits in per-lane private shared-memory slots (no barrier, no
+// warp synchronisation); S = W^T W is formed from the register tiles.  The
+// next element's A and B are pulled into L2 while this one is eliminated.
+// PAIR: warps w and w + 4 of the 8-warp CTA (same SM sub-partition) meet at
+// a named barrier before every pivot tile, so their 8x8 factorisations run
+// together and their DMMA bursts share the pipe (see dsr::sweep).
+using dsr::PairSync;
+
+template <int NS, int NC, int WPB, int MINB, bool PAIR>
+__global__ void __launch_bounds__(32 * WPB, MINB)
+    spd_schur_w1(const double* __restrict__ A, const double* __restrict__ B,
+                 double* __restrict__ S, int* __restrict__ info, int64_t batch) {
+  using G = Geo<NS, NC>;
+  constexpr int NP = G::NP, NCB = G::NCB, LA = G::LA;
+  extern __shared__ __align__(128) double smem[];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, g = lane >> 2, t = lane & 3;
+  double* Tl = smem + warp * (G::NT * 64) + 2 * lane;
+  static_assert(!PAIR || WPB == 8, "pairs: warps w, w + 4 of an 8-warp CTA");
+  const int64_t nw = (int64_t)gridDim.x * WPB;
+  // every warp of the CTA runs the same number of rounds (the pair barriers);
+  // a warp past the end repeats the last element without storing
+  const int64_t e0 = (int64_t)blockIdx.x * WPB;
+  const int64_t rounds = e0 < batch ? (batch - e0 + nw - 1) / nw : 0;
+#pragma unroll 1
+  for (int64_t rd = 0; rd < rounds; ++rd) {
+    const int64_t ew = e0 + warp + rd * nw;
+    const bool live = ew < batch;
+    const int64_t e = live ? ew : batch - 1;
+    if (e + nw < batch) {
+      const char* na = reinterpret_cast<const char*>(A + (e + nw) * LA);
+      for (int off = lane * 128; off < LA * 8; off += 32 * 128)
+        asm volatile("prefetch.global.L2 [%0];" ::"l"(na + off));
+      const char* nb = reinterpret_cast<const char*>(B + (e + nw) * (int64_t)(NS * NC));
+      for (int off = lane * 128; off < NS * NC * 8; off += 32 * 128)
+        asm volatile("prefetch.global.L2 [%0];" ::"l"(nb + off));
+    }
+    const double* Ae = A + e * LA;
+    const double* Be = B + e * (int64_t)(NS * NC);
+#pragma unroll
+    for (int i = 0; i < NP; ++i)
+#pragma unroll
+      for (int j = 0; j <= i; ++j) {
+        const int r = 8 * i + g, c0 = 8 * j + 2 * t;
+        double2 v;
+        v.x = (r < NS && c0 < NS) ? -__ldg(Ae + (r >= c0 ? pk(r, c0) : pk(c0, r))) : (r == c0 ? -1.0 : 0.0);
+        v.y = (r < NS && c0 + 1 < NS) ? -__ldg(Ae + (r >= c0 + 1 ? pk(r, c0 + 1) : pk(c0 + 1, r)))
+                                      : (r == c0 + 1 ? -1.0 : 0.0);   // the slots hold -A
+        *reinterpret_cast<double2*>(Tl + G::q(i, j) * 64) = v;
+      }
+    double2 bt[NCB][NP];
+#pragma unroll
+    for (int c = 0; c < NCB; ++c)
+#pragma unroll
+      for (int i = 0; i < NP; ++i) bt[c][i] = load_bt<NS, NC>(Be, c, i);
+    int bad = 0;
+    double2 none[1][1];
+    if constexpr (PAIR)
+      dsr::sweep<NP, NCB, false>(Tl, bt, none, bad, PairSync{1 + (warp & 3)});
+    else
+      dsr::sweep<NP, NCB, false>(Tl, bt, none, bad);
+    if (!live) continue;
+    double* Se = S + e * (int64_t)(NC * (NC + 1) / 2);
+#pragma unroll
+    for (int c = 0; c < NCB; ++c) {
+      const int row = 8 * c + g;
+#pragma unroll
+      for (int d = 0; d <= c; ++d) {
+        double2 o = make_double2(0.0, 0.0);
+#pragma unroll
+        for (int j = 0; j < NP; ++j) dsr::mma_xyt(o, bt[c][j], bt[d][j]);
+        const int col = 8 * d + 2 * t;
+        if (row < NC) {
+          if (col <= row) Se[row * (row + 1) / 2 + col] = o.x;
+          if (col + 1 <= row) Se[row * (row + 1) / 2 + col + 1] = o.y;
+        }
+      }
+    }
+    if (lane == 0 && info) info[e] = bad;
+  }
+}
+
 }  // namespace micro
 
 template <int NS, int NC, int YM>
@@ -451,6 +536,22 @@ template <int NS, int NC>
 int launch_spd_schur_w2(const double* A, const double* B, double* S, int* info, int64_t batch,
                         cudaStream_t st) {
   // MCS_MICRO_YIELD = throttle mask (A/B measurements; default MCS_MICRO_YM)
+  // default: one warp per element, register resident; MCS_MICRO=2: the
+  // two-warp kernel (and its MCS_MICRO_YIELD throttle variants)
+  static const int mv = getenv("MCS_MICRO") ? atoi(getenv("MCS_MICRO")) : 1;
+  if (mv != 2) {
+    // MCS_MICRO=3: the same kernel without the pair barriers (A/B)
+    auto kern = mv == 3 ? micro::spd_schur_w1<NS, NC, 8, 1, false> : micro::spd_schur_w1<NS, NC, 8, 1, true>;
+    const size_t smem = (size_t)8 * micro::Geo<NS, NC>::NT * 64 * sizeof(double);
+    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    int per_sm = 0;
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, 256, smem) != cudaSuccess ||
+        per_sm < 1)
+      per_sm = 1;
+    const int64_t want = (batch + 7) / 8, cap = (int64_t)per_sm * sm_count();
+    kern<<<(int)(want < cap ? want : cap), 256, smem, st>>>(A, B, S, info, batch);
+    return launch_status();
+  }
   static const int ym = getenv("MCS_MICRO_YIELD") ? atoi(getenv("MCS_MICRO_YIELD")) : MCS_MICRO_YM;
   switch (ym) {
     case 1: return launch_w2<NS, NC, 1>(A, B, S, info, batch, st);
