@@ -52,6 +52,10 @@ __device__ unsigned long long g_fz_prof[8];
 #define FZ_T(i)
 #endif
 
+#ifndef MCS_FZ_CPP4
+#define MCS_FZ_CPP4 4   // Y column chunks per pass at k = 4 (4 = one pass; tools/fused_prof.py sweeps it)
+#endif
+
 namespace fz {
 
 constexpr int W_MSIG = 0, W_ADIV = 27, NWS = 36;   // weight slots (refblocks.py), 30.. = 0
@@ -137,7 +141,7 @@ struct Geo {
   // phase-A factors alias the packed S_T (dead until the first pass ends),
   // G has its own slot (it lives across the passes)
   static constexpr bool BIG = K >= 5;
-  static constexpr int CPP = BIG ? 3 : NKC;
+  static constexpr int CPP = BIG ? 3 : (K == 4 ? MCS_FZ_CPP4 : NKC);
   static constexpr int NPASS = (NKC + CPP - 1) / CPP;
   static constexpr int NG = 6 * ml * 2;               // G[edge group][m][s]
   // per-warp shared memory (doubles)

@@ -17,11 +17,12 @@ from paper_2207_08481_b200.dofmap import FeSystem  # noqa: E402
 from paper_2207_08481_b200.problems import baseline_config  # noqa: E402
 
 WPB = int(os.environ.get("WPB", "12"))
-so = os.path.join(ROOT, "tools", f"_fused_prof_{WPB}.so")
+CPP = int(os.environ.get("CPP", "4"))
+so = os.path.join(ROOT, "tools", f"_fused_prof_{WPB}_{CPP}.so")
 csrc = os.path.join(ROOT, "paper_2207_08481_b200", "csrc")
 if not os.path.exists(so):
     subprocess.check_call(["nvcc", "-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-std=c++17",
-                           "-Xcompiler", "-fPIC", "-shared", "-DMCS_FUSED_PROF", f"-DMCS_FZ_WPB4={WPB}", "-I", csrc, "-I",
+                           "-Xcompiler", "-fPIC", "-shared", "-DMCS_FUSED_PROF", f"-DMCS_FZ_WPB4={WPB}", f"-DMCS_FZ_CPP4={CPP}", "-I", csrc, "-I",
                            os.path.join(ROOT, "include"), "--expt-relaxed-constexpr",
                            os.path.join(csrc, "condense_fused.cu"), "-o", so])
 lib = ctypes.CDLL(so)
