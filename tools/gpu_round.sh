@@ -9,7 +9,7 @@ timeout 1200 python bench.py > gpurun_out/bench_$TAG.json 2> gpurun_out/bench_$T
 if [ -n "$NCU" ]; then
 export MCS_NO_GRAPH=1
 timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --csv --log-file gpurun_out/launches_$TAG.csv python bench.py --steps 2 --warmup 3 --no-micro --no-stokes --no-cfg3 --no-cpu-solver --cpu-sample 8 > gpurun_out/ncu_launch_$TAG.log 2>&1
-timeout 900 ncu --set full --import-source on --clock-control none -k "regex:(condense_fused|spd_schur_w2|elem_apply|ext_restrict|ext_prolong|jacobi_apply|mf_forward|mf_top_solve|cg_update)" -c 12 -o gpurun_out/full_$TAG python tools/prof_kernels.py all > gpurun_out/ncu_full_$TAG.log 2>&1
+timeout 900 ncu --set full --import-source on --clock-control none -k "regex:(condense_fused|spd_schur_w1|elem_apply|ext_restrict|ext_prolong|jacobi_apply|mf_forward|mf_top_solve|cg_update)" -c 12 -o gpurun_out/full_$TAG python tools/prof_kernels.py all > gpurun_out/ncu_full_$TAG.log 2>&1
 timeout 600 ncu --set full --import-source on --clock-control none -k "regex:(condense_fused_kernel|double_schur_reg)" -c 2 -o gpurun_out/full_ds_$TAG python tools/prof_kernels.py ds > gpurun_out/ncu_full_ds_$TAG.log 2>&1
 fi
 tail -3 gpurun_out/pytest_gpu_$TAG.log; tail -2 gpurun_out/smoke_$TAG.log; tail -2 gpurun_out/bench_$TAG.err
