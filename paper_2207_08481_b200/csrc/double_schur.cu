@@ -177,7 +177,7 @@ static int launch_double_schur_warp(const double* ST, double* ext, double* Sd, i
 template <int K, int WPB, int MINB, bool PAIR>
 __global__ void __launch_bounds__(32 * WPB, MINB)
     double_schur_reg(const double* __restrict__ ST, double* __restrict__ ext,
-                     double* __restrict__ Sd, int* __restrict__ info, int64_t nt) {
+                     double* __restrict__ Sd, int* __restrict__ info, int64_t nt, int pf) {
   using G = dsr::Geo<K>;
   using L = ExtLayout<K>;
   static_assert(!PAIR || WPB == 8, "pairs: warps w, w + 4 of an 8-warp CTA");
@@ -194,7 +194,7 @@ __global__ void __launch_bounds__(32 * WPB, MINB)
   for (int64_t rd = 0; rd < rounds; ++rd) {
     const int64_t ew = e0 + warp + rd * nw;
     const int64_t e = ew < nt ? ew : nt - 1;
-    if (e + nw < nt) {                     // the next element's S_T into L2
+    if (pf && e + nw < nt) {               // the next element's S_T into L2
       const char* nx = reinterpret_cast<const char*>(ST + (e + nw) * L::st_len);
       for (int off = lane * 128; off < L::st_len * 8; off += 32 * 128)
         asm volatile("prefetch.global.L2 [%0];" ::"l"(nx + off));
@@ -221,7 +221,8 @@ static int launch_double_schur_reg(const double* ST, double* ext, double* Sd, in
       per_sm < 1)
     per_sm = 1;
   const int64_t want = (nt + WPB - 1) / WPB, cap = (int64_t)per_sm * sm_count();
-  kern<<<(int)(want < cap ? want : cap), 32 * WPB, smem, st>>>(ST, ext, Sd, info, nt);
+  static const int pf = getenv("MCS_DSR_PF") ? atoi(getenv("MCS_DSR_PF")) : 0;   // 1: L2 prefetch of the next S_T (same time, 1.4x the DRAM reads)
+  kern<<<(int)(want < cap ? want : cap), 32 * WPB, smem, st>>>(ST, ext, Sd, info, nt, pf);
   return launch_status();
 }
 

@@ -434,8 +434,7 @@ __global__ void __launch_bounds__(64, 6)
 // B^T lives in registers in the DMMA row layout and becomes W^T = B^T L^-T
 // under the right-looking sweep over the 8x8 pivot tiles of A; the trailing
 // part of A sits in per-lane private shared-memory slots (no barrier, no
-// warp synchronisation); S = W^T W is formed from the register tiles.  The
-// next element's A and B are pulled into L2 while this one is eliminated.
+// warp synchronisation); S = W^T W is formed from the register tiles.
 // PAIR: warps w and w + 4 of the 8-warp CTA (same SM sub-partition) meet at
 // a named barrier before every pivot tile, so their 8x8 factorisations run
 // together and their DMMA bursts share the pipe (see dsr::sweep).
@@ -444,7 +443,7 @@ using dsr::PairSync;
 template <int NS, int NC, int WPB, int MINB, bool PAIR>
 __global__ void __launch_bounds__(32 * WPB, MINB)
     spd_schur_w1(const double* __restrict__ A, const double* __restrict__ B,
-                 double* __restrict__ S, int* __restrict__ info, int64_t batch) {
+                 double* __restrict__ S, int* __restrict__ info, int64_t batch, int pf) {
   using G = Geo<NS, NC>;
   constexpr int NP = G::NP, NCB = G::NCB, LA = G::LA;
   extern __shared__ __align__(128) double smem[];
@@ -461,7 +460,7 @@ __global__ void __launch_bounds__(32 * WPB, MINB)
     const int64_t ew = e0 + warp + rd * nw;
     const bool live = ew < batch;
     const int64_t e = live ? ew : batch - 1;
-    if (e + nw < batch) {
+    if (pf && e + nw < batch) {
       const char* na = reinterpret_cast<const char*>(A + (e + nw) * LA);
       for (int off = lane * 128; off < LA * 8; off += 32 * 128)
         asm volatile("prefetch.global.L2 [%0];" ::"l"(na + off));
@@ -549,7 +548,8 @@ int launch_spd_schur_w2(const double* A, const double* B, double* S, int* info, 
         per_sm < 1)
       per_sm = 1;
     const int64_t want = (batch + 7) / 8, cap = (int64_t)per_sm * sm_count();
-    kern<<<(int)(want < cap ? want : cap), 256, smem, st>>>(A, B, S, info, batch);
+    static const int pf = getenv("MCS_MICRO_PF") ? atoi(getenv("MCS_MICRO_PF")) : 0;   // 1: L2 prefetch of the next element (measured slower: L2 thrash, 1.6x the DRAM reads)
+    kern<<<(int)(want < cap ? want : cap), 256, smem, st>>>(A, B, S, info, batch, pf);
     return launch_status();
   }
   static const int ym = getenv("MCS_MICRO_YIELD") ? atoi(getenv("MCS_MICRO_YIELD")) : MCS_MICRO_YM;
