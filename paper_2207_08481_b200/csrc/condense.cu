@@ -232,7 +232,7 @@ MCS_API int mcs_spd_schur_batched(int n, int m, int64_t batch, const double* A_p
   if (batch <= 0) return 0;
   auto st = static_cast<cudaStream_t>(stream);
   // default: the one-warp register-resident kernel of micro.cu (MCS_MICRO=2: its
-  // two-warp kernel, 3: one warp without the pair barriers); MCS_MICRO=5: the v5 engine
+  // two-warp kernel, 3: one warp per element with pair barriers); MCS_MICRO=5: the v5 engine
   static const int which = getenv("MCS_MICRO") ? atoi(getenv("MCS_MICRO")) : 1;
   if (n == 60 && m == 36) {
     if (which == 5) return launch_spd_schur_v5<60, 36, 4, 5>(A_packed_lower, B, S_packed, info, batch, st);

@@ -47,16 +47,61 @@ __device__ __forceinline__ void mma_xyt(double2& c, double2 x, double2 y) {
 }
 
 // Cholesky M M^T = Y of one SPD 8x8 tile in the row layout (lower triangle
-// significant) and M^-1, also in the row layout, by forward elimination of
-// the identity alongside.  The elimination needs only 1/d per pivot, and the
-// NEXT pivot d' = Y[p+1][p+1] - Y[p+1][p]^2 / d is formed ahead of the tile
-// update from two extra shuffles (the same fma the update performs, so the
-// value is bitwise the one the update leaves in the tile): the reciprocal
-// chain (fma -> rcp) and the update chain (shuffle -> fma) run side by side
-// instead of end to end.  The scaling d^-1/2 feeds the M^-1 recurrence off
-// the critical path.
+// significant), returned as M^-1 in the row layout.  With Y = Lu D Lu^T (Lu
+// unit lower), M^-1 = D^-1/2 Lu^-1: the elimination of the tile and the
+// forward elimination of an identity (-> Lu^-1) share the multipliers
+// w = Y[g][p] / d_p, so a pivot costs one reciprocal, one multiply and four
+// fmas per lane; the row scaling d_g^-1/2 is ONE rsqrt per lane at the end
+// (lane (g, t) keeps the pivot of its own row).  The NEXT pivot
+// d' = Y[p+1][p+1] - Y[p+1][p]^2 / d is formed ahead of the tile update from
+// two extra shuffles (the same fma the update performs, so the value is
+// bitwise the one the update leaves in the tile): the reciprocal chain
+// (fma -> rcp) and the update chain (shuffle -> fma) run side by side
+// instead of end to end.
 // bad: first non-positive pivot (1-based, offset by base), 0 if none yet.
 __device__ __forceinline__ double2 chol8m(double y0, double y1, int& bad, int base) {
+  const int lane = threadIdx.x & 31, g = lane >> 2, t = lane & 3;
+  double x0 = (g == 2 * t) ? 1.0 : 0.0, x1 = (g == 2 * t + 1) ? 1.0 : 0.0;
+  double d = __shfl_sync(0xffffffffu, y0, 0);
+  double r = rcp64(d);
+  double dg = 1.0;                                         // the pivot of row g
+#pragma unroll
+  for (int p = 0; p < 8; ++p) {
+    const int sp = p >> 1;
+    const double yp = (p & 1) ? y1 : y0;                   // Y[g][p] in lanes t == sp
+    const double yg = __shfl_sync(0xffffffffu, yp, 4 * g + sp);
+    const double yc0 = __shfl_sync(0xffffffffu, yp, 8 * t + sp);
+    const double yc1 = __shfl_sync(0xffffffffu, yp, 8 * t + 4 + sp);
+    double dn = 1.0, rn = 1.0;
+    if (p < 7) {
+      const double e = __shfl_sync(0xffffffffu, yp, 4 * (p + 1) + sp);
+      const double f = __shfl_sync(0xffffffffu, ((p + 1) & 1) ? y1 : y0, 4 * (p + 1) + ((p + 1) >> 1));
+      dn = fma(-(e * r), e, f);
+      rn = rcp64(dn);
+    }
+    if (!(d > 0.0) && bad == 0) bad = base + p + 1;
+    dg = (g == p) ? d : dg;
+    const double w = yg * r;                               // Lu[g][p]
+    y0 = fma(-w, yc0, y0);
+    y1 = fma(-w, yc1, y1);
+    const double xp0 = __shfl_sync(0xffffffffu, x0, 4 * p + t);
+    const double xp1 = __shfl_sync(0xffffffffu, x1, 4 * p + t);
+    if (g > p) {
+      x0 = fma(-w, xp0, x0);
+      x1 = fma(-w, xp1, x1);
+    }
+    d = dn;
+    r = rn;
+  }
+  const double sc = rsqrt_nr(dg);
+  return make_double2(x0 * sc, x1 * sc);
+}
+
+// Variant with the scaling d^-1/2 taken per pivot inside the loop (eight
+// rsqrt per tile, twice the FP64 instructions, but no rsqrt after the last
+// pivot): measured faster in the k = 5, 6 double Schur, slower in the fused
+// kernel and the microbench.
+__device__ __forceinline__ double2 chol8m_rs(double y0, double y1, int& bad, int base) {
   const int lane = threadIdx.x & 31, g = lane >> 2, t = lane & 3;
   double x0 = (g == 2 * t) ? 1.0 : 0.0, x1 = (g == 2 * t + 1) ? 1.0 : 0.0;
   double d = __shfl_sync(0xffffffffu, y0, 0);
@@ -120,7 +165,7 @@ struct PairSync {
 // latency-bound factorisations coincide and their DMMA bursts share the
 // FP64 pipe (a warp streaming DMMAs starves a co-resident warp's dependent
 // FP64 chain: tools/dmma_prio.cu; unsynchronised, two warps serialise).
-template <int NP, int NCB, bool IT, class SY = NoSync>
+template <int NP, int NCB, bool IT, class SY = NoSync, bool RS = false>
 __device__ __forceinline__ void sweep(double* __restrict__ Tl, double2 (&bt)[NCB][NP],
                                       double2 (&it)[IT ? NP : 1][IT ? NP : 1], int& bad,
                                       SY sync = SY()) {
@@ -137,7 +182,8 @@ __device__ __forceinline__ void sweep(double* __restrict__ Tl, double2 (&bt)[NCB
   for (int j = 0; j < NP; ++j) {
     sync(j);
     const double2 dj = *reinterpret_cast<const double2*>(Tl + q(j, j) * 64);
-    const double2 mi = chol8m(-dj.x, -dj.y, bad, 8 * j);   // M_j^-1
+    const double2 mi = RS ? chol8m_rs(-dj.x, -dj.y, bad, 8 * j)
+                          : chol8m(-dj.x, -dj.y, bad, 8 * j);   // M_j^-1
     // panel: -L_ij = (-A_ij) M_j^-T
     double2 ln[NP];
 #pragma unroll
@@ -190,7 +236,7 @@ __device__ __forceinline__ void sweep(double* __restrict__ Tl, double2 (&bt)[NCB
 // One element.  sym(a, b): entry (a, b) of the symmetric S_T (global or
 // shared memory); T: this warp's NT private tile slots (16-byte aligned).
 // Returns false if S_oo is not positive definite.
-template <int K, class SYM, class SY = NoSync>
+template <int K, class SYM, class SY = NoSync, bool RS = false>
 __device__ __forceinline__ bool element(SYM sym, double* __restrict__ T,
                                         double* __restrict__ xo, double* __restrict__ so,
                                         SY sync = SY()) {
@@ -228,7 +274,7 @@ __device__ __forceinline__ bool element(SYM sym, double* __restrict__ T,
 
   double2 it[NP][NP];
   int bad = 0;
-  sweep<NP, NCB, true>(Tl, bt, it, bad, sync);
+  sweep<NP, NCB, true, SY, RS>(Tl, bt, it, bad, sync);
 
   // ---- Sd_T = S_cc - W^T W (lower tiles), S_cc loaded ahead of each chain
 #pragma unroll

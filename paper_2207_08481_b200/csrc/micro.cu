@@ -539,8 +539,9 @@ int launch_spd_schur_w2(const double* A, const double* B, double* S, int* info, 
   // two-warp kernel (and its MCS_MICRO_YIELD throttle variants)
   static const int mv = getenv("MCS_MICRO") ? atoi(getenv("MCS_MICRO")) : 1;
   if (mv != 2) {
-    // MCS_MICRO=3: the same kernel without the pair barriers (A/B)
-    auto kern = mv == 3 ? micro::spd_schur_w1<NS, NC, 8, 1, false> : micro::spd_schur_w1<NS, NC, 8, 1, true>;
+    // MCS_MICRO=3: the same kernel with the pair barriers (A/B: +5% with the
+    // rsqrt-per-pivot factorisation, -1% with the current one)
+    auto kern = mv == 3 ? micro::spd_schur_w1<NS, NC, 8, 1, true> : micro::spd_schur_w1<NS, NC, 8, 1, false>;
     const size_t smem = (size_t)8 * micro::Geo<NS, NC>::NT * 64 * sizeof(double);
     cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     int per_sm = 0;
