@@ -621,9 +621,19 @@ __global__ void __launch_bounds__(32 * WPB, MINB)
     // S_co and an identity block as right-hand sides, then Sd_T, X and
     // S_oo^-1 as X Y^T products of register tiles
     if constexpr (DS) {
-      static_assert(!BIG, "phase D of the big degrees runs as its own kernel");
       auto S = [&](int a, int b) { return a >= b ? Spk[pk(a, b)] : Spk[pk(b, a)]; };
-      if (!dsr::element<K>(S, U, ext + e * L::len, Sd + e * L::sd_len)) bad |= 2;
+      if constexpr (BIG) {
+        // the tile slots over the interior rows of the packed S_T: S_oo and
+        // S_co are in registers before the first slot is written, S_cc (read
+        // last) lies in the rows before and after them
+        constexpr int T0 = even(pk(G::NEM, 0));
+        static_assert(T0 + dsr::Geo<K>::PER_WARP <= pk(G::NEM + G::NI, 0), "slots inside the interior rows");
+        if (!dsr::element<K, decltype(S), dsr::NoSync, true, true>(S, Spk + T0, ext + e * L::len,
+                                                                   Sd + e * L::sd_len))
+          bad |= 2;
+      } else {
+        if (!dsr::element<K>(S, U, ext + e * L::len, Sd + e * L::sd_len)) bad |= 2;
+      }
     }
     FZ_T(3);
     if (lane == 0 && info) info[e] = bad;
@@ -702,6 +712,9 @@ MCS_API int mcs_condense_fused(int k, int64_t nt, const double* W, int nwgt, con
     case 2: return launch_condense_fused<2, 16, 1, true>(nt, W, nwgt, tables, S_packed, ext, Sd_packed, info, st);
     case 3: return launch_condense_fused<3, 12, 1, true>(nt, W, nwgt, tables, S_packed, ext, Sd_packed, info, st);
     case 4: return launch_condense_fused<4, MCS_FZ_WPB4, 1, true>(nt, W, nwgt, tables, S_packed, ext, Sd_packed, info, st);
+    // k = 5, 6: the passes pipeline with the double Schur as phase D
+    case 5: return launch_condense_fused<5, 4, 2, true>(nt, W, nwgt, tables, S_packed, ext, Sd_packed, info, st);
+    case 6: return launch_condense_fused<6, 4, 2, true>(nt, W, nwgt, tables, S_packed, ext, Sd_packed, info, st);
   }
   return -1000;
 }

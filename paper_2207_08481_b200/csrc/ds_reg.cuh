@@ -236,7 +236,11 @@ __device__ __forceinline__ void sweep(double* __restrict__ Tl, double2 (&bt)[NCB
 // One element.  sym(a, b): entry (a, b) of the symmetric S_T (global or
 // shared memory); T: this warp's NT private tile slots (16-byte aligned).
 // Returns false if S_oo is not positive definite.
-template <int K, class SYM, class SY = NoSync, bool RS = false>
+// ALIAS: the tile slots T overlap memory that sym() reads for S_oo and S_co
+// (the fused k = 5, 6 kernel puts them over the interior rows of the packed
+// S_T): every such entry is loaded into registers before the first slot is
+// written.  The S_cc entries read at the end must lie outside T.
+template <int K, class SYM, class SY = NoSync, bool RS = false, bool ALIAS = false>
 __device__ __forceinline__ bool element(SYM sym, double* __restrict__ T,
                                         double* __restrict__ xo, double* __restrict__ so,
                                         SY sync = SY()) {
@@ -261,6 +265,22 @@ __device__ __forceinline__ bool element(SYM sym, double* __restrict__ T,
       bt[c][i] = v;
     }
   }
+  if constexpr (ALIAS) {
+    double2 a0[G::NT];
+#pragma unroll
+    for (int i = 0; i < NP; ++i)
+#pragma unroll
+      for (int j = 0; j <= i; ++j) {
+        const int r = 8 * i + g, c0 = 8 * j + 2 * t;
+        double2 v;
+        v.x = (r < NI && c0 < NI) ? -sym(NEM + r, NEM + c0) : (r == c0 ? -1.0 : 0.0);
+        v.y = (r < NI && c0 + 1 < NI) ? -sym(NEM + r, NEM + c0 + 1) : (r == c0 + 1 ? -1.0 : 0.0);
+        a0[G::q(i, j)] = v;
+      }
+    __syncwarp();                          // every lane holds its S_co and S_oo entries
+#pragma unroll
+    for (int q = 0; q < G::NT; ++q) *reinterpret_cast<double2*>(Tl + q * 64) = a0[q];
+  } else {
 #pragma unroll
   for (int i = 0; i < NP; ++i)
 #pragma unroll
@@ -272,6 +292,7 @@ __device__ __forceinline__ bool element(SYM sym, double* __restrict__ T,
       *reinterpret_cast<double2*>(Tl + G::q(i, j) * 64) = v;
     }
 
+  }
   double2 it[NP][NP];
   int bad = 0;
   sweep<NP, NCB, true, SY, RS>(Tl, bt, it, bad, sync);
