@@ -359,6 +359,9 @@ def run_config(args, cfg, dev, world, steps, warmup, l2_flush, peaks, full=True)
         "executed_frac": f_kern_exec * nt / (t_kern * 1e-3) / 1e12 / P,
         "step_achieved": step_ach, "step_frac": step_ach / P,
         "traffic": ncu_traffic(kpref),
+        "note": "frac counts the dense formulation's flops (SURVEY §8.0.1), so the structured "
+                "algebra (DESIGN.md §3.2, ~2.5x fewer flops at k = 4, ~4x at k = 6) can exceed 1; "
+                "executed_frac counts the flops the kernels issue",
         "peak_source": "profiles/fp64_peak_r01.json (measured DMMA m8n8k4 peak, B200)"}
     res = {"condensation": out, "_step": step, "_launch": launch,
            "_bufs": (W, W_h, ST, ext, Sd, info, fused), "prob": prob}

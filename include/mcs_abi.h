@@ -53,8 +53,13 @@ int mcs_condense_struct(int k, int64_t nt, const double* srecords, double* S_pac
 
 /* ---- generation-fused structured condensation for any k (used for k = 5, 6,
  *      where Y does not fit a warp's registers): S_T from the geometry weights
- *      W [nt][nwgt >= 30] and the tables [mcs_fused_table_len(k)], CTA per
- *      element, Y in shared memory; the compact record never reaches HBM. */
+ *      W [nt][nwgt >= 30] and the tables [mcs_fused_table_len(k)]; the compact
+ *      record never reaches HBM.  k = 5, 6: the warp-per-element pipeline of
+ *      mcs_condense_fused in passes over the columns of Y (the lane-ordered
+ *      tables live in a library-owned device buffer rebuilt on `stream` at
+ *      every call: concurrent calls for the same k with DIFFERENT tables on
+ *      different streams are not supported); k <= 4 (and MCS_GEN=1): CTA per
+ *      element, Y in shared memory. */
 int mcs_condense_gen(int k, int64_t nt, const double* W, int nwgt, const double* tables,
                      double* S_packed, int* info, void* stream);
 /* k = 5, 6: mcs_condense_gen plus the double Schur outputs in the same kernel
@@ -64,11 +69,13 @@ int mcs_condense_gen(int k, int64_t nt, const double* W, int nwgt, const double*
 int mcs_condense_gen_ds(int k, int64_t nt, const double* W, int nwgt, const double* tables,
                         double* S_packed, double* ext, double* Sd_packed, int* info, void* stream);
 
-/* ---- fused element pipeline for k <= 4 (replaces assembly.py:49-91 +
+/* ---- fused element pipeline, k = 2..6 (replaces assembly.py:49-91 +
  *      condensation.py:159-177 + condensation.py:207-226 per element): one
  *      warp per element generates Bsig from the reference-cell tables and the
  *      element's geometry weights W [nt][nwgt >= 30], forms S_T = adiv + Y Y^T
  *      and the double Schur outputs (ext, Sd_packed as mcs_double_schur).
+ *      (The package uses it for k <= 4; at k = 5, 6 mcs_condense_gen followed
+ *      by mcs_double_schur gives bitwise the same outputs and is faster.)
  *      tables: [mcs_fused_table_len(k)] (engine.fused_tables).  info bit 0:
  *      singular stress block, bit 1: S_oo not SPD. */
 int mcs_fused_table_len(int k);
