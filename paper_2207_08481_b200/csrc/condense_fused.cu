@@ -170,8 +170,17 @@ struct Geo {
   static constexpr int TAB_A = TAB_MB + even(6 * nb * nb);   // ARef [6][ml][9]
   static constexpr int TAB_SMEM = TAB_A + even(6 * 9 * ml);
   // bubble column of DMMA n-tile bt, output column n (-1: none)
+  // HALF: the last pure bubble chunk holds <= 4 columns: they sit on the even
+  // columns (the k slots of the first m8n8k4 step of Y Y^T), the odd ones are
+  // zero and phase C skips the second step for that chunk (k = 6)
+  static constexpr int BLAST = NBP > 0 ? BREST - 8 * (NBP - 1) : 0;
+  static constexpr bool HALF = NBP > 0 && BLAST <= 4;
   __host__ __device__ static constexpr int jmap(int bt, int n) {
     if (MIX && bt == 0) return (n >= 2 * r && n - 2 * r < nb) ? n - 2 * r : -1;
+    if (HALF && bt == NBT - 1) {
+      const int j = BMIX + 8 * (bt - MIX) + n / 2;
+      return (n % 2 == 0 && n / 2 < BLAST) ? j : -1;
+    }
     const int j = BMIX + 8 * (bt - MIX) + n;
     return j < nb ? j : -1;
   }
@@ -584,6 +593,7 @@ __global__ void __launch_bounds__(32 * WPB, MINB)
         for (int kc = 0; kc < NCH; ++kc) {
 #pragma unroll
           for (int J = 0; J <= I; ++J) dmma884(acc[J][0], acc[J][1], Yf[I][kc].x, Yf[J][kc].x);
+          if (G::HALF && k0 + kc == NKC - 1) continue;     // odd columns of the last chunk are zero
 #pragma unroll
           for (int J = 0; J <= I; ++J) dmma884(acc[J][0], acc[J][1], Yf[I][kc].y, Yf[J][kc].y);
         }
