@@ -136,6 +136,16 @@ struct Geo {
   static constexpr int NKC = NLF + MIX + NBP;         // 8-column chunks of Y
   static constexpr int NKS = (nb + 3) / 4;            // k-steps of the bubble DMMA
   static constexpr int NR = T::NR, NRB = NR / 8;
+  static constexpr int TAIL = nloc - 8 * (NRB - 1);   // real rows of the last 8-row tile
+#ifndef MCS_FZ_NO_STAIL
+  // TAIL == 1 (k = 5): that row's S_T entries as dot products in phase C
+  // (measured: k = 5 1.89 -> 1.75 ms; with TAIL == 2 at k = 4 the shuffles
+  // cost more than the 48 DMMAs they replace: 0.324 -> 0.329 ms)
+  static constexpr bool STAIL = TAIL <= 1;
+#else
+  static constexpr bool STAIL = false;
+#endif
+  static_assert(!STAIL || 8 * (NRB - 1) >= nu, "tail rows are Vhat rows (no adiv term)");
   static constexpr int st_len = ExtLayout<K>::st_len;
   // k >= 5 (BIG): Y in passes of CPP chunks, tables in global memory, the
   // phase-A factors alias the packed S_T (dead until the first pass ends),
@@ -575,7 +585,7 @@ __global__ void __launch_bounds__(32 * WPB, MINB)
       // one tile row I at a time: the I + 1 independent accumulator chains of
       // the row interleave (k outer, J inner) and share the A operand Y_I
 #pragma unroll
-      for (int I = 0; I < NRB; ++I) {
+      for (int I = 0; I < NRB - (G::STAIL ? 1 : 0); ++I) {
         const int i = 8 * I + g;
         double acc[NRB][2];
 #pragma unroll
@@ -611,6 +621,41 @@ __global__ void __launch_bounds__(32 * WPB, MINB)
           }
         }
         asm volatile("" ::: "memory");   // keep the epilogue loads row by row (registers)
+      }
+      // the last tile row holds TAIL real rows (Vhat rows: no adiv term):
+      // NRB tiles of DMMAs for them would be mostly padding, so their entries
+      // S[i0][j] = Y[i0] . Y[j] are plain dot products -- row i0 of Y is
+      // broadcast from the lanes g == rr of the last tile (same t: same
+      // columns), every lane dots it with its own rows, the four t lanes of
+      // a row add up
+      if constexpr (G::STAIL) {
+#pragma unroll
+        for (int rr = 0; rr < G::TAIL; ++rr) {
+          const int i0 = 8 * (NRB - 1) + rr;
+          double2 yt[NCH];
+#pragma unroll
+          for (int kc = 0; kc < NCH; ++kc) {
+            yt[kc].x = __shfl_sync(0xffffffffu, Yf[NRB - 1][kc].x, 4 * rr + t);
+            yt[kc].y = __shfl_sync(0xffffffffu, Yf[NRB - 1][kc].y, 4 * rr + t);
+          }
+#pragma unroll
+          for (int I = 0; I < NRB; ++I) {
+            double pd = 0.0;
+#pragma unroll
+            for (int kc = 0; kc < NCH; ++kc) {
+              pd = fma(Yf[I][kc].x, yt[kc].x, pd);
+              if (G::HALF && k0 + kc == NKC - 1) continue;
+              pd = fma(Yf[I][kc].y, yt[kc].y, pd);
+            }
+            pd += __shfl_xor_sync(0xffffffffu, pd, 1);
+            pd += __shfl_xor_sync(0xffffffffu, pd, 2);
+            const int j = 8 * I + g;
+            if (t == 0 && j <= i0) {
+              if constexpr (PS > 0) pd += Spk[pk(i0, j)];
+              Spk[pk(i0, j)] = pd;
+            }
+          }
+        }
       }
     };
     pass(IC<0>{});
