@@ -28,6 +28,8 @@
 // chunk: low blocks m = 4 kc + t (2 columns per lane), then the bubble
 // columns, produced by a DMMA of the bubble part of B with L_b^-T whose
 // accumulator layout IS the operand layout.
+#include <cstdlib>
+
 #include "common.cuh"
 #include "ds_reg.cuh"
 
@@ -326,7 +328,12 @@ struct IC {
 };
 
 // DS: the double Schur as phase D (ext, Sd written); otherwise S_T only.
-template <int K, int WPB, int MINB, bool DS>
+// PAIR: the WPB / 4 warps of an SM sub-partition (w, w + 4, ...) start every
+// element together (named barrier), so that their chain-bound phase A runs
+// side by side and their DMMA-bound phases share the pipe (a warp streaming
+// DMMAs starves a co-resident warp's dependent FP64 chain).
+// Measured: k = 6 3.72 -> 3.48 ms; k = 5 1.75 -> 1.86 ms (off).
+template <int K, int WPB, int MINB, bool DS, bool PAIR = false>
 __global__ void __launch_bounds__(32 * WPB, MINB)
     condense_fused_kernel(const double* __restrict__ Wg, int nwgt, const double* __restrict__ tab,
                           const double* __restrict__ gtab, double* __restrict__ ST,
@@ -362,8 +369,15 @@ __global__ void __launch_bounds__(32 * WPB, MINB)
   const int nwl = nwgt < 30 ? nwgt : 30;
   double wnext = (e < nt && lane < nwl) ? __ldg(Wg + e * nwgt + lane) : 0.0;
 
+  static_assert(!PAIR || WPB % 4 == 0, "groups: the warps w, w + 4, ... of one CTA");
+  const int64_t e0 = static_cast<int64_t>(blockIdx.x) * WPB;
+  int64_t rounds = e0 < nt ? (nt - e0 + nw - 1) / nw : 0;   // PAIR: the same trip count for the CTA
 #pragma unroll 1
-  for (; e < nt; e += nw) {
+  for (; PAIR ? rounds > 0 : e < nt; e += nw, --rounds) {
+    if constexpr (PAIR) {
+      asm volatile("bar.sync %0, %1;" ::"r"(1 + (warp & 3)), "n"(32 * (WPB / 4)) : "memory");
+      if (e >= nt) continue;
+    }
     if (lane < nwl) wts[lane] = wnext;
     if (e + nw < nt && lane < nwl) wnext = __ldg(Wg + (e + nw) * nwgt + lane);   // prefetch
     __syncwarp();
@@ -696,16 +710,19 @@ __global__ void __launch_bounds__(32 * WPB, MINB)
   }
 }
 
+#ifndef MCS_FZ_PAIR4
+#define MCS_FZ_PAIR4 false   // k = 4: the three warps of a sub-partition in lockstep per element (A/B)
+#endif
 #ifndef MCS_FZ_WPB4
 #define MCS_FZ_WPB4 12   // warps per CTA at k = 4 (tools/fused_prof.py sweeps it)
 #endif
 
-template <int K, int WPB, int MINB, bool DS>
+template <int K, int WPB, int MINB, bool DS, bool PAIR = false>
 static int launch_condense_fused(int64_t nt, const double* W, int nwgt, const double* tab,
                                  double* ST, double* ext, double* Sd, int* info,
                                  cudaStream_t st) {
   using G = fz::Geo<K>;
-  auto kern = condense_fused_kernel<K, WPB, MINB, DS>;
+  auto kern = condense_fused_kernel<K, WPB, MINB, DS, PAIR>;
   const size_t smem =
       ((G::BIG ? 0 : G::TAB_SMEM) + static_cast<size_t>(WPB) * G::PER_WARP) * sizeof(double);
   double* gtab = nullptr;
@@ -734,9 +751,16 @@ static int launch_condense_fused(int64_t nt, const double* W, int nwgt, const do
 // k = 5, 6 without the double Schur (mcs_condense_gen routes here)
 int launch_condense_fused_big(int k, int64_t nt, const double* W, int nwgt, const double* tab,
                               double* ST, int* info, cudaStream_t st) {
+  // pairs of warps start every element together: default at k = 6 only
+  // (MCS_FZ_PAIR=0 / 1 forces it off / on for k = 5, 6)
+  static const int pair = getenv("MCS_FZ_PAIR") ? atoi(getenv("MCS_FZ_PAIR")) : -1;
   switch (k) {
-    case 5: return launch_condense_fused<5, 4, 2, false>(nt, W, nwgt, tab, ST, nullptr, nullptr, info, st);
-    case 6: return launch_condense_fused<6, 4, 2, false>(nt, W, nwgt, tab, ST, nullptr, nullptr, info, st);
+    case 5:
+      if (pair == 1) return launch_condense_fused<5, 8, 1, false, true>(nt, W, nwgt, tab, ST, nullptr, nullptr, info, st);
+      return launch_condense_fused<5, 4, 2, false>(nt, W, nwgt, tab, ST, nullptr, nullptr, info, st);
+    case 6:
+      if (pair != 0) return launch_condense_fused<6, 8, 1, false, true>(nt, W, nwgt, tab, ST, nullptr, nullptr, info, st);
+      return launch_condense_fused<6, 4, 2, false>(nt, W, nwgt, tab, ST, nullptr, nullptr, info, st);
   }
   return -1000;
 }
@@ -766,7 +790,7 @@ MCS_API int mcs_condense_fused(int k, int64_t nt, const double* W, int nwgt, con
     // one CTA per SM: the compact tables once per CTA, one element per warp
     case 2: return launch_condense_fused<2, 16, 1, true>(nt, W, nwgt, tables, S_packed, ext, Sd_packed, info, st);
     case 3: return launch_condense_fused<3, 12, 1, true>(nt, W, nwgt, tables, S_packed, ext, Sd_packed, info, st);
-    case 4: return launch_condense_fused<4, MCS_FZ_WPB4, 1, true>(nt, W, nwgt, tables, S_packed, ext, Sd_packed, info, st);
+    case 4: return launch_condense_fused<4, MCS_FZ_WPB4, 1, true, MCS_FZ_PAIR4>(nt, W, nwgt, tables, S_packed, ext, Sd_packed, info, st);
     // k = 5, 6: the passes pipeline with the double Schur as phase D
     case 5: return launch_condense_fused<5, 4, 2, true>(nt, W, nwgt, tables, S_packed, ext, Sd_packed, info, st);
     case 6: return launch_condense_fused<6, 4, 2, true>(nt, W, nwgt, tables, S_packed, ext, Sd_packed, info, st);

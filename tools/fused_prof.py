@@ -18,17 +18,19 @@ from paper_2207_08481_b200.problems import baseline_config  # noqa: E402
 
 WPB = int(os.environ.get("WPB", "12"))
 CPP = int(os.environ.get("CPP", "4"))
-so = os.path.join(ROOT, "tools", f"_fused_prof_{WPB}_{CPP}.so")
+PAIR = os.environ.get("PAIR", "false")
+so = os.path.join(ROOT, "tools", f"_fused_prof_{WPB}_{CPP}_{PAIR}.so")
 csrc = os.path.join(ROOT, "paper_2207_08481_b200", "csrc")
 if not os.path.exists(so):
     subprocess.check_call(["nvcc", "-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-std=c++17",
-                           "-Xcompiler", "-fPIC", "-shared", "-DMCS_FUSED_PROF", f"-DMCS_FZ_WPB4={WPB}", f"-DMCS_FZ_CPP4={CPP}", "-I", csrc, "-I",
+                           "-Xcompiler", "-fPIC", "-shared", "-DMCS_FUSED_PROF", f"-DMCS_FZ_WPB4={WPB}", f"-DMCS_FZ_CPP4={CPP}", f"-DMCS_FZ_PAIR4={PAIR}", "-I", csrc, "-I",
                            os.path.join(ROOT, "include"), "--expt-relaxed-constexpr",
                            os.path.join(csrc, "condense_fused.cu"), "-o", so])
 lib = ctypes.CDLL(so)
 P, I, L = ctypes.c_void_p, ctypes.c_int, ctypes.c_int64
 lib.mcs_condense_fused.argtypes = [I, L, P, I, P, P, P, P, P, P]
-prob = baseline_config(2)
+CFG = int(os.environ.get("CFG", "2"))
+prob = baseline_config(CFG)
 fes = FeSystem(prob.mesh, prob.regions, prob.k)
 k, nt = prob.k, prob.mesh.num_triangles
 W = engine.to_dev(refblocks.element_weights(fes, prob.nu))
@@ -47,7 +49,7 @@ for _ in range(10):
     lib.mcs_condense_fused(*args)
 ev1.record()
 torch.cuda.synchronize()
-print(f"WPB {WPB}: {ev0.elapsed_time(ev1) / 10:.4f} ms per launch (with clock accounting)")
+print(f"cfg{CFG} k={k} WPB {WPB}: {ev0.elapsed_time(ev1) / 10:.4f} ms per launch (with clock accounting)")
 sym = ctypes.c_ulonglong * 8
 buf = sym()
 cudart = ctypes.CDLL("libcudart.so") if False else None
