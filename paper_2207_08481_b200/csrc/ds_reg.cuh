@@ -160,6 +160,15 @@ struct PairSync {
   }
 };
 
+// the same barrier before the first pivot tile only (the pair starts every
+// element together and drifts afterwards)
+struct PairSync0 {
+  int id;
+  __device__ __forceinline__ void operator()(int j) const {
+    if (j == 0) asm volatile("bar.sync %0, 64;" ::"r"(id) : "memory");
+  }
+};
+
 // sync(j) runs before pivot tile j is factorised: the kernels pair the two
 // warps of an SM sub-partition with a named barrier there, so that their
 // latency-bound factorisations coincide and their DMMA bursts share the

@@ -440,7 +440,7 @@ __global__ void __launch_bounds__(64, 6)
 // together and their DMMA bursts share the pipe (see dsr::sweep).
 using dsr::PairSync;
 
-template <int NS, int NC, int WPB, int MINB, bool PAIR>
+template <int NS, int NC, int WPB, int MINB, int PAIR>
 __global__ void __launch_bounds__(32 * WPB, MINB)
     spd_schur_w1(const double* __restrict__ A, const double* __restrict__ B,
                  double* __restrict__ S, int* __restrict__ info, int64_t batch, int pf) {
@@ -488,8 +488,10 @@ __global__ void __launch_bounds__(32 * WPB, MINB)
       for (int i = 0; i < NP; ++i) bt[c][i] = load_bt<NS, NC>(Be, c, i);
     int bad = 0;
     double2 none[1][1];
-    if constexpr (PAIR)
+    if constexpr (PAIR == 1)
       dsr::sweep<NP, NCB, false>(Tl, bt, none, bad, PairSync{1 + (warp & 3)});
+    else if constexpr (PAIR == 2)
+      dsr::sweep<NP, NCB, false>(Tl, bt, none, bad, dsr::PairSync0{1 + (warp & 3)});
     else
       dsr::sweep<NP, NCB, false>(Tl, bt, none, bad);
     if (!live) continue;
@@ -539,9 +541,10 @@ int launch_spd_schur_w2(const double* A, const double* B, double* S, int* info, 
   // two-warp kernel (and its MCS_MICRO_YIELD throttle variants)
   static const int mv = getenv("MCS_MICRO") ? atoi(getenv("MCS_MICRO")) : 1;
   if (mv != 2) {
-    // MCS_MICRO=3: the same kernel with the pair barriers (A/B: +5% with the
-    // rsqrt-per-pivot factorisation, -1% with the current one)
-    auto kern = mv == 3 ? micro::spd_schur_w1<NS, NC, 8, 1, true> : micro::spd_schur_w1<NS, NC, 8, 1, false>;
+    // default: the pair meets once per element (22.3 ms); 3: before every
+    // pivot tile (22.9 ms); 4: never (22.75 ms)
+    auto kern = mv == 3 ? micro::spd_schur_w1<NS, NC, 8, 1, 1>
+                        : (mv == 4 ? micro::spd_schur_w1<NS, NC, 8, 1, 0> : micro::spd_schur_w1<NS, NC, 8, 1, 2>);
     const size_t smem = (size_t)8 * micro::Geo<NS, NC>::NT * 64 * sizeof(double);
     cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     int per_sm = 0;
