@@ -40,7 +40,7 @@ if what in ("all", "cfg"):
     print("iters", rep.iterations)
 if what in ("all", "ds"):
     # cfg3 (k = 6): generation-fused condensation + the warp-per-element double Schur
-    prob = baseline_config(3, int(os.environ.get("PROF_N3", "128")))
+    prob = baseline_config(3, int(os.environ.get("PROF_N3", "256")))
     fes = FeSystem(prob.mesh, prob.regions, prob.k)
     sys_ = double_schur(condense_sigma_omega(fes, prob.nu, prob.body_force))
     torch.cuda.synchronize()
