@@ -306,27 +306,6 @@ __device__ __forceinline__ bool element(SYM sym, double* __restrict__ T,
   int bad = 0;
   sweep<NP, NCB, true, SY, RS>(Tl, bt, it, bad, sync);
 
-  // ---- Sd_T = S_cc - W^T W (lower tiles), S_cc loaded ahead of each chain
-#pragma unroll
-  for (int c = 0; c < NCB; ++c) {
-    const int row = 8 * c + g, a = cpl_local<K>(row);
-#pragma unroll
-    for (int d = 0; d <= c; ++d) {
-      const int col = 8 * d + 2 * t;
-      double s0 = 0.0, s1 = 0.0;
-      if (row < NC) {
-        if (col <= row) s0 = sym(a, cpl_local<K>(col));
-        if (col + 1 <= row) s1 = sym(a, cpl_local<K>(col + 1));
-      }
-      double2 o = make_double2(0.0, 0.0);
-#pragma unroll
-      for (int j = 0; j < NP; ++j) mma_xyt(o, bt[c][j], bt[d][j]);
-      if (row < NC) {
-        if (col <= row) so[pk(row, col)] = s0 - o.x;
-        if (col + 1 <= row) so[pk(row, col + 1)] = s1 - o.y;
-      }
-    }
-  }
   // ---- X = L^-T W (row tile I: sum over I' >= I), row-major n_int x ncpl
 #pragma unroll
   for (int I = 0; I < NP; ++I) {
@@ -361,6 +340,45 @@ __device__ __forceinline__ bool element(SYM sym, double* __restrict__ T,
         if (col <= row) xo[L::x_len + pk(row, col)] = o.x;
         if (col + 1 <= row) xo[L::x_len + pk(row, col + 1)] = o.y;
       }
+    }
+  }
+  // ---- Sd_T = S_cc - W^T W (lower tiles), last: `it` is dead by now, and
+  // the S_cc entries of tile row c + 1 are requested before the DMMA chains
+  // of row c (a single chain, ~260 clk, does not cover an L2 round trip)
+  {
+    double2 cur[NCB], nxt[NCB];
+    auto load_row = [&](int c, double2 (&dst)[NCB]) {
+      const int row = 8 * c + g, a = cpl_local<K>(row);
+#pragma unroll
+      for (int d = 0; d < NCB; ++d) {
+        if (d > c) continue;
+        const int col = 8 * d + 2 * t;
+        double2 v = make_double2(0.0, 0.0);
+        if (row < NC) {
+          if (col <= row) v.x = sym(a, cpl_local<K>(col));
+          if (col + 1 <= row) v.y = sym(a, cpl_local<K>(col + 1));
+        }
+        dst[d] = v;
+      }
+    };
+    load_row(0, cur);
+#pragma unroll
+    for (int c = 0; c < NCB; ++c) {
+      if (c + 1 < NCB) load_row(c + 1, nxt);
+      const int row = 8 * c + g;
+#pragma unroll
+      for (int d = 0; d <= c; ++d) {
+        double2 o = make_double2(0.0, 0.0);
+#pragma unroll
+        for (int j = 0; j < NP; ++j) mma_xyt(o, bt[c][j], bt[d][j]);
+        const int col = 8 * d + 2 * t;
+        if (row < NC) {
+          if (col <= row) so[pk(row, col)] = cur[d].x - o.x;
+          if (col + 1 <= row) so[pk(row, col + 1)] = cur[d].y - o.y;
+        }
+      }
+#pragma unroll
+      for (int d = 0; d < NCB; ++d) cur[d] = nxt[d];
     }
   }
   return __all_sync(0xffffffffu, bad == 0);
