@@ -249,7 +249,7 @@ __device__ __forceinline__ void sweep(double* __restrict__ Tl, double2 (&bt)[NCB
 // (the fused k = 5, 6 kernel puts them over the interior rows of the packed
 // S_T): every such entry is loaded into registers before the first slot is
 // written.  The S_cc entries read at the end must lie outside T.
-template <int K, class SYM, class SY = NoSync, bool RS = false, bool ALIAS = false>
+template <int K, class SYM, class SY = NoSync, bool RS = false, bool ALIAS = false, bool SDLAST = false>
 __device__ __forceinline__ bool element(SYM sym, double* __restrict__ T,
                                         double* __restrict__ xo, double* __restrict__ so,
                                         SY sync = SY()) {
@@ -306,6 +306,29 @@ __device__ __forceinline__ bool element(SYM sym, double* __restrict__ T,
   int bad = 0;
   sweep<NP, NCB, true, SY, RS>(Tl, bt, it, bad, sync);
 
+  if constexpr (!SDLAST) {
+  // ---- Sd_T = S_cc - W^T W (lower tiles), S_cc loaded ahead of each chain
+#pragma unroll
+  for (int c = 0; c < NCB; ++c) {
+    const int row = 8 * c + g, a = cpl_local<K>(row);
+#pragma unroll
+    for (int d = 0; d <= c; ++d) {
+      const int col = 8 * d + 2 * t;
+      double s0 = 0.0, s1 = 0.0;
+      if (row < NC) {
+        if (col <= row) s0 = sym(a, cpl_local<K>(col));
+        if (col + 1 <= row) s1 = sym(a, cpl_local<K>(col + 1));
+      }
+      double2 o = make_double2(0.0, 0.0);
+#pragma unroll
+      for (int j = 0; j < NP; ++j) mma_xyt(o, bt[c][j], bt[d][j]);
+      if (row < NC) {
+        if (col <= row) so[pk(row, col)] = s0 - o.x;
+        if (col + 1 <= row) so[pk(row, col + 1)] = s1 - o.y;
+      }
+    }
+  }
+  }
   // ---- X = L^-T W (row tile I: sum over I' >= I), row-major n_int x ncpl
 #pragma unroll
   for (int I = 0; I < NP; ++I) {
@@ -342,10 +365,12 @@ __device__ __forceinline__ bool element(SYM sym, double* __restrict__ T,
       }
     }
   }
-  // ---- Sd_T = S_cc - W^T W (lower tiles), last: `it` is dead by now, and
-  // the S_cc entries of tile row c + 1 are requested before the DMMA chains
-  // of row c (a single chain, ~260 clk, does not cover an L2 round trip)
-  {
+  // ---- SDLAST (S_T in global memory): Sd_T = S_cc - W^T W last: `it` is
+  // dead by now, and the S_cc entries of tile row c + 1 are requested before
+  // the DMMA chains of row c (a single chain, ~260 clk, does not cover an L2
+  // round trip).  With S_T in shared memory (fused phase D) Sd_T first is
+  // 1.5% faster.
+  if constexpr (SDLAST) {
     double2 cur[NCB], nxt[NCB];
     auto load_row = [&](int c, double2 (&dst)[NCB]) {
       const int row = 8 * c + g, a = cpl_local<K>(row);
