@@ -39,6 +39,10 @@ from . import _abi, engine
 DENSE_MAX = 1024
 LEAF = int(os.environ.get("MCS_LEAF", "64"))   # max dofs of a nested-dissection leaf (A/B in PCG: 64 > 80 > 96)
 TOP_MAX = int(os.environ.get("MCS_TOP_MAX", "4096"))   # dense-inverse top (A/B in PCG: 4096 > 2048)
+# supernode amalgamation of the separator tree: "lo-hi[,lo-hi...]" merges, into
+# every node of height hi, its descendants of height >= lo (one front, one
+# level kernel instead of hi - lo + 1).  "" = none.
+AMALG = os.environ.get("MCS_AMALG", "")
 
 
 @dataclass
@@ -78,6 +82,56 @@ def _nested_dissection(A: sp.csr_matrix, xy: np.ndarray, leaf: int) -> _Node:
     return rec(np.arange(n))
 
 
+def _heights(root):
+    h = {}
+
+    def walk(nd):
+        h[id(nd)] = 1 + max([walk(c) for c in nd.children], default=-1)
+        return h[id(nd)]
+
+    walk(root)
+    return h
+
+
+def _amalgamate(root: _Node, spec: str) -> _Node:
+    """Merge bands of the separator tree into supernodes (see AMALG): the
+    merged node eliminates the union of the own dofs (descendants first), its
+    children are the subtrees hanging below the band.  Any such merge keeps
+    the factorisation exact (the front is dense); it trades a few more factor
+    bytes for fewer dependent level kernels."""
+    bands = []
+    for part in filter(None, (q.strip() for q in spec.split(","))):
+        lo, hi = (int(v) for v in part.split("-"))
+        if not 0 <= lo < hi:
+            raise ValueError(f"MCS_AMALG band {part!r}")
+        bands.append((lo, hi))
+    for lo, hi in sorted(bands, reverse=True):          # top bands first: heights below stay valid
+        h = _heights(root)
+
+        def absorb(nd, lo=lo, h=h):
+            """own dofs (postorder) and hanging subtrees of nd's descendants of height >= lo"""
+            own, kids = [], []
+            for c in nd.children:
+                if h[id(c)] >= lo:
+                    o, k = absorb(c)
+                    own += o + [c.own]
+                    kids += k
+                else:
+                    kids.append(c)
+            return own, kids
+
+        def walk(nd, lo=lo, hi=hi, h=h):
+            if h[id(nd)] == hi:
+                own, kids = absorb(nd)
+                nd.own = np.concatenate(own + [nd.own]) if own else nd.own
+                nd.children = kids
+            for c in nd.children:
+                walk(c)
+
+        walk(root)
+    return root
+
+
 def _postorder(root):
     out = []
 
@@ -104,6 +158,8 @@ def multifrontal_factor(A: sp.csr_matrix, xy: np.ndarray, leaf: int = LEAF) -> M
     A = A.tocsr()
     n = A.shape[0]
     root = _nested_dissection(A, xy, leaf)
+    if AMALG:
+        root = _amalgamate(root, AMALG)
     nodes = _postorder(root)
     perm = np.concatenate([nd.own for nd in nodes]).astype(np.int64)
     pos = np.empty(n, dtype=np.int64)
@@ -193,8 +249,13 @@ def _upload_multifrontal(F: MultifrontalFactor):
         oo += nb
         bo += nb
         Bcat.append(nd.B)
-    src_t = -np.ones((F.n, 2), dtype=np.int64)
-    src_o = -np.ones((max(oo, 1), 2), dtype=np.int64)
+    # gather sources per entry: one slot per child (2 in a plain separator
+    # tree, more under amalgamated supernodes); the kernels read the count
+    # from the node record
+    nslot = max(2, max(len(nd.children) for nd in nodes))
+    node_tab[:, 9] = nslot
+    src_t = -np.ones((F.n, nslot), dtype=np.int64)
+    src_o = -np.ones((max(oo, 1), nslot), dtype=np.int64)
     for i, nd in enumerate(nodes):
         ns = len(nd.own)
         loc = {int(p): r for r, p in enumerate(nd.B)}

@@ -23,7 +23,7 @@ namespace mcs {
 constexpr int MF_THREADS = 256;
 
 struct NodeRec {
-  int64_t s0, ns, nb, oL, oLT, oW, oWT, oo, ob, pad;
+  int64_t s0, ns, nb, oL, oLT, oW, oWT, oo, ob, nslot;   // nslot: gather sources per entry (>= 2)
 };
 
 // start of row j of a packed-upper row-major n x n matrix, minus j (so that
@@ -149,19 +149,23 @@ __global__ void __launch_bounds__(MF_THREADS)
   // all gathers up front, in parallel: own right-hand side and the child
   // updates that pass through to the boundary
   for (int j = threadIdx.x; j < ns + nb; j += MF_THREADS) {
+    const int S = (int)nd.nslot;
     if (j < ns) {
       const int64_t p = nd.s0 + j;
       double v = b[__ldg(perm + p)];
-      const int a = __ldg(src_t + 2 * p), c = __ldg(src_t + 2 * p + 1);
-      if (a >= 0) v -= out[a];
-      if (c >= 0) v -= out[c];
+      const int* sp = src_t + S * p;
+      for (int q = 0; q < S; ++q) {      // fixed order: deterministic
+        const int a = __ldg(sp + q);
+        if (a >= 0) v -= out[a];
+      }
       t[j] = v;
     } else {
-      const int64_t q = nd.oo + (j - ns);
-      const int a = __ldg(src_o + 2 * q), c = __ldg(src_o + 2 * q + 1);
+      const int* sp = src_o + S * (nd.oo + (j - ns));
       double v = 0.0;
-      if (a >= 0) v += out[a];
-      if (c >= 0) v += out[c];
+      for (int q = 0; q < S; ++q) {
+        const int a = __ldg(sp + q);
+        if (a >= 0) v += out[a];
+      }
       pass[j - ns] = v;
     }
   }
@@ -301,6 +305,7 @@ __global__ void __launch_bounds__(MF_THREADS)
     mbar_expect_tx(&bar, len * 8);
     if (len) bulk_g2s(F, mats + nd.oL, len * 8, &bar);
   }
+  const int S = (int)nd.nslot;    // gather sources per entry: two preloaded, the rest (amalgamated nodes) at gather time
   int ia[MF_PRE], ib[MF_PRE], ic[MF_PRE];
 #pragma unroll
   for (int u = 0; u < MF_PRE; ++u) {
@@ -309,12 +314,12 @@ __global__ void __launch_bounds__(MF_THREADS)
     if (j < ns) {
       const int64_t p = nd.s0 + j;
       ia[u] = __ldg(perm + p);
-      ib[u] = __ldg(src_t + 2 * p);
-      ic[u] = __ldg(src_t + 2 * p + 1);
+      ib[u] = __ldg(src_t + S * p);
+      ic[u] = __ldg(src_t + S * p + 1);
     } else if (j < ns + nb) {
       const int64_t q = nd.oo + (j - ns);
-      ib[u] = __ldg(src_o + 2 * q);
-      ic[u] = __ldg(src_o + 2 * q + 1);
+      ib[u] = __ldg(src_o + S * q);
+      ic[u] = __ldg(src_o + S * q + 1);
     }
   }
   pdl_wait();
@@ -324,11 +329,21 @@ __global__ void __launch_bounds__(MF_THREADS)
       double v = b[pv];
       if (a >= 0) v -= out[a];
       if (c >= 0) v -= out[c];
+      const int* sp = src_t + S * (nd.s0 + j);
+      for (int q = 2; q < S; ++q) {
+        const int e = __ldg(sp + q);
+        if (e >= 0) v -= out[e];
+      }
       t[j] = v;
     } else {
       double v = 0.0;
       if (a >= 0) v += out[a];
       if (c >= 0) v += out[c];
+      const int* sp = src_o + S * (nd.oo + (j - ns));
+      for (int q = 2; q < S; ++q) {
+        const int e = __ldg(sp + q);
+        if (e >= 0) v += out[e];
+      }
       pass[j - ns] = v;
     }
   };
@@ -340,10 +355,10 @@ __global__ void __launch_bounds__(MF_THREADS)
   for (int j = threadIdx.x + MF_PRE * MF_THREADS; j < ns + nb; j += MF_THREADS) {
     if (j < ns) {
       const int64_t p = nd.s0 + j;
-      gather(j, __ldg(perm + p), __ldg(src_t + 2 * p), __ldg(src_t + 2 * p + 1));
+      gather(j, __ldg(perm + p), __ldg(src_t + S * p), __ldg(src_t + S * p + 1));
     } else {
       const int64_t q = nd.oo + (j - ns);
-      gather(j, -1, __ldg(src_o + 2 * q), __ldg(src_o + 2 * q + 1));
+      gather(j, -1, __ldg(src_o + S * q), __ldg(src_o + S * q + 1));
     }
   }
   __syncthreads();
@@ -438,7 +453,7 @@ static size_t mf_stage_smem(int max_ns, int max_nb, int& blk_max) {
   // forward [block | t : max_ns | ys : max_ns | pass : max_nb],
   // backward [block | s : max_ns | perm (ints) : max_ns | xb : max_nb]
   const size_t bytes = ((size_t)blk_max + 2 * (size_t)max_ns + max_nb) * sizeof(double);
-  return bytes <= 200 * 1024 ? bytes : 0;
+  return bytes <= 224 * 1024 ? bytes : 0;   // of the 227 KB a CTA can have
 }
 
 }  // namespace mcs

@@ -151,3 +151,32 @@ def test_multifrontal_factor_exact(cfg, n, leaf):
     finally:
         co.TOP_MAX = co_top
     assert np.abs(xh - ref).max() <= 1e-11 * np.abs(ref).max()
+
+
+@pytest.mark.parametrize("spec", ["1-2", "1-3", "0-1,2-3"])
+def test_multifrontal_factor_exact_with_amalgamated_supernodes(spec):
+    """Supernode amalgamation of the separator tree (coarse.AMALG) keeps the
+    factorisation exact and removes levels from the schedule."""
+    prob = baseline_config(2, 24)
+    fes = FeSystem(prob.mesh, prob.regions, prob.k)
+    A = pc.coarse_matrix(fes, prob.nu)
+    xy = fes.mesh.vertices[np.flatnonzero(fes.dof_vbar.is_free) // 2]
+    base = co.multifrontal_factor(A, xy, leaf=16)
+    keep = co.AMALG
+    try:
+        co.AMALG = spec
+        F = co.multifrontal_factor(A, xy, leaf=16)
+    finally:
+        co.AMALG = keep
+    assert len(F.levels) < len(base.levels)
+    assert sorted(F.perm.tolist()) == list(range(A.shape[0]))
+    b = np.random.default_rng(1).standard_normal(A.shape[0])
+    ref = spla.spsolve(A.tocsc(), b)
+    assert np.abs(emulate_solve(F, b) - ref).max() <= 1e-12 * np.abs(ref).max()
+    co_top = co.TOP_MAX
+    try:
+        co.TOP_MAX = 200
+        xh = emulate_hybrid(F, b)
+    finally:
+        co.TOP_MAX = co_top
+    assert np.abs(xh - ref).max() <= 1e-11 * np.abs(ref).max()
