@@ -97,26 +97,39 @@ class _PcgState:
         """Record one step per rz-slot parity (the state is restored after
         the eager warm-up the capture needs)."""
         torch = __import__("torch")
+        import gc
         ws = workspace()
         saved = [t.clone() for t in (self.x, self.r, self.p, self.z, ws.sc)]
         cur = torch.cuda.current_stream()
         side = torch.cuda.Stream()
         side.wait_stream(cur)
         graphs = []
-        with torch.cuda.stream(side):
-            self.step(ws.RZ0, ws.RZ1)
-            for rz, rzn in ((ws.RZ0, ws.RZ1), (ws.RZ1, ws.RZ0)):
-                g = torch.cuda.CUDAGraph()
-                with torch.cuda.graph(g, stream=side):
-                    self.step(rz, rzn)
-                graphs.append(g)
-            # two steps per replay: the second is gated off on the device when
-            # the first one stops the loop (one host read-back per two steps)
-            pair = torch.cuda.CUDAGraph(keep_graph=True)
-            with torch.cuda.graph(pair, stream=side):
-                self.step(ws.RZ0, ws.RZ1, gate_out=ws.GATE)
-                self.step(ws.RZ1, ws.RZ0, ws.PAP2, ws.RR2, gate_in=ws.GATE)
-            pair.instantiate()
+        # No cyclic garbage collection while a stream is capturing: collecting
+        # an older operator's PCG state there destroys its CUDA graphs and
+        # frees their private pools (cudaFree / cudaGraphExecDestroy), which
+        # invalidates the running capture (seen as error 901 on the next
+        # launch).  Pending garbage is collected before the first capture.
+        gc_was_enabled = gc.isenabled()
+        gc.collect()
+        gc.disable()
+        try:
+            with torch.cuda.stream(side):
+                self.step(ws.RZ0, ws.RZ1)
+                for rz, rzn in ((ws.RZ0, ws.RZ1), (ws.RZ1, ws.RZ0)):
+                    g = torch.cuda.CUDAGraph()
+                    with torch.cuda.graph(g, stream=side):
+                        self.step(rz, rzn)
+                    graphs.append(g)
+                # two steps per replay: the second is gated off on the device when
+                # the first one stops the loop (one host read-back per two steps)
+                pair = torch.cuda.CUDAGraph(keep_graph=True)
+                with torch.cuda.graph(pair, stream=side):
+                    self.step(ws.RZ0, ws.RZ1, gate_out=ws.GATE)
+                    self.step(ws.RZ1, ws.RZ0, ws.PAP2, ws.RR2, gate_in=ws.GATE)
+                pair.instantiate()
+        finally:
+            if gc_was_enabled:
+                gc.enable()
         cur.wait_stream(side)
         for t, v in zip((self.x, self.r, self.p, self.z, ws.sc), saved):
             t.copy_(v)
