@@ -697,7 +697,7 @@ __global__ void __launch_bounds__(32 * WPB, MINB)
         // last) lies in the rows before and after them
         constexpr int T0 = even(pk(G::NEM, 0));
         static_assert(T0 + dsr::Geo<K>::PER_WARP <= pk(G::NEM + G::NI, 0), "slots inside the interior rows");
-        if (!dsr::element<K, decltype(S), dsr::NoSync, true, true>(S, Spk + T0, ext + e * L::len,
+        if (!dsr::element_pm<K, decltype(S), dsr::NoSync, true, true>(S, Spk + T0, ext + e * L::len,
                                                                    Sd + e * L::sd_len))
           bad |= 2;
       } else {

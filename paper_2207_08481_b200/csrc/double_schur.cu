@@ -203,10 +203,10 @@ __global__ void __launch_bounds__(32 * WPB, MINB)
     auto sym = [&](int a, int b) { return __ldg(S + (a >= b ? pk(a, b) : pk(b, a))); };
     bool ok;
     if constexpr (PAIR)
-      ok = dsr::element<K, decltype(sym), dsr::PairSync0, (K >= 5), false, true>(sym, T, ext + e * L::len, Sd + e * L::sd_len,
+      ok = dsr::element_pm<K, decltype(sym), dsr::PairSync0, (K >= 5), false, true>(sym, T, ext + e * L::len, Sd + e * L::sd_len,
                                                                   dsr::PairSync0{1 + (warp & 3)});
     else
-      ok = dsr::element<K, decltype(sym), dsr::NoSync, (K >= 5), false, true>(sym, T, ext + e * L::len, Sd + e * L::sd_len);
+      ok = dsr::element_pm<K, decltype(sym), dsr::NoSync, (K >= 5), false, true>(sym, T, ext + e * L::len, Sd + e * L::sd_len);
     if (lane == 0 && info) info[e] = ok ? 0 : 1;
   }
 }

@@ -45,6 +45,33 @@ __device__ __forceinline__ void mma_xyt(double2& c, double2 x, double2 y) {
   dmma884(c.x, c.y, x.x, y.x);
   dmma884(c.x, c.y, x.y, y.y);
 }
+// the first m8n8k4 step only (k slots 0, 2, 4, 6): a k tile whose odd columns are zero
+__device__ __forceinline__ void mma_xyt_even(double2& c, double2 x, double2 y) {
+  dmma884(c.x, c.y, x.x, y.x);
+}
+// HALF ? even k slots only : both steps
+template <bool HALF>
+__device__ __forceinline__ void mma_tile(double2& c, double2 x, double2 y) {
+  if constexpr (HALF) mma_xyt_even(c, x, y);
+  else mma_xyt(c, x, y);
+}
+
+// Positions of the N pivot dofs in NP = ceil(N / 8) tiles.  When the last
+// tile holds REM <= 4 dofs (k = 6: 35 = 4 * 8 + 3; the microbench: 60 =
+// 7 * 8 + 4) they sit on its EVEN slots and the odd slots are padding
+// (identity rows): every product that contracts over that tile then needs
+// only the first of its two m8n8k4 steps (HALF).
+template <int N>
+struct PivMap {
+  static constexpr int NP = (N + 7) / 8, REM = N - 8 * (NP - 1);
+  static constexpr bool HALF = REM <= 4 && NP > 1;
+  // dof at slot s of tile `tile`, -1 for padding
+  __host__ __device__ static constexpr int dof(int tile, int s) {
+    if (tile < NP - 1) return 8 * tile + s;          // full tiles: no padding
+    if (HALF) return (s % 2 == 0 && s / 2 < REM) ? 8 * tile + s / 2 : -1;
+    return s < REM ? 8 * tile + s : -1;
+  }
+};
 
 // Cholesky M M^T = Y of one SPD 8x8 tile in the row layout (lower triangle
 // significant), returned as M^-1 in the row layout.  With Y = Lu D Lu^T (Lu
@@ -174,7 +201,9 @@ struct PairSync0 {
 // latency-bound factorisations coincide and their DMMA bursts share the
 // FP64 pipe (a warp streaming DMMAs starves a co-resident warp's dependent
 // FP64 chain: tools/dmma_prio.cu; unsynchronised, two warps serialise).
-template <int NP, int NCB, bool IT, class SY = NoSync, bool RS = false>
+// HALF: the last pivot tile's odd slots are padding (PivMap): its diagonal
+// products take one m8n8k4 step.
+template <int NP, int NCB, bool IT, class SY = NoSync, bool RS = false, bool HALF = false>
 __device__ __forceinline__ void sweep(double* __restrict__ Tl, double2 (&bt)[NCB][NP],
                                       double2 (&it)[IT ? NP : 1][IT ? NP : 1], int& bad,
                                       SY sync = SY()) {
@@ -211,14 +240,18 @@ __device__ __forceinline__ void sweep(double* __restrict__ Tl, double2 (&bt)[NCB
 #pragma unroll
     for (int c = 0; c < NCB; ++c) {
       double2 o = make_double2(0.0, 0.0);
-      mma_xyt(o, bt[c][j], mi);
+      if (HALF && j == NP - 1) mma_xyt_even(o, bt[c][j], mi);
+      else mma_xyt(o, bt[c][j], mi);
       bt[c][j] = o;
     }
     if constexpr (IT) {
 #pragma unroll
       for (int J = 0; J <= j; ++J) {
         double2 o = make_double2(0.0, 0.0);
-        mma_xyt(o, J == j ? eye : it[J][j], mi);
+        // (HALF, J == j: the padding rows of this tile come out zero instead
+        // of unit rows; they are never stored nor multiplied into stored ones)
+        if (HALF && j == NP - 1) mma_xyt_even(o, J == j ? eye : it[J][j], mi);
+        else mma_xyt(o, J == j ? eye : it[J][j], mi);
         it[J][j] = o;
       }
     }
@@ -396,6 +429,177 @@ __device__ __forceinline__ bool element(SYM sym, double* __restrict__ T,
         double2 o = make_double2(0.0, 0.0);
 #pragma unroll
         for (int j = 0; j < NP; ++j) mma_xyt(o, bt[c][j], bt[d][j]);
+        const int col = 8 * d + 2 * t;
+        if (row < NC) {
+          if (col <= row) so[pk(row, col)] = cur[d].x - o.x;
+          if (col + 1 <= row) so[pk(row, col + 1)] = cur[d].y - o.y;
+        }
+      }
+#pragma unroll
+      for (int d = 0; d < NCB; ++d) cur[d] = nxt[d];
+    }
+  }
+  return __all_sync(0xffffffffu, bad == 0);
+}
+
+// The same with the pivot dofs placed by PivMap (k = 6: the three interior
+// dofs of the last tile on its even slots, products over it in one m8n8k4
+// step).  Kept apart from element(): the fused k <= 4 kernel is sensitive to
+// the code around its phase D (+-1-2% from equivalent index arithmetic).
+// ALIAS: the tile slots T overlap memory that sym() reads for S_oo and S_co
+// (the fused k = 5, 6 kernel puts them over the interior rows of the packed
+// S_T): every such entry is loaded into registers before the first slot is
+// written.  The S_cc entries read at the end must lie outside T.
+template <int K, class SYM, class SY = NoSync, bool RS = false, bool ALIAS = false, bool SDLAST = false>
+__device__ __forceinline__ bool element_pm(SYM sym, double* __restrict__ T,
+                                        double* __restrict__ xo, double* __restrict__ so,
+                                        SY sync = SY()) {
+  using G = Geo<K>;
+  using L = ExtLayout<K>;
+  using PM = PivMap<G::NI>;
+  constexpr int NC = G::NC, NEM = G::NEM, NP = G::NP, NCB = G::NCB;
+  constexpr bool HALF = PM::HALF;
+  const int lane = threadIdx.x & 31, g = lane >> 2, t = lane & 3;
+  double* Tl = T + 2 * lane;
+  // ---- loads: S_co tiles into registers, S_oo lower tiles into the slots
+  // (interior dof of row g / columns 2t, 2t + 1 of pivot tile i: PivMap)
+  double2 bt[NCB][NP];
+#pragma unroll
+  for (int c = 0; c < NCB; ++c) {
+    const int row = 8 * c + g, a = cpl_local<K>(row);
+#pragma unroll
+    for (int i = 0; i < NP; ++i) {
+      const int d0 = PM::dof(i, 2 * t), d1 = PM::dof(i, 2 * t + 1);
+      double2 v = make_double2(0.0, 0.0);
+      if (row < NC) {
+        if (d0 >= 0) v.x = sym(a, NEM + d0);
+        if (d1 >= 0) v.y = sym(a, NEM + d1);
+      }
+      bt[c][i] = v;
+    }
+  }
+  auto soo_tile = [&](int i, int j) {
+    const int rd = PM::dof(i, g), c0 = PM::dof(j, 2 * t), c1 = PM::dof(j, 2 * t + 1);
+    double2 v;
+    v.x = (rd >= 0 && c0 >= 0) ? -sym(NEM + rd, NEM + c0) : ((i == j && g == 2 * t) ? -1.0 : 0.0);
+    v.y = (rd >= 0 && c1 >= 0) ? -sym(NEM + rd, NEM + c1) : ((i == j && g == 2 * t + 1) ? -1.0 : 0.0);
+    return v;
+  };
+  if constexpr (ALIAS) {
+    double2 a0[G::NT];
+#pragma unroll
+    for (int i = 0; i < NP; ++i)
+#pragma unroll
+      for (int j = 0; j <= i; ++j) a0[G::q(i, j)] = soo_tile(i, j);
+    __syncwarp();                          // every lane holds its S_co and S_oo entries
+#pragma unroll
+    for (int q = 0; q < G::NT; ++q) *reinterpret_cast<double2*>(Tl + q * 64) = a0[q];
+  } else {
+#pragma unroll
+    for (int i = 0; i < NP; ++i)
+#pragma unroll
+      for (int j = 0; j <= i; ++j) *reinterpret_cast<double2*>(Tl + G::q(i, j) * 64) = soo_tile(i, j);
+  }
+  double2 it[NP][NP];
+  int bad = 0;
+  sweep<NP, NCB, true, SY, RS, HALF>(Tl, bt, it, bad, sync);
+
+  // products that contract over the last pivot tile take one m8n8k4 step when
+  // its odd slots are padding
+  auto mma_p = [&](double2& o, double2 x, double2 y, int ktile) {
+    if (HALF && ktile == NP - 1) mma_xyt_even(o, x, y);
+    else mma_xyt(o, x, y);
+  };
+  if constexpr (!SDLAST) {
+  // ---- Sd_T = S_cc - W^T W (lower tiles), S_cc loaded ahead of each chain
+#pragma unroll
+  for (int c = 0; c < NCB; ++c) {
+    const int row = 8 * c + g, a = cpl_local<K>(row);
+#pragma unroll
+    for (int d = 0; d <= c; ++d) {
+      const int col = 8 * d + 2 * t;
+      double s0 = 0.0, s1 = 0.0;
+      if (row < NC) {
+        if (col <= row) s0 = sym(a, cpl_local<K>(col));
+        if (col + 1 <= row) s1 = sym(a, cpl_local<K>(col + 1));
+      }
+      double2 o = make_double2(0.0, 0.0);
+#pragma unroll
+      for (int j = 0; j < NP; ++j) mma_p(o, bt[c][j], bt[d][j], j);
+      if (row < NC) {
+        if (col <= row) so[pk(row, col)] = s0 - o.x;
+        if (col + 1 <= row) so[pk(row, col + 1)] = s1 - o.y;
+      }
+    }
+  }
+  }
+  // ---- X = L^-T W (row tile I: sum over I' >= I), row-major n_int x ncpl
+#pragma unroll
+  for (int I = 0; I < NP; ++I) {
+    const int row = PM::dof(I, g);
+#pragma unroll
+    for (int c = 0; c < NCB; ++c) {
+      double2 o = make_double2(0.0, 0.0);
+#pragma unroll
+      for (int Ip = I; Ip < NP; ++Ip) mma_p(o, it[I][Ip], bt[c][Ip], Ip);
+      const int col = 8 * c + 2 * t;
+      if (row >= 0) {
+        if constexpr (NC % 2 == 0) {
+          if (col < NC) *reinterpret_cast<double2*>(xo + row * NC + col) = o;
+        } else {
+          if (col < NC) xo[row * NC + col] = o.x;
+          if (col + 1 < NC) xo[row * NC + col + 1] = o.y;
+        }
+      }
+    }
+  }
+  // ---- S_oo^-1 = L^-T L^-1 (lower packed)
+#pragma unroll
+  for (int I = 0; I < NP; ++I) {
+    const int row = PM::dof(I, g);
+#pragma unroll
+    for (int Iq = 0; Iq <= I; ++Iq) {
+      double2 o = make_double2(0.0, 0.0);
+#pragma unroll
+      for (int Ip = I; Ip < NP; ++Ip) mma_p(o, it[I][Ip], it[Iq][Ip], Ip);
+      const int c0 = PM::dof(Iq, 2 * t), c1 = PM::dof(Iq, 2 * t + 1);
+      if (row >= 0) {
+        if (c0 >= 0 && c0 <= row) xo[L::x_len + pk(row, c0)] = o.x;
+        if (c1 >= 0 && c1 <= row) xo[L::x_len + pk(row, c1)] = o.y;
+      }
+    }
+  }
+  // ---- SDLAST (S_T in global memory): Sd_T = S_cc - W^T W last: `it` is
+  // dead by now, and the S_cc entries of tile row c + 1 are requested before
+  // the DMMA chains of row c (a single chain, ~260 clk, does not cover an L2
+  // round trip).  With S_T in shared memory (fused phase D) Sd_T first is
+  // 1.5% faster.
+  if constexpr (SDLAST) {
+    double2 cur[NCB], nxt[NCB];
+    auto load_row = [&](int c, double2 (&dst)[NCB]) {
+      const int row = 8 * c + g, a = cpl_local<K>(row);
+#pragma unroll
+      for (int d = 0; d < NCB; ++d) {
+        if (d > c) continue;
+        const int col = 8 * d + 2 * t;
+        double2 v = make_double2(0.0, 0.0);
+        if (row < NC) {
+          if (col <= row) v.x = sym(a, cpl_local<K>(col));
+          if (col + 1 <= row) v.y = sym(a, cpl_local<K>(col + 1));
+        }
+        dst[d] = v;
+      }
+    };
+    load_row(0, cur);
+#pragma unroll
+    for (int c = 0; c < NCB; ++c) {
+      if (c + 1 < NCB) load_row(c + 1, nxt);
+      const int row = 8 * c + g;
+#pragma unroll
+      for (int d = 0; d <= c; ++d) {
+        double2 o = make_double2(0.0, 0.0);
+#pragma unroll
+        for (int j = 0; j < NP; ++j) mma_p(o, bt[c][j], bt[d][j], j);
         const int col = 8 * d + 2 * t;
         if (row < NC) {
           if (col <= row) so[pk(row, col)] = cur[d].x - o.x;

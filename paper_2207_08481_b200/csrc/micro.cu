@@ -470,30 +470,42 @@ __global__ void __launch_bounds__(32 * WPB, MINB)
     }
     const double* Ae = A + e * LA;
     const double* Be = B + e * (int64_t)(NS * NC);
+    // pivot dofs by tile slot (dsr::PivMap: n = 60 puts the four dofs of the
+    // last tile on its even slots, so products over that tile take one DMMA)
+    using PM = dsr::PivMap<NS>;
+    auto asym = [&](int r, int c) { return __ldg(Ae + (r >= c ? pk(r, c) : pk(c, r))); };
 #pragma unroll
     for (int i = 0; i < NP; ++i)
 #pragma unroll
       for (int j = 0; j <= i; ++j) {
-        const int r = 8 * i + g, c0 = 8 * j + 2 * t;
-        double2 v;
-        v.x = (r < NS && c0 < NS) ? -__ldg(Ae + (r >= c0 ? pk(r, c0) : pk(c0, r))) : (r == c0 ? -1.0 : 0.0);
-        v.y = (r < NS && c0 + 1 < NS) ? -__ldg(Ae + (r >= c0 + 1 ? pk(r, c0 + 1) : pk(c0 + 1, r)))
-                                      : (r == c0 + 1 ? -1.0 : 0.0);   // the slots hold -A
+        const int rd = PM::dof(i, g), c0 = PM::dof(j, 2 * t), c1 = PM::dof(j, 2 * t + 1);
+        double2 v;   // the slots hold -A (padding: -1 on the diagonal)
+        v.x = (rd >= 0 && c0 >= 0) ? -asym(rd, c0) : ((i == j && g == 2 * t) ? -1.0 : 0.0);
+        v.y = (rd >= 0 && c1 >= 0) ? -asym(rd, c1) : ((i == j && g == 2 * t + 1) ? -1.0 : 0.0);
         *reinterpret_cast<double2*>(Tl + G::q(i, j) * 64) = v;
       }
-    double2 bt[NCB][NP];
+    double2 bt[NCB][NP];   // B^T tile (c, i): lane (g, t) gets B[dof(i, 2t + s)][8c + g]
 #pragma unroll
     for (int c = 0; c < NCB; ++c)
 #pragma unroll
-      for (int i = 0; i < NP; ++i) bt[c][i] = load_bt<NS, NC>(Be, c, i);
+      for (int i = 0; i < NP; ++i) {
+        const int col = 8 * c + g, r0 = PM::dof(i, 2 * t), r1 = PM::dof(i, 2 * t + 1);
+        double2 v = make_double2(0.0, 0.0);
+        if (col < NC) {
+          if (r0 >= 0) v.x = __ldg(Be + r0 * NC + col);
+          if (r1 >= 0) v.y = __ldg(Be + r1 * NC + col);
+        }
+        bt[c][i] = v;
+      }
     int bad = 0;
     double2 none[1][1];
     if constexpr (PAIR == 1)
-      dsr::sweep<NP, NCB, false>(Tl, bt, none, bad, PairSync{1 + (warp & 3)});
+      dsr::sweep<NP, NCB, false, PairSync, false, PM::HALF>(Tl, bt, none, bad, PairSync{1 + (warp & 3)});
     else if constexpr (PAIR == 2)
-      dsr::sweep<NP, NCB, false>(Tl, bt, none, bad, dsr::PairSync0{1 + (warp & 3)});
+      dsr::sweep<NP, NCB, false, dsr::PairSync0, false, PM::HALF>(Tl, bt, none, bad,
+                                                                 dsr::PairSync0{1 + (warp & 3)});
     else
-      dsr::sweep<NP, NCB, false>(Tl, bt, none, bad);
+      dsr::sweep<NP, NCB, false, dsr::NoSync, false, PM::HALF>(Tl, bt, none, bad);
     if (!live) continue;
     double* Se = S + e * (int64_t)(NC * (NC + 1) / 2);
 #pragma unroll
@@ -503,7 +515,10 @@ __global__ void __launch_bounds__(32 * WPB, MINB)
       for (int d = 0; d <= c; ++d) {
         double2 o = make_double2(0.0, 0.0);
 #pragma unroll
-        for (int j = 0; j < NP; ++j) dsr::mma_xyt(o, bt[c][j], bt[d][j]);
+        for (int j = 0; j < NP; ++j) {
+          if (PM::HALF && j == NP - 1) dsr::mma_xyt_even(o, bt[c][j], bt[d][j]);
+          else dsr::mma_xyt(o, bt[c][j], bt[d][j]);
+        }
         const int col = 8 * d + 2 * t;
         if (row < NC) {
           if (col <= row) Se[row * (row + 1) / 2 + col] = o.x;
