@@ -799,6 +799,12 @@ MCS_API int mcs_condense_fused(int k, int64_t nt, const double* W, int nwgt, con
 }
 
 #ifdef MCS_FUSED_PROF
+extern "C" __attribute__((visibility("default"))) int fz_prof_gen(int k, int64_t nt, const double* W, int nwgt,
+                                                                  const double* tables, double* S_packed,
+                                                                  int* info, void* stream) {
+  return mcs::launch_condense_fused_big(k, nt, W, nwgt, tables, S_packed, info,
+                                        static_cast<cudaStream_t>(stream));
+}
 extern "C" __attribute__((visibility("default"))) void fz_prof_read(unsigned long long* out) {
   cudaMemcpyFromSymbol(out, mcs::g_fz_prof, 8 * sizeof(unsigned long long));
 }

@@ -29,6 +29,8 @@ if not os.path.exists(so):
 lib = ctypes.CDLL(so)
 P, I, L = ctypes.c_void_p, ctypes.c_int, ctypes.c_int64
 lib.mcs_condense_fused.argtypes = [I, L, P, I, P, P, P, P, P, P]
+lib.fz_prof_gen.argtypes = [I, L, P, I, P, P, P, P]
+GEN = os.environ.get("GEN") == "1"   # k = 5, 6: the condensation alone (mcs_condense_gen's kernel)
 CFG = int(os.environ.get("CFG", "2"))
 prob = baseline_config(CFG)
 fes = FeSystem(prob.mesh, prob.regions, prob.k)
@@ -41,12 +43,15 @@ Sd = torch.empty((nt, _abi.call("mcs_sd_stride", k)), dtype=torch.float64, devic
 info = torch.empty(nt, dtype=torch.int32, device="cuda")
 args = (k, nt, W.data_ptr(), W.shape[1], tab.data_ptr(), ST.data_ptr(), ext.data_ptr(),
         Sd.data_ptr(), info.data_ptr(), torch.cuda.current_stream().cuda_stream)
-lib.mcs_condense_fused(*args)
+gargs = (k, nt, W.data_ptr(), W.shape[1], tab.data_ptr(), ST.data_ptr(), info.data_ptr(),
+         torch.cuda.current_stream().cuda_stream)
+run = (lambda: lib.fz_prof_gen(*gargs)) if GEN else (lambda: lib.mcs_condense_fused(*args))
+run()
 torch.cuda.synchronize()
 ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
 ev0.record()
 for _ in range(10):
-    lib.mcs_condense_fused(*args)
+    run()
 ev1.record()
 torch.cuda.synchronize()
 print(f"cfg{CFG} k={k} WPB {WPB}: {ev0.elapsed_time(ev1) / 10:.4f} ms per launch (with clock accounting)")
