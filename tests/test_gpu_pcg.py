@@ -180,3 +180,24 @@ def test_multifrontal_coarse_solve_exact(cuda, cfg, n, leaf):
     assert rel(cs.solve(b), ref) <= 1e-12
     # deterministic
     assert np.array_equal(cs.solve(b), cs.solve(b))
+
+
+@pytest.mark.parametrize("spec", ["1-2", "1-3", "0-1,2-3"])
+def test_multifrontal_coarse_solve_exact_with_amalgamated_supernodes(cuda, monkeypatch, spec):
+    """Supernode amalgamation of the separator tree (coarse.AMALG): merged
+    fronts have more than two children, the level kernels gather one source
+    slot per child; the solve stays exact and deterministic."""
+    import scipy.sparse.linalg as spla
+    from paper_2207_08481_b200 import coarse as co
+    prob = baseline_config(2, 40)
+    fes = FeSystem(prob.mesh, prob.regions, prob.k)
+    A = pc.coarse_matrix(fes, prob.nu)
+    xy = fes.mesh.vertices[np.flatnonzero(fes.dof_vbar.is_free) // 2]
+    monkeypatch.setattr(co, "AMALG", spec)
+    monkeypatch.setattr(co, "TOP_MAX", 300)          # keep several levels below the dense top
+    cs = co.factorize_coarse(A, xy, kind="multifrontal", leaf=32)
+    assert max(len(nd.children) for nd in cs.data.nodes) > 2
+    b = np.random.default_rng(2).standard_normal(A.shape[0])
+    ref = spla.spsolve(A.tocsc(), b)
+    assert rel(cs.solve(b), ref) <= 1e-12
+    assert np.array_equal(cs.solve(b), cs.solve(b))
