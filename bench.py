@@ -296,7 +296,7 @@ def run_config(args, cfg, dev, world, steps, warmup, l2_flush, peaks, full=True)
             ev.record(stream)
         _abi.call("mcs_double_schur", k, b - a, _abi.ptr(ST[a:b]), _abi.ptr(ext[a:b]),
                   _abi.ptr(Sd[a:b]), _abi.ptr(info[a:b]), st)
-        return 2
+        return 3      # lane-table kernel + condensation + double Schur
 
     def step(ev=None):
         if ev:
